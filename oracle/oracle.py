@@ -1,0 +1,220 @@
+"""oracle/oracle.py — TEST INFRASTRUCTURE ONLY.
+
+ctypes front-end for the two CPU checkers built by oracle/Makefile:
+
+* ``Ref``  — oracle/_ref/liblps_ref.so: the unmodified reference library
+  (/root/reference/proj/src/*.cpp) behind oracle/ref_shim.cpp.
+* ``Port`` — oracle/_build/liblps_port.so: our plain-C restatement
+  (oracle/lps_oracle.c).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs may import this module. The product package never
+does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REF_SO = os.path.join(HERE, "_ref", "liblps_ref.so")
+PORT_SO = os.path.join(HERE, "_build", "liblps_port.so")
+
+STATUS_NAMES = {0: "Optimal", 1: "Unbounded", 2: "Infeasible", 3: "IterationLimit",
+                -1: "Error", -2: "PivotTooSmall"}
+
+
+class Config(C.Structure):
+    _fields_ = [("opt_tol", C.c_double), ("pivot_tol", C.c_double), ("feas_tol", C.c_double),
+                ("ratio_tie_tol", C.c_double), ("max_iter", C.c_long), ("anticycle", C.c_int),
+                ("workers", C.c_int), ("kernel", C.c_int)]
+
+
+class TraceEntry(C.Structure):
+    _fields_ = [("iteration", C.c_long), ("phase", C.c_int), ("row", C.c_int),
+                ("leaving", C.c_int), ("entering", C.c_int), ("objective", C.c_double)]
+
+
+class Result(C.Structure):
+    _fields_ = [("status", C.c_int), ("objective", C.c_double),
+                ("iterations_phase1", C.c_long), ("iterations_phase2", C.c_long),
+                ("total_seconds", C.c_double), ("tpi_seconds", C.c_double),
+                ("trace_len", C.c_long)]
+
+
+TRACE_DTYPE = np.dtype([("iteration", np.int64), ("phase", np.int32), ("row", np.int32),
+                        ("leaving", np.int32), ("entering", np.int32),
+                        ("objective", np.float64)])
+assert TRACE_DTYPE.itemsize == C.sizeof(TraceEntry)
+
+
+@dataclass
+class LP:
+    """Mirror of lps::StandardFormLP (lp_model.hpp:49-60)."""
+    m: int
+    n_total: int
+    A: np.ndarray          # (m, n_total) float64, row-major
+    b: np.ndarray          # (m,)
+    c: np.ndarray          # (n_total,)
+    col_kind: np.ndarray   # (n_total,) uint8: 0 structural, 1 slack
+    objective_sign: float = 1.0
+    objective_constant: float = 0.0
+    name: str = ""
+
+
+@dataclass
+class SolveOut:
+    status: int
+    objective: float
+    iterations_phase1: int
+    iterations_phase2: int
+    total_seconds: float
+    tpi_seconds: float
+    x: np.ndarray
+    trace: np.ndarray = field(default_factory=lambda: np.zeros(0, TRACE_DTYPE))
+    trace_len: int = 0
+
+    @property
+    def status_name(self) -> str:
+        return STATUS_NAMES.get(self.status, str(self.status))
+
+
+def make_config(opt_tol=1e-7, pivot_tol=1e-9, feas_tol=1e-7, ratio_tie_tol=1e-9, max_iter=0,
+                anticycle="tabu", workers=1, kernel="cached") -> Config:
+    return Config(opt_tol, pivot_tol, feas_tol, ratio_tie_tol, int(max_iter),
+                  1 if anticycle == "none" else 0, int(workers), 1 if kernel == "naive" else 0)
+
+
+def build(ref: bool = True) -> None:
+    """Builds the checkers (make; the reference half only if its sources exist)."""
+    targets = ["port"]
+    if ref and os.path.isdir("/root/reference/proj/src"):
+        targets.append("ref")
+    subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
+
+
+def _ptr(a, t):
+    return a.ctypes.data_as(C.POINTER(t))
+
+
+class _Lib:
+    def __init__(self, path: str, prefix: str):
+        if not os.path.exists(path):
+            raise FileNotFoundError(path)
+        self.lib = C.CDLL(path)
+        self.prefix = prefix
+        solve = getattr(self.lib, prefix + "solve")
+        solve.restype = C.c_int
+        solve.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                          C.POINTER(C.c_double), C.POINTER(C.c_uint8), C.POINTER(Config),
+                          C.POINTER(Result), C.POINTER(C.c_double), C.c_void_p, C.c_long]
+        self._solve = solve
+
+    def solve(self, lp: LP, cfg: Config | None = None, trace_cap: int = 1 << 20,
+              **kw) -> SolveOut:
+        cfg = cfg or make_config(**kw)
+        A = np.ascontiguousarray(lp.A, dtype=np.float64)
+        b = np.ascontiguousarray(lp.b, dtype=np.float64)
+        c = np.ascontiguousarray(lp.c, dtype=np.float64)
+        ck = np.ascontiguousarray(lp.col_kind, dtype=np.uint8)
+        x = np.zeros(lp.n_total, np.float64)
+        tr = np.zeros(max(trace_cap, 0), TRACE_DTYPE)
+        res = Result()
+        rc = self._solve(lp.m, lp.n_total, _ptr(A, C.c_double), _ptr(b, C.c_double),
+                         _ptr(c, C.c_double), _ptr(ck, C.c_uint8), C.byref(cfg), C.byref(res),
+                         _ptr(x, C.c_double), tr.ctypes.data if trace_cap > 0 else None,
+                         trace_cap)
+        if rc == 1:
+            raise RuntimeError(self.last_error())
+        n = min(res.trace_len, trace_cap)
+        return SolveOut(res.status, res.objective, res.iterations_phase1, res.iterations_phase2,
+                        res.total_seconds, res.tpi_seconds, x, tr[:n].copy(), res.trace_len)
+
+    def last_error(self) -> str:
+        return ""
+
+
+class Ref(_Lib):
+    """The compiled, unmodified reference (oracle/_ref)."""
+
+    def __init__(self, path: str = REF_SO):
+        super().__init__(path, "ref_")
+        L = self.lib
+        L.ref_lp_generate.restype = C.c_void_p
+        L.ref_lp_generate.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int]
+        L.ref_lp_from_mps.restype = C.c_void_p
+        L.ref_lp_from_mps.argtypes = [C.c_char_p]
+        L.ref_lp_dims.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.ref_lp_copy.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                  C.POINTER(C.c_double), C.POINTER(C.c_uint8),
+                                  C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.ref_lp_free.argtypes = [C.c_void_p]
+        L.ref_last_error.restype = C.c_char_p
+
+    def last_error(self) -> str:
+        return self.lib.ref_last_error().decode()
+
+    def _take(self, h, name="") -> LP:
+        if not h:
+            raise RuntimeError(self.last_error())
+        m, n = C.c_int(), C.c_int()
+        self.lib.ref_lp_dims(h, C.byref(m), C.byref(n))
+        m, n = m.value, n.value
+        A = np.zeros((m, n)); b = np.zeros(m); c = np.zeros(n)
+        ck = np.zeros(n, np.uint8)
+        sgn, const = C.c_double(), C.c_double()
+        self.lib.ref_lp_copy(h, _ptr(A, C.c_double), _ptr(b, C.c_double), _ptr(c, C.c_double),
+                             _ptr(ck, C.c_uint8), C.byref(sgn), C.byref(const))
+        self.lib.ref_lp_free(h)
+        return LP(m, n, A, b, c, ck, sgn.value, const.value, name)
+
+    def generate(self, rows: int, cols: int, seed: int = 1, form: int = 0,
+                 sparsity: int = 0) -> LP:
+        return self._take(self.lib.ref_lp_generate(rows, cols, sparsity, seed, form),
+                          f"{rows}_{cols}_f{form}_s{seed}")
+
+    def from_mps(self, path: str) -> LP:
+        return self._take(self.lib.ref_lp_from_mps(path.encode()),
+                          os.path.splitext(os.path.basename(path))[0])
+
+
+class Port(_Lib):
+    """Our plain-C restatement (oracle/lps_oracle.c)."""
+
+    def __init__(self, path: str = PORT_SO):
+        super().__init__(path, "lpo_")
+        L = self.lib
+        L.lpo_generate.restype = C.c_int
+        L.lpo_generate.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int,
+                                   C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                   C.POINTER(C.c_double), C.POINTER(C.c_uint8)]
+        L.lpo_generated_n_total.restype = C.c_int
+        L.lpo_generated_n_total.argtypes = [C.c_int, C.c_int, C.c_int]
+
+    def generate(self, rows: int, cols: int, seed: int = 1, form: int = 0,
+                 sparsity: int = 0) -> LP:
+        n = self.lib.lpo_generated_n_total(rows, cols, form)
+        A = np.zeros((rows, n)); b = np.zeros(rows); c = np.zeros(n)
+        ck = np.zeros(n, np.uint8)
+        rc = self.lib.lpo_generate(rows, cols, sparsity, seed, form, _ptr(A, C.c_double),
+                                   _ptr(b, C.c_double), _ptr(c, C.c_double), _ptr(ck, C.c_uint8))
+        if rc:
+            raise ValueError("lpo_generate: rows and cols must be positive")
+        return LP(rows, n, A, b, c, ck, -1.0 if form else 1.0, 0.0,
+                  f"{rows}_{cols}_f{form}_s{seed}")
+
+
+def save_lp(path: str, lp: LP) -> None:
+    np.savez_compressed(path, m=lp.m, n_total=lp.n_total, A=lp.A, b=lp.b, c=lp.c,
+                        col_kind=lp.col_kind, objective_sign=lp.objective_sign,
+                        objective_constant=lp.objective_constant, name=lp.name)
+
+
+def load_lp(path: str) -> LP:
+    z = np.load(path, allow_pickle=False)
+    return LP(int(z["m"]), int(z["n_total"]), z["A"], z["b"], z["c"], z["col_kind"],
+              float(z["objective_sign"]), float(z["objective_constant"]), str(z["name"]))
