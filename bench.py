@@ -1,0 +1,270 @@
+#!/usr/bin/env python
+"""Benchmark: simplex iterations/s on BASELINE.json's headline config.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+                    [--tto] [--no-cpu-baseline]
+
+A "step" is one pivot of the dense revised simplex (one pass of the hot path:
+ratio test, pivot row, pricing, fused update + FTRAN) on a synthetic LP from
+the reference's own generator (seed 1), resident in HBM. W warm-up pivots run
+first (untimed), then exactly K pivots are timed with CUDA events on the
+solver's stream. The working set (A: 1.0 GB, B^-1: 0.5 GB at m=8000) is far
+larger than the 126 MB L2, so no flush is needed between pivots.
+
+Prints ONE JSON line (rank 0). `--impl reference` times the reference's own
+CPU implementation (oracle/_ref, i.e. lps::two_phase_solve compiled from the
+unmodified reference sources) on the same LP with all host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE.json configs[0..4]
+    "c1": dict(rows=256, cols=512, form=1, seed=1, cpu_pivots=824,
+               label="C1 random dense LP m=256 n=512 (<= rows, maximize; slack start), seed 1"),
+    "c2": dict(rows=2000, cols=4000, form=0, seed=1, cpu_pivots=300,
+               label="C2 random dense LP m=2000 n=4000 (generator verbatim, equality rows), seed 1"),
+    "c3": dict(rows=8000, cols=16000, form=0, seed=1, cpu_pivots=60,
+               label="C3 random dense LP m=8000 n=16000 (generator verbatim, equality rows), seed 1"),
+    "c4": dict(rows=4000, cols=8000, form=2, seed=1, cpu_pivots=1,
+               label="C4 degenerate LP m=4000 n=8000 (<= rows, maximize, half the rows a_i - a_i+1 "
+                     "with b_i = 0), seed 1"),
+    "c5": dict(rows=24000, cols=48000, form=0, seed=1, cpu_pivots=5,
+               label="C5 random dense LP m=24000 n=48000 (generator verbatim), seed 1"),
+}
+METRIC = "simplex iterations/sec, dense LP m=8000"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def __enter__(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.device),
+                                          f"--query-gpu={self.Q}", "--format=csv,noheader,nounits"],
+                                         capture_output=True, text=True, timeout=5).stdout
+                    for line in out.strip().splitlines():
+                        self.rows.append([v.strip() for v in line.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 3 + k and r[3 + k].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def make_lp(cfg):
+    import paper_1803_04378_b200 as P
+    return P.generate(P.GenSpec(cfg["rows"], cfg["cols"], P.SparsityClass.dense, cfg["seed"],
+                                P.Form(cfg["form"])))
+
+
+def cpu_reference(lp, pivots: int, warmup: int = 0):
+    """Times the reference CPU solver (oracle/_ref if built, else the C port) on
+    the same LP: `pivots` pivots from the start, solve() clock only
+    (solver.cpp:332,363). Returns (value it/s, dict)."""
+    from oracle.oracle import LP, Port, Ref, make_config
+    cores = os.cpu_count() or 1
+    try:
+        impl, kind = Ref(), "reference"
+    except Exception:
+        impl, kind = Port(), "port"
+        cores = 1
+    olp = LP(lp.m, lp.n_total, lp.A, lp.b, lp.c, lp.col_kind)
+    if warmup:
+        impl.solve(olp, make_config(max_iter=warmup, workers=cores), trace_cap=0)
+    out = impl.solve(olp, make_config(max_iter=pivots, workers=cores), trace_cap=0)
+    n = out.iterations_phase1 + out.iterations_phase2
+    val = n / out.total_seconds if out.total_seconds > 0 else None
+    return val, dict(kind=kind, cores=cores, pivots=n, seconds=out.total_seconds,
+                     lib="oracle/_ref/liblps_ref.so (lps_core, unmodified reference sources)"
+                     if kind == "reference" else "oracle/_build/liblps_port.so")
+
+
+def run_reference_arm(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    lp = make_lp(cfg)
+    k = max(1, min(args.steps, cfg["cpu_pivots"] if args.steps > cfg["cpu_pivots"] else args.steps))
+    val, info = cpu_reference(lp, k, warmup=min(args.warmup, 3))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": "iterations/s",
+        "n_gpus": args.gpus, "steps": info["pivots"], "warmup": min(args.warmup, 3),
+        "ms_per_step": 1e3 * info["seconds"] / max(1, info["pivots"]),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator lps::generate, seed 1)",
+        "config": {"workload": cfg["label"], "m": lp.m, "n_total": lp.n_total,
+                   "sample": f"first {info['pivots']} pivots from the start basis"},
+        "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": info["cores"],
+                         "kind": info["kind"],
+                         "sample": f"first {info['pivots']} pivots of {cfg['label']}"},
+        "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import paper_1803_04378_b200 as P
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        raise SystemExit("multi-GPU sharding is not implemented yet (single-GPU solver only)")
+    device = 0
+    lp = make_lp(cfg)
+    W, K = args.warmup, args.steps
+
+    # ---- device-resident timing: W warm-up pivots, then K timed pivots
+    s = P.SimplexSolver(lp, P.SolverConfig(device=device, max_iter=W))
+    s.solve()
+    c0 = s.counters()
+    s.set_max_iter(W + K)
+    s.profile(True)
+    with ClockSampler(device) as clk:
+        rep = s.solve()
+    dev_ms = s.device_ms()
+    c1 = s.counters()
+    stats = s.profile_stats()
+    done = rep.iterations - W
+    s.close()
+    value = done / (dev_ms / 1e3)
+
+    # ---- roofline of the dominant kernel
+    peak, peak_kind = _peaks()
+    kern = {}
+    for name, st in stats.items():
+        if st["launches"] and st["ms"] > 0:
+            kern[name] = dict(launches=st["launches"], ms_total=round(st["ms"], 4),
+                              us_per_launch=round(1e3 * st["ms"] / st["launches"], 3),
+                              gbs=round(st["bytes"] / (st["ms"] / 1e3) / 1e9, 1),
+                              share=None)
+    tot = sum(v["ms_total"] for v in kern.values()) or 1.0
+    for v in kern.values():
+        v["share"] = round(v["ms_total"] / tot, 4)
+    dom = max(kern, key=lambda k: kern[k]["ms_total"])
+    ach = kern[dom]["gbs"]
+    pivot_bytes = sum(stats[k]["bytes"] for k in stats) / max(1, done)
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_kind,
+                "per_pivot": {"algorithmic_bytes": pivot_bytes,
+                              "achieved_gbs": round(pivot_bytes * value / 1e9, 1),
+                              "frac": round(pivot_bytes * value / 1e9 / peak, 4)},
+                "kernels": kern}
+
+    # ---- end to end through the public API with host buffers
+    t0 = time.perf_counter()
+    s2 = P.SimplexSolver(lp, P.SolverConfig(device=device, max_iter=K))
+    rep2 = s2.solve()
+    x = rep2.x  # solve() already read x back (device -> host)
+    t1 = time.perf_counter()
+    cnt = s2.counters()
+    s2.close()
+    e2e_val = rep2.iterations / (t1 - t0)
+    e2e = {"value": e2e_val, "unit": "iterations/s",
+           "h2d_bytes_per_step": cnt["h2d_bytes"] / max(1, rep2.iterations),
+           "d2h_bytes_per_step": (cnt["d2h_bytes"] + 8 * len(x)) / max(1, rep2.iterations),
+           "includes": "lpsg_create (A upload from host), solve, x readback; "
+                       f"{rep2.iterations} pivots from the start basis"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": done,
+        "warmup": W, "ms_per_step": dev_ms / max(1, done), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference generator lps::generate, seed 1)",
+        "config": {"workload": cfg["label"], "m": lp.m, "n_total": lp.n_total,
+                   "pivots_timed": [W, W + done], "phase_at_end": s.phase() if False else None,
+                   "l2": "working set > L2 (A 8*m*n_total B, B^-1 8*m^2 B); no flush needed",
+                   "parallelism": f"single GPU"},
+        "roofline": roofline,
+        "e2e": e2e,
+        "gpu_launches": c1["kernel_launches"] - c0["kernel_launches"],
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        val, info = cpu_reference(lp, cfg["cpu_pivots"])
+        line["cpu_baseline"] = {"value": val, "unit": "iterations/s", "cores": info["cores"],
+                                "kind": info["kind"],
+                                "sample": f"first {info['pivots']} pivots of the same LP "
+                                          f"({info['seconds']:.2f} s, {info['lib']})"}
+    if args.tto:
+        t0 = time.perf_counter()
+        s3 = P.SimplexSolver(lp, P.SolverConfig(device=device))
+        rep3 = s3.solve()
+        t_dev = s3.device_ms()
+        s3.close()
+        line["time_to_optimal"] = {"status": rep3.status.name, "objective": rep3.objective,
+                                   "iterations": rep3.iterations, "device_s": t_dev / 1e3,
+                                   "wall_s": time.perf_counter() - t0}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tto", action="store_true", help="also time a full solve to optimality")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,182 @@
+/* include/lpsg.h — C ABI of the B200-native dense revised simplex ("lpsg").
+ *
+ * This is the drop-in boundary for the reference's solver entry points
+ * (/root/reference/proj/include/lps/solver.hpp). Plain pointers and sizes only;
+ * no torch or C++ types cross it. Every function returns an lpsg_status code
+ * (LPSG_OK on success) and leaves a thread-local message for lpsg_last_error().
+ * No exceptions cross the ABI; the C++ shim (include/lpsg.hpp) rethrows them as
+ * the reference's error types (errors.hpp:9-11, 58-64).
+ *
+ * Implementation: paper_1803_04378_b200/csrc/ (C++ host driver + sm_100a CUDA
+ * kernels). There is no CPU fallback: on a machine without a usable B200 every
+ * solver entry point fails with LPSG_CUDA_ERROR.
+ */
+#ifndef LPSG_H
+#define LPSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Error codes. Outcomes of a solve are lpsg_solve_status, not errors. */
+typedef enum {
+    LPSG_OK = 0,
+    LPSG_PIVOT_TOO_SMALL = 1, /* lps::PivotTooSmall (errors.hpp:58-60, solver.cpp:241-244) */
+    LPSG_CUDA_ERROR = 2,
+    LPSG_OUT_OF_MEMORY = 3,
+    LPSG_INVALID_ARGUMENT = 4,
+    LPSG_NCCL_ERROR = 5,
+    LPSG_EMPTY_PROBLEM = 6    /* lps::DegenerateSpec / EmptyProblem (errors.hpp:17-19,66-68) */
+} lpsg_status;
+
+/* lps::SolveStatus (solver.hpp:14), same order. */
+typedef enum {
+    LPSG_OPTIMAL = 0,
+    LPSG_UNBOUNDED = 1,
+    LPSG_INFEASIBLE = 2,
+    LPSG_ITERATION_LIMIT = 3
+} lpsg_solve_status;
+
+/* lps::ColKind (lp_model.hpp:22). */
+enum { LPSG_COL_STRUCTURAL = 0, LPSG_COL_SLACK = 1 };
+
+/* lps::StandardFormLP (lp_model.hpp:49-60): Min c.x s.t. A x = b, b >= 0, x >= 0.
+ * A is row-major m x n_total. Caller-owned; copied to the device by lpsg_create. */
+typedef struct {
+    int m;
+    int n_total;
+    const double* A;
+    const double* b;
+    const double* c;
+    const uint8_t* col_kind;
+} lpsg_problem;
+
+/* lps::SolverConfig (solver.hpp:34-45) plus device placement. memory_budget,
+ * kernel and workers select simulation behaviour in the reference
+ * (solver.hpp:41-43): accepted and ignored here (case_used is always in-core). */
+typedef struct {
+    double opt_tol;        /* 1e-7 */
+    double pivot_tol;      /* 1e-9 */
+    double feas_tol;       /* 1e-7 */
+    double ratio_tie_tol;  /* 1e-9, relative */
+    long max_iter;         /* 0 = 50 * (m + n_work)  (solver.cpp:64) */
+    int anticycle;         /* 0 tabu, 1 none (solver.hpp:16) */
+    int kernel;            /* ignored (0 cached, 1 naive) */
+    int workers;           /* ignored */
+    int device;            /* CUDA device ordinal, default 0 */
+    int batch;             /* pivots enqueued per host check (0 = auto) */
+    int use_graphs;        /* capture pivot batches in CUDA graphs (default 1) */
+    int reserved[6];
+} lpsg_config;
+
+/* lps::SolveReport (solver.hpp:47-57); x is fetched with lpsg_get_x. */
+typedef struct {
+    int status;             /* lpsg_solve_status */
+    double objective;       /* tableau T[0][m]; -inf unbounded, NaN infeasible (solver.cpp:366-377) */
+    long iterations_phase1;
+    long iterations_phase2;
+    double total_seconds;   /* solve() only, like solver.cpp:332,363 */
+    double tpi_seconds;     /* total / max(1, iterations) (solver.cpp:387-388) */
+    int case_used;          /* always 0 = in-core (tiled_engine.hpp:24) */
+} lpsg_report;
+
+/* One pivot, as the reference's IterationObserver sees it (solver.hpp:21-32,
+ * solver.cpp:264-275): phase, cumulative iteration, the basis row that
+ * changed, the variables that left / entered, and T[0][m] after the pivot. */
+typedef struct {
+    long iteration;
+    int phase;
+    int row;
+    int leaving;
+    int entering;
+    double objective;
+} lpsg_trace;
+
+typedef void (*lpsg_observer)(const lpsg_trace* pivot, void* user);
+
+typedef struct lpsg_solver lpsg_solver;
+
+/* ---- library ---------------------------------------------------------- */
+const char* lpsg_last_error(void);
+const char* lpsg_version(void);
+/* Number of CUDA devices usable by this library (0 when none). */
+int lpsg_device_count(void);
+void lpsg_config_default(lpsg_config* cfg);
+
+/* ---- solver lifecycle: replaces SimplexSolver::SimplexSolver (solver.cpp:24-77),
+ *      SimplexSolver::solve (solver.cpp:331-392) and two_phase_solve
+ *      (solver.hpp:173, solver.cpp:394-397). ---------------------------- */
+int lpsg_create(const lpsg_problem* lp, const lpsg_config* cfg, lpsg_solver** out);
+int lpsg_solve(lpsg_solver* s, lpsg_report* report);
+/* Standard-form point, artificials excluded (solver.cpp:378-383); n = n_total. */
+int lpsg_get_x(lpsg_solver* s, double* x, int n);
+void lpsg_destroy(lpsg_solver* s);
+/* One-shot: create + solve + x + destroy. x may be NULL. */
+int lpsg_two_phase_solve(const lpsg_problem* lp, const lpsg_config* cfg, lpsg_report* report,
+                         double* x);
+
+/* Per-pivot trace: observer (called on the caller thread, in pivot order,
+ * after each device batch) and/or a retained copy of the whole trace. */
+int lpsg_set_observer(lpsg_solver* s, lpsg_observer cb, void* user);
+int lpsg_keep_trace(lpsg_solver* s, int keep);
+int lpsg_get_trace(lpsg_solver* s, lpsg_trace* out, long cap, long* len);
+
+/* ---- step API: SimplexSolver's public steps (solver.hpp:79-168) ---------- */
+/* price (solver.cpp:79-129) */
+int lpsg_price(lpsg_solver* s, int* optimal, int* entering, double* reduced_cost);
+/* compute_direction (solver.cpp:131-136) */
+int lpsg_compute_direction(lpsg_solver* s, int entering, double reduced_cost);
+/* ratio_test (solver.cpp:138-162); candidates ascending, *ncand may exceed cap. */
+int lpsg_ratio_test(lpsg_solver* s, int* unbounded, double* theta, int* cand, int cap,
+                    int* ncand);
+/* select_leaving (solver.cpp:215-238), tabu + batched device lookahead. */
+int lpsg_select_leaving(lpsg_solver* s, const int* cand, int ncand, int entering, int* row);
+/* lookahead_score (solver.cpp:164-213) for each candidate row, batched. */
+int lpsg_lookahead_scores(lpsg_solver* s, const int* rows, int k, int entering, double* scores);
+/* pivot_update (solver.cpp:240-254); LPSG_PIVOT_TOO_SMALL when |y_rk| <= pivot_tol. */
+int lpsg_pivot_update(lpsg_solver* s, int leaving_row, int entering);
+
+/* Figure-1 tableau accessors (solver.hpp:139-151): row i of m+2 doubles
+ * (row 0 = [W | obj | d], row i>0 = [B^-1 row i-1 | b_bar | y]). */
+int lpsg_dims(lpsg_solver* s, int* m, int* n_total, int* n_work);
+int lpsg_read_row(lpsg_solver* s, int i, double* out);
+int lpsg_basis(lpsg_solver* s, int* basic, int m);
+int lpsg_phase(lpsg_solver* s);
+
+/* ---- measurement -------------------------------------------------------
+ * Budget for the next lpsg_solve call. A solve that stopped with
+ * LPSG_ITERATION_LIMIT resumes from the same state (the reference's solve() is
+ * single-shot; resuming is an extension used by the benchmark). */
+int lpsg_set_max_iter(lpsg_solver* s, long max_iter);
+
+/* Per-kernel CUDA-event timing of the pivot loop (enable resets the counters).
+ * algorithmic_bytes is what the reference's step must touch. */
+typedef struct {
+    const char* name;
+    long launches;
+    double milliseconds;
+    double algorithmic_bytes;
+} lpsg_kernel_stat;
+int lpsg_profile(lpsg_solver* s, int enable);
+int lpsg_profile_get(lpsg_solver* s, lpsg_kernel_stat* out, int cap, int* n);
+/* CUDA-event time of the last lpsg_solve call, measured on the solver's stream. */
+int lpsg_last_solve_device_ms(lpsg_solver* s, double* ms);
+/* Kernel launches issued and host<->device bytes moved since creation. */
+int lpsg_counters(lpsg_solver* s, long* kernel_launches, long long* h2d_bytes,
+                  long long* d2h_bytes);
+
+/* ---- input plumbing: lps::generate (generator.cpp:35-72) plus the
+ *      BASELINE.json input forms and canonicalize (lp_model.cpp:43-163) for
+ *      them. form: 0 equality (verbatim), 1 le + maximize, 2 degenerate.
+ *      sparsity: 0 dense, 1 S20, 2 S60. Arrays sized m x n_total etc. ----- */
+int lpsg_generated_n_total(int rows, int cols, int form);
+int lpsg_generate(int rows, int cols, int sparsity, uint64_t seed, int form, double* A,
+                  double* b, double* c, uint8_t* col_kind);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LPSG_H */

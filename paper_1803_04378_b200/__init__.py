@@ -1,0 +1,18 @@
+"""paper_1803_04378_b200 — B200-native dense revised simplex (lpsg).
+
+A drop-in for the iteration loop of the reference's C++ solver
+(/root/reference/proj/src/solver.cpp): the host API mirrors lps::two_phase_solve /
+lps::SimplexSolver, and all per-pivot work runs in hand-written sm_100a CUDA
+kernels behind the C ABI in include/lpsg.h.
+"""
+from .solver import (  # noqa: F401
+    Anticycle, ColKind, CudaError, DegenerateSpec, Error, Form, GenSpec, IterationView,
+    PivotTooSmall, SimplexSolver, SolveReport, SolverConfig, SolveStatus, SparsityClass,
+    StandardFormLP, TRACE_DTYPE, device_count, generate, two_phase_solve)
+
+__all__ = [
+    "Anticycle", "ColKind", "CudaError", "DegenerateSpec", "Error", "Form", "GenSpec",
+    "IterationView", "PivotTooSmall", "SimplexSolver", "SolveReport", "SolverConfig",
+    "SolveStatus", "SparsityClass", "StandardFormLP", "TRACE_DTYPE", "device_count",
+    "generate", "two_phase_solve",
+]

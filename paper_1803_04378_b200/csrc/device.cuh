@@ -1,0 +1,129 @@
+// device.cuh — device-side state and kernel launchers of the lpsg solver.
+//
+// HBM layout (SURVEY.md §7 "Kernel plan"):
+//   T      column-major (m+1) columns x ldT rows: columns 0..m-1 = B^-1, column m = b_bar.
+//          Element (i, j) of the reference's tableau row i+1 (solver.hpp:71-76) is
+//          T[j*ldT + i]. Row-owner threads therefore read coalesced along i.
+//   top    row 0 of the tableau: [W (m) | obj | d]  (m+2 doubles)
+//   Y      the pivot column y (tableau column m+1, rows 1..m)
+//   xrow   the pivot row divided by y_rk (m+2 doubles)
+//   A_cm   column-major copy of A (column j contiguous, m doubles) — FTRAN operand a_q
+//   A_nb   row-major m x ld_nb "nonbasic pricing matrix": slot s holds column slot2col[s];
+//          slots [0, n_scan) are exactly the nonbasic non-artificial columns
+//   ctl    control block; every per-pivot decision lives on the device so pivot
+//          batches run without host round trips.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lpsg {
+
+enum CtlStatus : int {
+    ST_RUNNING = 0,
+    ST_OPTIMAL = 1,
+    ST_UNBOUNDED = 2,
+    ST_TIE = 3,          // ratio test tied under tabu: host runs select_leaving
+    ST_ITER_LIMIT = 4,
+    ST_PIVOT_ERR = 5,    // |y_rk| <= pivot_tol
+    ST_HOLD = 6          // step API / phase boundary: kernels idle
+};
+
+struct LogEntry {
+    long long iteration;
+    int phase;
+    int row;
+    int leaving;
+    int entering;
+    double objective;
+};
+
+struct Ctl {
+    int status;
+    int pending;       // a pivot was committed; the tableau update is outstanding
+    int q;             // entering column (last pricing result)
+    int r;             // leaving row (ratio test / host)
+    double d;          // reduced cost of q
+    double theta;
+    int ncand;
+    int n_scan;        // active pricing slots
+    long long total_iter;
+    long long budget;
+    int phase;
+    int log_len;
+    int no_ftran;      // update without the fused FTRAN (drive-out, step API)
+    int upd_r;         // row of the pending update
+    int upd_q;         // column entering in the pending update
+    int any_ratio;
+    unsigned int ticket_price;
+    unsigned int ticket_update;
+    unsigned int ticket_misc;
+    int found;         // drive-out scan result
+    double found_red;
+    int pad[2];
+};
+
+struct Dev {
+    int m, n_total, n_work;
+    long long ldT;
+    long long ld_nb;
+    double* T;
+    double* top;
+    double* Y;
+    double* xrow;
+    const double* A_cm;
+    double* A_nb;
+    int* slot2col;
+    int* col2slot;
+    int* basic;
+    unsigned char* frozen;
+    const double* cost_p1;
+    const double* cost_true;
+    Ctl* ctl;
+    int* cand;
+    double* pz;
+    int* pj;
+    LogEntry* log;
+    int log_cap;
+    int num_sms;
+    double opt_tol, pivot_tol, feas_tol, ratio_tie_tol;
+    int anticycle;
+    int price_grid;
+    int update_grid;
+};
+
+// Lookahead (solver.cpp:164-213) batch buffers.
+struct LookaheadDev {
+    int K;            // candidates in this batch
+    int ldx;          // row pitch of X / Wp (>= m+1)
+    const int* rows;  // K candidate rows
+    double* X;        // K x ldx : candidate pivot rows divided by piv (B^-1 part + b_bar)
+    double* Wp;       // K x ldx : W' = W - d * X
+    double* Abest;    // K x m   : a_{best_k}
+    double* bz;       // K best z
+    int* bj;          // K best column
+    double* theta;    // K
+    double* score;    // K
+    double* part_z;   // partials
+    int* part_j;
+    double* part_t;
+    int nblk;         // partial blocks per candidate
+    int q;            // entering column
+    double d;         // entering reduced cost
+};
+
+// ---- launchers (kernels.cu) -------------------------------------------------
+void launch_init_tableau(const Dev& d, const double* b, cudaStream_t st);
+void launch_rebuild_top(const Dev& d, cudaStream_t st);
+void launch_price(const Dev& d, cudaStream_t st);
+void launch_update(const Dev& d, cudaStream_t st);
+void launch_ratio(const Dev& d, cudaStream_t st);
+void launch_pivot(const Dev& d, cudaStream_t st);
+void launch_transpose(const double* A_rm, double* A_cm, int m, int n, cudaStream_t st);
+void launch_build_nb_from(const Dev& d, const double* A_rm, int n_scan, cudaStream_t st);
+void launch_drive_scan(const Dev& d, int row, double* scratch, cudaStream_t st);
+void launch_lookahead(const Dev& d, LookaheadDev& la, cudaStream_t st);
+void launch_gather_row(const Dev& d, int i, double* out, cudaStream_t st);
+
+}  // namespace lpsg

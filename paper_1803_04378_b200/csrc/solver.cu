@@ -1,0 +1,971 @@
+// solver.cu — host driver of the lpsg dense revised simplex and its C ABI.
+//
+// The iteration loop of lps::SimplexSolver (solver.cpp:278-293) runs on the
+// device as a fused four-kernel chain per pivot:
+//
+//     k_ratio  -> k_pivot -> k_price(W_{t+1}) -> k_update(T_t -> T_{t+1}, Y_{t+1})
+//
+// Every decision (entering column, leaving row, optimality, unboundedness, the
+// iteration budget) is taken on the device and recorded in the control block,
+// so the host enqueues batches of pivots and only synchronises once per batch
+// to drain the pivot log (note_iteration's tabu bookkeeping and the observer).
+// Ratio-test ties under the tabu rule (select_leaving, solver.cpp:215-238) stop
+// the device chain; the host applies the tabu filter and scores the survivors
+// with the batched device lookahead, then resumes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <unordered_set>
+#include <vector>
+
+#include "device.cuh"
+#include "lpsg.h"
+
+namespace lpsg {
+
+namespace {
+thread_local std::string g_err;
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) {
+        const int code = e == cudaErrorMemoryAllocation ? LPSG_OUT_OF_MEMORY : LPSG_CUDA_ERROR;
+        cudaGetLastError();
+        throw Error(code, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+}
+#define CK(x) ck((x), #x)
+
+template <class T>
+T* dalloc(size_t n) {
+    void* p = nullptr;
+    CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+long long round_up(long long v, long long a) { return (v + a - 1) / a * a; }
+}  // namespace
+
+class Solver {
+public:
+    Solver(const lpsg_problem& lp, const lpsg_config& cfg);
+    ~Solver();
+
+    void solve(lpsg_report* rep);
+    void get_x(double* x, int n);
+
+    // step API (solver.hpp:79-168)
+    void step_price(int* optimal, int* entering, double* red);
+    void step_compute_direction(int entering, double red);
+    void step_ratio(int* unbounded, double* theta, std::vector<int>& cand);
+    int select_leaving(const std::vector<int>& cand, int entering);
+    void lookahead(const std::vector<int>& rows, int entering, std::vector<double>& scores);
+    void step_pivot(int r, int q);
+    void read_row(int i, double* out);
+
+    int m() const { return m_; }
+    int n_total() const { return n_total_; }
+    int n_work() const { return n_work_; }
+    int phase() const { return phase_; }
+    const std::vector<int>& basic() const { return basic_; }
+
+    lpsg_observer observer = nullptr;
+    void* observer_user = nullptr;
+    bool keep_trace = false;
+    std::vector<lpsg_trace> trace;
+
+private:
+    int run_phase();
+    void enter_phase2();
+    void drive_out_artificials();
+    void rebuild_top_row();
+    void pull(bool with_log);
+    void push();
+    void drain_log();
+    void note_pivot(const LogEntry& e);
+    void enqueue_pivots(int n);
+    double objective_value();
+
+    lpsg_config cfg_;
+    int m_, n_total_, n_art_ = 0, n_work_ = 0;
+    long long max_iter_ = 0;
+    int phase_ = 1;
+    long long total_iter_ = 0, phase_iter_[2] = {0, 0};
+    std::vector<int> basic_;
+    std::vector<char> frozen_;
+    std::unordered_map<int, std::unordered_set<int>> banned_;  // TabuState (solver.hpp:66-69)
+    double last_objective_ = 0.0;
+    int final_status_ = LPSG_ITERATION_LIMIT;
+    bool solved_ = false;
+    bool done_ = false;        // terminal status reached (not resumable)
+    long long n_scan_host_ = 0;
+
+    cudaStream_t st_ = nullptr;
+    Dev d_{};
+    Ctl* hctl_ = nullptr;       // pinned mirror of the control block
+    LogEntry* hlog_ = nullptr;  // pinned mirror of the pivot log
+    int* hone_ = nullptr;       // pinned constant 1 (stream-ordered flag writes)
+    double* scratch_ = nullptr;
+    double* cost_buf_ = nullptr;
+    int batch_ = 16;
+
+public:
+    // ---- counters and optional per-kernel CUDA-event profile
+    enum Kind { K_RATIO = 0, K_PIVOT, K_PRICE, K_UPDATE, K_OTHER, K_NUM };
+    struct KStat {
+        long launches = 0;
+        double ms = 0.0;
+        double bytes = 0.0;
+    };
+    KStat kstat[K_NUM];
+    long launches_total = 0;
+    double last_device_ms = 0.0;   // CUDA-event span of the last solve() on the solver stream
+    long long h2d_bytes = 0, d2h_bytes = 0;
+    void set_profile(bool on);
+    void set_max_iter(long long v);
+
+private:
+    bool prof_ = false;
+    std::vector<cudaEvent_t> ev_pool_;
+    struct EvRec {
+        int kind;
+        cudaEvent_t a, b;
+        double bytes;
+    };
+    std::vector<EvRec> ev_used_;
+    template <class F>
+    void L(int kind, double bytes, F&& f);
+    void flush_profile();
+    double bytes_of(int kind) const;
+};
+
+template <class F>
+void Solver::L(int kind, double bytes, F&& f) {
+    ++launches_total;
+    if (!prof_) {
+        f();
+        return;
+    }
+    if (ev_pool_.size() < 2) {
+        for (int k = 0; k < 64; ++k) {
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            ev_pool_.push_back(e);
+        }
+    }
+    EvRec r{kind, ev_pool_.back(), nullptr, bytes};
+    ev_pool_.pop_back();
+    r.b = ev_pool_.back();
+    ev_pool_.pop_back();
+    CK(cudaEventRecord(r.a, st_));
+    f();
+    CK(cudaEventRecord(r.b, st_));
+    ev_used_.push_back(r);
+}
+
+void Solver::flush_profile() {
+    for (auto& r : ev_used_) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, r.a, r.b));
+        kstat[r.kind].launches += 1;
+        kstat[r.kind].ms += ms;
+        kstat[r.kind].bytes += r.bytes;
+        ev_pool_.push_back(r.a);
+        ev_pool_.push_back(r.b);
+    }
+    ev_used_.clear();
+}
+
+// Algorithmic HBM bytes per launch: what the reference's step
+// must touch, not what the kernel happens to move.
+double Solver::bytes_of(int kind) const {
+    const double m = m_;
+    switch (kind) {
+        case K_PRICE: return 8.0 * m * (double)n_scan_host_ + 8.0 * m;       // A_nb slots + W
+        case K_UPDATE: return 16.0 * m * (m + 1.0) + 16.0 * m;               // T read+write, y, a_q
+        case K_RATIO: return 16.0 * m;                                       // y, b_bar
+        case K_PIVOT: return 8.0 * (m + 1.0) * 3.0 + 16.0 * m;               // row r, x, W; slot copy
+        default: return 0.0;
+    }
+}
+
+void Solver::set_profile(bool on) {
+    prof_ = on;
+    for (auto& k : kstat) k = KStat{};
+}
+
+void Solver::set_max_iter(long long v) {
+    max_iter_ = v > 0 ? v : 50LL * (m_ + n_work_);
+    hctl_->budget = max_iter_;
+    push();
+    CK(cudaStreamSynchronize(st_));
+}
+
+Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(lp.m), n_total_(lp.n_total) {
+    if (lp.m <= 0 || lp.n_total <= 0)
+        throw Error(LPSG_EMPTY_PROBLEM, "lpsg_create: problem has no rows or no columns");
+    if (!lp.A || !lp.b || !lp.c || !lp.col_kind)
+        throw Error(LPSG_INVALID_ARGUMENT, "lpsg_create: null problem array");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= 0) {
+        cudaGetLastError();
+        throw Error(LPSG_CUDA_ERROR, "lpsg_create: no CUDA device available (the solver has no CPU fallback)");
+    }
+    if (cfg.device < 0 || cfg.device >= ndev) throw Error(LPSG_INVALID_ARGUMENT, "lpsg_create: bad device ordinal");
+    CK(cudaSetDevice(cfg.device));
+    CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    const int m = m_, n = n_total_;
+
+    // ---- start basis (solver.cpp:27-39): first row i (ascending) with A[i][j] == 1.0
+    // for each slack column j (ascending), skipping rows already taken.
+    basic_.assign(m, -1);
+    {
+        std::vector<int> slack_cols;
+        for (int j = 0; j < n; ++j)
+            if (lp.col_kind[j] == LPSG_COL_SLACK) slack_cols.push_back(j);
+        if (!slack_cols.empty()) {
+            std::vector<std::vector<int>> ones(slack_cols.size());
+            for (int i = 0; i < m; ++i) {
+                const double* row = lp.A + (size_t)i * n;
+                for (size_t k = 0; k < slack_cols.size(); ++k)
+                    if (row[slack_cols[k]] == 1.0) ones[k].push_back(i);
+            }
+            for (size_t k = 0; k < slack_cols.size(); ++k)
+                for (int i : ones[k])
+                    if (basic_[i] < 0) {
+                        basic_[i] = slack_cols[k];
+                        break;
+                    }
+        }
+    }
+    for (int i = 0; i < m; ++i)
+        if (basic_[i] < 0) ++n_art_;
+    n_work_ = n + n_art_;
+    std::vector<double> cost(2 * (size_t)n_work_, 0.0);  // [c_phase1 | c_true]
+    for (int j = 0; j < n; ++j) cost[n_work_ + j] = lp.c[j];
+    {
+        int next = n;
+        for (int i = 0; i < m; ++i) {
+            if (basic_[i] >= 0) continue;
+            cost[next] = 1.0;  // c_phase1 of the artificial (solver.cpp:56)
+            basic_[i] = next++;
+        }
+    }
+    frozen_.assign(m, 0);
+    max_iter_ = cfg_.max_iter > 0 ? cfg_.max_iter : 50LL * (m + n_work_);
+    phase_ = n_art_ > 0 ? 1 : 2;
+
+    // ---- device layout
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, cfg.device));
+    d_.m = m;
+    d_.n_total = n;
+    d_.n_work = n_work_;
+    d_.ldT = round_up(m + 1, 32);
+    d_.ld_nb = round_up(n, 32) + 32;
+    d_.num_sms = prop.multiProcessorCount;
+    d_.opt_tol = cfg_.opt_tol;
+    d_.pivot_tol = cfg_.pivot_tol;
+    d_.feas_tol = cfg_.feas_tol;
+    d_.ratio_tie_tol = cfg_.ratio_tie_tol;
+    d_.anticycle = cfg_.anticycle;
+    d_.price_grid = 2 * d_.num_sms;
+    d_.update_grid = (m + 127) / 128;
+    batch_ = cfg_.batch > 0 ? cfg_.batch : (m <= 1024 ? 64 : m <= 4096 ? 16 : 4);
+    d_.log_cap = batch_ + 8;
+
+    d_.T = dalloc<double>((size_t)(m + 1) * d_.ldT);
+    d_.top = dalloc<double>(m + 2);
+    d_.Y = dalloc<double>(m);
+    d_.xrow = dalloc<double>(m + 2);
+    double* A_cm = dalloc<double>((size_t)n * m);
+    d_.A_cm = A_cm;
+    d_.A_nb = dalloc<double>((size_t)m * d_.ld_nb + 64);
+    d_.slot2col = dalloc<int>(d_.ld_nb);
+    d_.col2slot = dalloc<int>(n);
+    d_.basic = dalloc<int>(m);
+    d_.frozen = dalloc<unsigned char>(m);
+    cost_buf_ = dalloc<double>(2 * (size_t)n_work_);
+    d_.cost_p1 = cost_buf_;
+    d_.cost_true = cost_buf_ + n_work_;
+    d_.ctl = dalloc<Ctl>(1);
+    d_.cand = dalloc<int>(m);
+    d_.pz = dalloc<double>(d_.price_grid);
+    d_.pj = dalloc<int>(d_.price_grid);
+    d_.log = dalloc<LogEntry>(d_.log_cap);
+    scratch_ = dalloc<double>(m + 2);
+    CK(cudaMallocHost(&hctl_, sizeof(Ctl)));
+    CK(cudaMallocHost(&hlog_, sizeof(LogEntry) * d_.log_cap));
+    CK(cudaMallocHost(&hone_, sizeof(int)));
+    *hone_ = 1;
+
+    // ---- upload A once (row-major), derive the column-major copy and the
+    // nonbasic pricing matrix, then drop the staging copy.
+    std::vector<char> in_basis(n_work_, 0);
+    for (int i = 0; i < m; ++i) in_basis[basic_[i]] = 1;
+    std::vector<int> slot2col, col2slot(n, -1);
+    for (int j = 0; j < n; ++j)
+        if (!in_basis[j]) {
+            col2slot[j] = (int)slot2col.size();
+            slot2col.push_back(j);
+        }
+    const int n_scan = (int)slot2col.size();
+    n_scan_host_ = n_scan;
+    {
+        double* A_rm = dalloc<double>((size_t)m * n);
+        CK(cudaMemcpyAsync(A_rm, lp.A, sizeof(double) * (size_t)m * n, cudaMemcpyHostToDevice, st_));
+        launch_transpose(A_rm, A_cm, m, n, st_);
+        CK(cudaMemsetAsync(d_.slot2col, 0xff, sizeof(int) * d_.ld_nb, st_));
+        if (n_scan)
+            CK(cudaMemcpyAsync(d_.slot2col, slot2col.data(), sizeof(int) * n_scan, cudaMemcpyHostToDevice, st_));
+        CK(cudaMemcpyAsync(d_.col2slot, col2slot.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st_));
+        CK(cudaMemsetAsync(d_.A_nb, 0, sizeof(double) * ((size_t)m * d_.ld_nb + 64), st_));
+        launch_build_nb_from(d_, A_rm, n_scan, st_);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st_));
+        CK(cudaFree(A_rm));
+    }
+    CK(cudaMemcpyAsync(d_.basic, basic_.data(), sizeof(int) * m, cudaMemcpyHostToDevice, st_));
+    CK(cudaMemsetAsync(d_.frozen, 0, m, st_));
+    CK(cudaMemcpyAsync(cost_buf_, cost.data(), sizeof(double) * cost.size(), cudaMemcpyHostToDevice, st_));
+    CK(cudaMemsetAsync(d_.Y, 0, sizeof(double) * m, st_));
+    CK(cudaMemsetAsync(d_.top, 0, sizeof(double) * (m + 2), st_));
+
+    // ---- initial Figure-1 tableau B = I, b_bar = b (solver.cpp:66-72)
+    CK(cudaMemsetAsync(d_.T, 0, sizeof(double) * (size_t)(m + 1) * d_.ldT, st_));
+    CK(cudaMemcpyAsync(scratch_, lp.b, sizeof(double) * m, cudaMemcpyHostToDevice, st_));
+    launch_init_tableau(d_, scratch_, st_);
+
+    h2d_bytes += 8LL * m * n + 8LL * m + 8LL * (long long)cost.size() + 4LL * (n_scan + n + m);
+    std::memset(hctl_, 0, sizeof(Ctl));
+    hctl_->status = ST_HOLD;
+    hctl_->q = -1;
+    hctl_->r = -1;
+    hctl_->n_scan = n_scan;
+    hctl_->budget = max_iter_;
+    hctl_->phase = phase_;
+    hctl_->upd_r = -1;
+    hctl_->found = INT_MAX;
+    push();
+    rebuild_top_row();
+    last_objective_ = objective_value();
+}
+
+Solver::~Solver() {
+    if (st_) cudaStreamSynchronize(st_);
+    void* bufs[] = {d_.T, d_.top, d_.Y, d_.xrow, (void*)d_.A_cm, d_.A_nb, d_.slot2col, d_.col2slot,
+                    d_.basic, d_.frozen, cost_buf_, d_.ctl, d_.cand, d_.pz, d_.pj, d_.log, scratch_};
+    for (void* p : bufs)
+        if (p) cudaFree(p);
+    if (hctl_) cudaFreeHost(hctl_);
+    if (hlog_) cudaFreeHost(hlog_);
+    if (hone_) cudaFreeHost(hone_);
+    if (st_) cudaStreamDestroy(st_);
+}
+
+void Solver::push() {
+    CK(cudaMemcpyAsync(d_.ctl, hctl_, sizeof(Ctl), cudaMemcpyHostToDevice, st_));
+    h2d_bytes += sizeof(Ctl);
+}
+
+void Solver::pull(bool with_log) {
+    CK(cudaMemcpyAsync(hctl_, d_.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st_));
+    d2h_bytes += sizeof(Ctl);
+    if (with_log) {
+        CK(cudaMemcpyAsync(hlog_, d_.log, sizeof(LogEntry) * d_.log_cap, cudaMemcpyDeviceToHost, st_));
+        d2h_bytes += sizeof(LogEntry) * d_.log_cap;
+    }
+    CK(cudaStreamSynchronize(st_));
+    CK(cudaGetLastError());
+}
+
+double Solver::objective_value() {
+    double v = 0.0;
+    CK(cudaMemcpyAsync(&v, d_.top + m_, sizeof(double), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    return v;
+}
+
+void Solver::rebuild_top_row() {
+    launch_rebuild_top(d_, st_);
+    CK(cudaGetLastError());
+}
+
+// note_iteration (solver.cpp:256-276) for one logged pivot.
+void Solver::note_pivot(const LogEntry& e) {
+    ++total_iter_;
+    ++phase_iter_[phase_ - 1];
+    basic_[e.row] = e.entering;
+    if (e.leaving >= n_total_) --n_scan_host_;
+    if (last_objective_ - e.objective > cfg_.opt_tol) banned_.clear();
+    last_objective_ = e.objective;
+    lpsg_trace t{(long)e.iteration, e.phase, e.row, e.leaving, e.entering, e.objective};
+    if (keep_trace) trace.push_back(t);
+    if (observer) observer(&t, observer_user);
+}
+
+void Solver::drain_log() {
+    const int n = hctl_->log_len;
+    if (n > d_.log_cap) throw Error(LPSG_CUDA_ERROR, "pivot log overflow");
+    for (int k = 0; k < n; ++k) note_pivot(hlog_[k]);
+    hctl_->log_len = 0;
+}
+
+void Solver::enqueue_pivots(int n) {
+    for (int k = 0; k < n; ++k) {
+        L(K_RATIO, bytes_of(K_RATIO), [&] { launch_ratio(d_, st_); });
+        L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot(d_, st_); });
+        L(K_PRICE, bytes_of(K_PRICE), [&] { launch_price(d_, st_); });
+        L(K_UPDATE, bytes_of(K_UPDATE), [&] { launch_update(d_, st_); });
+    }
+    CK(cudaGetLastError());
+}
+
+// run_phase (solver.cpp:278-293) in the fused schedule.
+int Solver::run_phase() {
+    hctl_->status = ST_RUNNING;
+    hctl_->pending = 0;
+    hctl_->no_ftran = 0;
+    hctl_->log_len = 0;
+    hctl_->phase = phase_;
+    push();
+    L(K_PRICE, bytes_of(K_PRICE), [&] { launch_price(d_, st_); });  // price(W_t), first pivot of the phase
+    L(K_OTHER, 8.0 * m_ * (m_ + 1.0), [&] { launch_update(d_, st_); });  // standalone FTRAN (pending == 0)
+    CK(cudaGetLastError());
+    for (;;) {
+        enqueue_pivots(batch_);
+        pull(true);
+        if (prof_) flush_profile();
+        drain_log();
+        const int st = hctl_->status;
+        if (st == ST_RUNNING) {
+            push();
+            continue;
+        }
+        if (st == ST_TIE) {
+            std::vector<int> cand(hctl_->ncand);
+            CK(cudaMemcpy(cand.data(), d_.cand, sizeof(int) * cand.size(), cudaMemcpyDeviceToHost));
+            const int r = select_leaving(cand, hctl_->q);
+            hctl_->r = r;
+            hctl_->status = ST_RUNNING;
+            push();
+            L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot(d_, st_); });
+            L(K_PRICE, bytes_of(K_PRICE), [&] { launch_price(d_, st_); });
+            L(K_UPDATE, bytes_of(K_UPDATE), [&] { launch_update(d_, st_); });
+            continue;
+        }
+        if (st == ST_PIVOT_ERR) throw Error(LPSG_PIVOT_TOO_SMALL, "pivot element below pivot_tol");
+        if (st == ST_OPTIMAL) return LPSG_OPTIMAL;
+        if (st == ST_UNBOUNDED) return LPSG_UNBOUNDED;
+        if (st == ST_ITER_LIMIT) return LPSG_ITERATION_LIMIT;
+        throw Error(LPSG_CUDA_ERROR, "unexpected control status " + std::to_string(st));
+    }
+}
+
+// select_leaving (solver.cpp:215-238)
+int Solver::select_leaving(const std::vector<int>& cand, int entering) {
+    if (cand.size() == 1) return cand.front();
+    if (cfg_.anticycle == 1) return cand.front();
+    auto& banned = banned_[entering];
+    std::vector<int> survivors;
+    for (int r : cand)
+        if (!banned.count(basic_[r])) survivors.push_back(r);
+    if (survivors.empty()) survivors = cand;  // aspiration override
+    int chosen = survivors.front();
+    if (survivors.size() > 1) {
+        std::vector<double> scores;
+        lookahead(survivors, entering, scores);
+        double best = -1.0;
+        for (size_t k = 0; k < survivors.size(); ++k)
+            if (scores[k] > best) {
+                best = scores[k];
+                chosen = survivors[k];
+            }
+    }
+    banned.insert(basic_[chosen]);
+    return chosen;
+}
+
+// lookahead_score (solver.cpp:164-213) for every row in `rows`, batched on the device.
+void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<double>& scores) {
+    const int K = (int)rows.size();
+    scores.assign(K, 0.0);
+    if (K == 0) return;
+    const int m = m_;
+    const int ldx = (int)round_up(m + 1, 32);
+    const size_t per = (size_t)2 * ldx * sizeof(double);
+    const int kmax = (int)std::max<size_t>(1, std::min<size_t>(4096, ((size_t)2 << 30) / per));
+    const int kb = std::min(K, kmax);
+    LookaheadDev la{};
+    la.ldx = ldx;
+    la.q = entering;
+    la.nblk = (int)std::min<long long>(64, std::max<long long>((hctl_->n_scan + 255) / 256, (m + 127) / 128));
+    la.nblk = std::max(la.nblk, 1);
+    int* rows_d = dalloc<int>(kb);
+    la.rows = rows_d;
+    la.X = dalloc<double>((size_t)kb * ldx);
+    la.Wp = dalloc<double>((size_t)kb * ldx);
+    la.bz = dalloc<double>(kb);
+    la.bj = dalloc<int>(kb);
+    la.theta = dalloc<double>(kb);
+    la.score = dalloc<double>(kb);
+    la.part_z = dalloc<double>((size_t)kb * la.nblk);
+    la.part_j = dalloc<int>((size_t)kb * la.nblk);
+    la.part_t = dalloc<double>((size_t)kb * la.nblk);
+    for (int k0 = 0; k0 < K; k0 += kb) {
+        la.K = std::min(kb, K - k0);
+        CK(cudaMemcpyAsync(rows_d, rows.data() + k0, sizeof(int) * la.K, cudaMemcpyHostToDevice, st_));
+        launch_lookahead(d_, la, st_);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(scores.data() + k0, la.score, sizeof(double) * la.K, cudaMemcpyDeviceToHost, st_));
+        CK(cudaStreamSynchronize(st_));
+    }
+    void* bufs[] = {rows_d, la.X, la.Wp, la.bz, la.bj, la.theta, la.score, la.part_z, la.part_j, la.part_t};
+    for (void* p : bufs) cudaFree(p);
+}
+
+// drive_out_artificials (solver.cpp:295-316)
+void Solver::drive_out_artificials() {
+    for (int i = 0; i < m_; ++i) {
+        if (basic_[i] < n_total_) continue;
+        hctl_->found = INT_MAX;
+        hctl_->status = ST_HOLD;
+        push();
+        launch_drive_scan(d_, i, scratch_, st_);
+        CK(cudaGetLastError());
+        pull(false);
+        const int found = hctl_->found;
+        if (found < 0) {
+            frozen_[i] = 1;
+            const unsigned char one = 1;
+            CK(cudaMemcpy(d_.frozen + i, &one, 1, cudaMemcpyHostToDevice));
+            continue;
+        }
+        // compute_direction(found, red) then pivot_update(i, found), unfused
+        hctl_->q = found;
+        hctl_->d = hctl_->found_red;
+        hctl_->r = i;
+        hctl_->status = ST_RUNNING;
+        hctl_->pending = 0;
+        hctl_->no_ftran = 0;
+        hctl_->log_len = 0;
+        push();
+        launch_update(d_, st_);  // FTRAN only
+        launch_pivot(d_, st_);
+        CK(cudaMemcpyAsync(&d_.ctl->no_ftran, hone_, sizeof(int), cudaMemcpyHostToDevice, st_));
+        launch_update(d_, st_);  // update only
+        CK(cudaGetLastError());
+        pull(true);
+        if (hctl_->status == ST_PIVOT_ERR) throw Error(LPSG_PIVOT_TOO_SMALL, "pivot element below pivot_tol");
+        drain_log();
+        hctl_->no_ftran = 0;
+        hctl_->status = ST_HOLD;
+        push();
+    }
+}
+
+void Solver::enter_phase2() {
+    phase_ = 2;
+    hctl_->phase = 2;
+    hctl_->status = ST_HOLD;
+    push();
+    rebuild_top_row();
+    banned_.clear();
+    last_objective_ = objective_value();
+}
+
+// SimplexSolver::solve (solver.cpp:331-392). Resumable: a solve stopped by the
+// iteration budget continues from the same state after set_max_iter (the
+// benchmark uses this to time K pivots after W warm-up pivots); any other
+// outcome is final.
+void Solver::solve(lpsg_report* rep) {
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st_));
+    const double t0 = now_s();
+    int status = final_status_;
+    if (!done_) {
+        status = LPSG_OPTIMAL;
+        bool finished = false;
+        if (phase_ == 1) {
+            const int st = run_phase();
+            if (st == LPSG_ITERATION_LIMIT) {
+                status = LPSG_ITERATION_LIMIT;
+                finished = true;
+            } else if (st == LPSG_UNBOUNDED || objective_value() > cfg_.feas_tol) {
+                status = LPSG_INFEASIBLE;
+                finished = true;
+            } else {
+                drive_out_artificials();
+                enter_phase2();
+            }
+        }
+        if (!finished) status = run_phase();
+        done_ = status != LPSG_ITERATION_LIMIT;
+    }
+    hctl_->status = ST_HOLD;
+    push();
+    CK(cudaEventRecord(e1, st_));
+    CK(cudaStreamSynchronize(st_));
+    const double t1 = now_s();
+    {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        last_device_ms = ms;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    }
+    final_status_ = status;
+    solved_ = true;
+
+    rep->status = status;
+    switch (status) {
+        case LPSG_OPTIMAL:
+        case LPSG_ITERATION_LIMIT: rep->objective = objective_value(); break;
+        case LPSG_UNBOUNDED: rep->objective = -std::numeric_limits<double>::infinity(); break;
+        default: rep->objective = std::numeric_limits<double>::quiet_NaN();
+    }
+    rep->iterations_phase1 = phase_iter_[0];
+    rep->iterations_phase2 = phase_iter_[1];
+    rep->total_seconds = t1 - t0;
+    rep->tpi_seconds = rep->total_seconds / (double)std::max<long long>(1, total_iter_);
+    rep->case_used = 0;
+}
+
+// report.x (solver.cpp:378-383)
+void Solver::get_x(double* x, int n) {
+    if (n != n_total_) throw Error(LPSG_INVALID_ARGUMENT, "lpsg_get_x: n must equal n_total");
+    std::fill(x, x + n, 0.0);
+    if (solved_ && !(final_status_ == LPSG_OPTIMAL || final_status_ == LPSG_ITERATION_LIMIT)) return;
+    std::vector<double> bbar(m_);
+    CK(cudaMemcpyAsync(bbar.data(), d_.T + (size_t)m_ * d_.ldT, sizeof(double) * m_, cudaMemcpyDeviceToHost, st_));
+    d2h_bytes += 8LL * m_;
+    CK(cudaStreamSynchronize(st_));
+    for (int i = 0; i < m_; ++i)
+        if (basic_[i] < n_total_) x[basic_[i]] = bbar[i];
+}
+
+// ---- step API ---------------------------------------------------------------
+void Solver::step_price(int* optimal, int* entering, double* red) {
+    hctl_->status = ST_RUNNING;
+    hctl_->budget = LLONG_MAX;
+    push();
+    launch_price(d_, st_);
+    CK(cudaGetLastError());
+    pull(false);
+    *optimal = hctl_->status == ST_OPTIMAL;
+    *entering = hctl_->q;
+    *red = hctl_->d;
+    hctl_->status = ST_HOLD;
+    hctl_->budget = max_iter_;
+    push();
+}
+
+void Solver::step_compute_direction(int entering, double red) {
+    if (entering < 0 || entering >= n_total_) throw Error(LPSG_INVALID_ARGUMENT, "compute_direction: bad column");
+    hctl_->q = entering;
+    hctl_->d = red;
+    hctl_->status = ST_RUNNING;
+    hctl_->pending = 0;
+    hctl_->no_ftran = 0;
+    push();
+    launch_update(d_, st_);
+    CK(cudaGetLastError());
+    pull(false);
+    hctl_->status = ST_HOLD;
+    push();
+}
+
+void Solver::step_ratio(int* unbounded, double* theta, std::vector<int>& cand) {
+    hctl_->status = ST_RUNNING;
+    hctl_->pending = 0;
+    push();
+    launch_ratio(d_, st_);
+    CK(cudaGetLastError());
+    pull(false);
+    *unbounded = hctl_->status == ST_UNBOUNDED;
+    cand.clear();
+    *theta = 0.0;
+    if (!*unbounded) {
+        *theta = hctl_->theta;
+        cand.resize(hctl_->ncand);
+        CK(cudaMemcpy(cand.data(), d_.cand, sizeof(int) * cand.size(), cudaMemcpyDeviceToHost));
+    }
+    hctl_->status = ST_HOLD;
+    push();
+}
+
+void Solver::step_pivot(int r, int q) {
+    if (r < 0 || r >= m_ || q < 0 || q >= n_work_) throw Error(LPSG_INVALID_ARGUMENT, "pivot_update: bad index");
+    hctl_->r = r;
+    hctl_->q = q;
+    hctl_->status = ST_RUNNING;
+    hctl_->pending = 0;
+    hctl_->no_ftran = 1;
+    hctl_->log_len = 0;
+    push();
+    launch_pivot(d_, st_);
+    launch_update(d_, st_);
+    CK(cudaGetLastError());
+    pull(true);
+    if (hctl_->status == ST_PIVOT_ERR) {
+        hctl_->status = ST_HOLD;
+        hctl_->no_ftran = 0;
+        push();
+        throw Error(LPSG_PIVOT_TOO_SMALL, "pivot element in row " + std::to_string(r) + " below pivot_tol");
+    }
+    // pivot_update itself does not count an iteration (run_phase does)
+    if (hctl_->log_len > 0) basic_[hlog_[0].row] = hlog_[0].entering;
+    hctl_->log_len = 0;
+    hctl_->total_iter -= 1;
+    hctl_->status = ST_HOLD;
+    hctl_->no_ftran = 0;
+    push();
+}
+
+void Solver::read_row(int i, double* out) {
+    if (i < 0 || i > m_) throw Error(LPSG_INVALID_ARGUMENT, "read_row: bad row");
+    if (i == 0) {
+        CK(cudaMemcpyAsync(out, d_.top, sizeof(double) * (m_ + 2), cudaMemcpyDeviceToHost, st_));
+    } else {
+        launch_gather_row(d_, i - 1, scratch_, st_);
+        CK(cudaMemcpyAsync(out, scratch_, sizeof(double) * (m_ + 1), cudaMemcpyDeviceToHost, st_));
+        CK(cudaMemcpyAsync(out + m_ + 1, d_.Y + (i - 1), sizeof(double), cudaMemcpyDeviceToHost, st_));
+    }
+    CK(cudaStreamSynchronize(st_));
+}
+
+}  // namespace lpsg
+
+// ============================================================== C ABI ===
+struct lpsg_solver {
+    lpsg::Solver* s;
+};
+
+namespace {
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return LPSG_OK;
+    } catch (const lpsg::Error& e) {
+        lpsg::g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        lpsg::g_err = "host out of memory";
+        return LPSG_OUT_OF_MEMORY;
+    } catch (const std::exception& e) {
+        lpsg::g_err = e.what();
+        return LPSG_CUDA_ERROR;
+    }
+}
+int bad(const char* what) {
+    lpsg::g_err = what;
+    return LPSG_INVALID_ARGUMENT;
+}
+}  // namespace
+
+extern "C" {
+
+const char* lpsg_last_error(void) { return lpsg::g_err.c_str(); }
+const char* lpsg_version(void) { return "lpsg 0.1 (sm_100a, fp64)"; }
+
+int lpsg_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+void lpsg_config_default(lpsg_config* cfg) {
+    std::memset(cfg, 0, sizeof(*cfg));
+    cfg->opt_tol = 1e-7;
+    cfg->pivot_tol = 1e-9;
+    cfg->feas_tol = 1e-7;
+    cfg->ratio_tie_tol = 1e-9;
+    cfg->use_graphs = 1;
+}
+
+int lpsg_create(const lpsg_problem* lp, const lpsg_config* cfg, lpsg_solver** out) {
+    if (!lp || !out) return bad("lpsg_create: null argument");
+    lpsg_config c;
+    if (cfg) c = *cfg;
+    else lpsg_config_default(&c);
+    return guard([&] {
+        auto* h = new lpsg_solver{nullptr};
+        try {
+            h->s = new lpsg::Solver(*lp, c);
+        } catch (...) {
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int lpsg_solve(lpsg_solver* s, lpsg_report* rep) {
+    if (!s || !rep) return bad("lpsg_solve: null argument");
+    return guard([&] { s->s->solve(rep); });
+}
+
+int lpsg_get_x(lpsg_solver* s, double* x, int n) {
+    if (!s || !x) return bad("lpsg_get_x: null argument");
+    return guard([&] { s->s->get_x(x, n); });
+}
+
+void lpsg_destroy(lpsg_solver* s) {
+    if (!s) return;
+    delete s->s;
+    delete s;
+}
+
+int lpsg_two_phase_solve(const lpsg_problem* lp, const lpsg_config* cfg, lpsg_report* rep, double* x) {
+    lpsg_solver* h = nullptr;
+    int rc = lpsg_create(lp, cfg, &h);
+    if (rc) return rc;
+    rc = lpsg_solve(h, rep);
+    if (!rc && x) rc = lpsg_get_x(h, x, lp->n_total);
+    lpsg_destroy(h);
+    return rc;
+}
+
+int lpsg_set_observer(lpsg_solver* s, lpsg_observer cb, void* user) {
+    if (!s) return bad("lpsg_set_observer: null solver");
+    s->s->observer = cb;
+    s->s->observer_user = user;
+    return LPSG_OK;
+}
+
+int lpsg_keep_trace(lpsg_solver* s, int keep) {
+    if (!s) return bad("lpsg_keep_trace: null solver");
+    s->s->keep_trace = keep != 0;
+    return LPSG_OK;
+}
+
+int lpsg_get_trace(lpsg_solver* s, lpsg_trace* out, long cap, long* len) {
+    if (!s || !len) return bad("lpsg_get_trace: null argument");
+    const auto& t = s->s->trace;
+    *len = (long)t.size();
+    if (out)
+        for (long k = 0; k < std::min<long>(cap, *len); ++k) out[k] = t[k];
+    return LPSG_OK;
+}
+
+int lpsg_price(lpsg_solver* s, int* optimal, int* entering, double* red) {
+    if (!s || !optimal || !entering || !red) return bad("lpsg_price: null argument");
+    return guard([&] { s->s->step_price(optimal, entering, red); });
+}
+
+int lpsg_compute_direction(lpsg_solver* s, int entering, double red) {
+    if (!s) return bad("lpsg_compute_direction: null solver");
+    return guard([&] { s->s->step_compute_direction(entering, red); });
+}
+
+int lpsg_ratio_test(lpsg_solver* s, int* unbounded, double* theta, int* cand, int cap, int* ncand) {
+    if (!s || !unbounded || !theta || !ncand) return bad("lpsg_ratio_test: null argument");
+    return guard([&] {
+        std::vector<int> c;
+        s->s->step_ratio(unbounded, theta, c);
+        *ncand = (int)c.size();
+        if (cand)
+            for (int k = 0; k < std::min(cap, *ncand); ++k) cand[k] = c[k];
+    });
+}
+
+int lpsg_select_leaving(lpsg_solver* s, const int* cand, int ncand, int entering, int* row) {
+    if (!s || !cand || ncand <= 0 || !row) return bad("lpsg_select_leaving: bad argument");
+    return guard([&] { *row = s->s->select_leaving(std::vector<int>(cand, cand + ncand), entering); });
+}
+
+int lpsg_lookahead_scores(lpsg_solver* s, const int* rows, int k, int entering, double* scores) {
+    if (!s || !rows || k < 0 || !scores) return bad("lpsg_lookahead_scores: bad argument");
+    return guard([&] {
+        std::vector<double> sc;
+        s->s->lookahead(std::vector<int>(rows, rows + k), entering, sc);
+        std::copy(sc.begin(), sc.end(), scores);
+    });
+}
+
+int lpsg_pivot_update(lpsg_solver* s, int r, int q) {
+    if (!s) return bad("lpsg_pivot_update: null solver");
+    return guard([&] { s->s->step_pivot(r, q); });
+}
+
+int lpsg_dims(lpsg_solver* s, int* m, int* n_total, int* n_work) {
+    if (!s) return bad("lpsg_dims: null solver");
+    if (m) *m = s->s->m();
+    if (n_total) *n_total = s->s->n_total();
+    if (n_work) *n_work = s->s->n_work();
+    return LPSG_OK;
+}
+
+int lpsg_read_row(lpsg_solver* s, int i, double* out) {
+    if (!s || !out) return bad("lpsg_read_row: null argument");
+    return guard([&] { s->s->read_row(i, out); });
+}
+
+int lpsg_basis(lpsg_solver* s, int* basic, int m) {
+    if (!s || !basic || m != s->s->m()) return bad("lpsg_basis: bad argument");
+    std::copy(s->s->basic().begin(), s->s->basic().end(), basic);
+    return LPSG_OK;
+}
+
+int lpsg_phase(lpsg_solver* s) { return s ? s->s->phase() : -1; }
+
+int lpsg_set_max_iter(lpsg_solver* s, long max_iter) {
+    if (!s) return bad("lpsg_set_max_iter: null solver");
+    return guard([&] { s->s->set_max_iter(max_iter); });
+}
+
+int lpsg_profile(lpsg_solver* s, int enable) {
+    if (!s) return bad("lpsg_profile: null solver");
+    return guard([&] { s->s->set_profile(enable != 0); });
+}
+
+int lpsg_profile_get(lpsg_solver* s, lpsg_kernel_stat* out, int cap, int* n) {
+    if (!s || !n) return bad("lpsg_profile_get: null argument");
+    static const char* names[] = {"ratio", "pivot", "price", "update_ftran", "other"};
+    *n = lpsg::Solver::K_NUM;
+    for (int k = 0; out && k < std::min(cap, (int)lpsg::Solver::K_NUM); ++k) {
+        out[k].name = names[k];
+        out[k].launches = s->s->kstat[k].launches;
+        out[k].milliseconds = s->s->kstat[k].ms;
+        out[k].algorithmic_bytes = s->s->kstat[k].bytes;
+    }
+    return LPSG_OK;
+}
+
+int lpsg_last_solve_device_ms(lpsg_solver* s, double* ms) {
+    if (!s || !ms) return bad("lpsg_last_solve_device_ms: null argument");
+    *ms = s->s->last_device_ms;
+    return LPSG_OK;
+}
+
+int lpsg_counters(lpsg_solver* s, long* launches, long long* h2d, long long* d2h) {
+    if (!s) return bad("lpsg_counters: null solver");
+    if (launches) *launches = s->s->launches_total;
+    if (h2d) *h2d = s->s->h2d_bytes;
+    if (d2h) *d2h = s->s->d2h_bytes;
+    return LPSG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,360 @@
+"""Python mirror of the reference solver API (/root/reference/proj/include/lps/solver.hpp).
+
+Same names, argument meaning and error behaviour as the reference:
+
+* ``two_phase_solve(lp, cfg)``          solver.hpp:173 / solver.cpp:394-397
+* ``SimplexSolver`` step API             solver.hpp:79-168
+* ``SolverConfig`` / ``SolveReport``     solver.hpp:34-57
+* ``StandardFormLP``                     lp_model.hpp:49-60
+* ``generate(GenSpec)`` (+ input forms)  generator.cpp:35-72
+* errors ``PivotTooSmall`` etc.          errors.hpp
+
+Every call goes through the C ABI of the CUDA library (include/lpsg.h); there
+is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from . import _lib as L
+
+
+# ------------------------------------------------------------------ errors --
+class Error(RuntimeError):
+    """lps::Error (errors.hpp:9-11)."""
+
+
+class PivotTooSmall(Error):
+    """lps::PivotTooSmall (errors.hpp:58-60)."""
+
+
+class DegenerateSpec(Error):
+    """lps::DegenerateSpec / EmptyProblem (errors.hpp:66-68, 17-19)."""
+
+
+class CudaError(Error):
+    """Device failure (no CUDA device, launch error, out of memory)."""
+
+
+_ERRORS = {1: PivotTooSmall, 2: CudaError, 3: CudaError, 4: Error, 5: CudaError, 6: DegenerateSpec}
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = L.load().lpsg_last_error().decode()
+        raise _ERRORS.get(rc, Error)(msg)
+
+
+# ------------------------------------------------------------------- types --
+# One pivot of the trace (include/lpsg.h lpsg_trace), as a numpy record.
+TRACE_DTYPE = np.dtype([("iteration", np.int64), ("phase", np.int32), ("row", np.int32),
+                        ("leaving", np.int32), ("entering", np.int32),
+                        ("objective", np.float64)])
+
+class SolveStatus(enum.IntEnum):
+    """lps::SolveStatus (solver.hpp:14)."""
+    optimal = 0
+    unbounded = 1
+    infeasible = 2
+    iteration_limit = 3
+
+
+class Anticycle(enum.IntEnum):
+    tabu = 0
+    none = 1
+
+
+class ColKind(enum.IntEnum):
+    structural = 0
+    slack = 1
+    artificial = 2
+
+
+@dataclass
+class SolverConfig:
+    """lps::SolverConfig (solver.hpp:34-45) plus device placement."""
+    opt_tol: float = 1e-7
+    pivot_tol: float = 1e-9
+    feas_tol: float = 1e-7
+    ratio_tie_tol: float = 1e-9
+    max_iter: int = 0
+    anticycle: Anticycle = Anticycle.tabu
+    kernel: int = 0          # accepted, ignored (simulation knob, solver.hpp:42)
+    workers: int = 1         # accepted, ignored (solver.hpp:43)
+    device: int = 0
+    batch: int = 0
+    use_graphs: bool = True
+    observer: Optional[Callable[["IterationView"], None]] = None
+
+    def _c(self) -> L.Config:
+        c = L.Config()
+        L.load().lpsg_config_default(C.byref(c))
+        c.opt_tol, c.pivot_tol, c.feas_tol = self.opt_tol, self.pivot_tol, self.feas_tol
+        c.ratio_tie_tol, c.max_iter = self.ratio_tie_tol, int(self.max_iter)
+        c.anticycle, c.kernel, c.workers = int(self.anticycle), int(self.kernel), int(self.workers)
+        c.device, c.batch, c.use_graphs = int(self.device), int(self.batch), int(self.use_graphs)
+        return c
+
+
+@dataclass
+class IterationView:
+    """Per-pivot snapshot (solver.hpp:21-32) minus the tableau rows."""
+    phase: int
+    iteration: int
+    objective: float
+    row: int
+    leaving: int
+    entering: int
+
+
+@dataclass
+class SolveReport:
+    """lps::SolveReport (solver.hpp:47-57)."""
+    status: SolveStatus = SolveStatus.iteration_limit
+    objective: float = 0.0
+    x: np.ndarray = field(default_factory=lambda: np.zeros(0))
+    iterations_phase1: int = 0
+    iterations_phase2: int = 0
+    total_seconds: float = 0.0
+    tpi_seconds: float = 0.0
+    case_used: str = "InCore"
+
+    @property
+    def iterations(self) -> int:
+        return self.iterations_phase1 + self.iterations_phase2
+
+
+@dataclass
+class StandardFormLP:
+    """lps::StandardFormLP (lp_model.hpp:49-60): Min c.x, A x = b, b >= 0, x >= 0."""
+    m: int
+    n_total: int
+    A: np.ndarray
+    b: np.ndarray
+    c: np.ndarray
+    col_kind: np.ndarray
+    name: str = ""
+    objective_sign: float = 1.0
+    objective_constant: float = 0.0
+
+    def __post_init__(self):
+        self.A = np.ascontiguousarray(self.A, dtype=np.float64).reshape(self.m, self.n_total)
+        self.b = np.ascontiguousarray(self.b, dtype=np.float64)
+        self.c = np.ascontiguousarray(self.c, dtype=np.float64)
+        self.col_kind = np.ascontiguousarray(self.col_kind, dtype=np.uint8)
+
+    def _c(self) -> L.Problem:
+        p = L.Problem()
+        p.m, p.n_total = self.m, self.n_total
+        p.A = self.A.ctypes.data_as(C.POINTER(C.c_double))
+        p.b = self.b.ctypes.data_as(C.POINTER(C.c_double))
+        p.c = self.c.ctypes.data_as(C.POINTER(C.c_double))
+        p.col_kind = self.col_kind.ctypes.data_as(C.POINTER(C.c_uint8))
+        return p
+
+
+class SparsityClass(enum.IntEnum):
+    dense = 0
+    s20 = 1
+    s60 = 2
+
+
+class Form(enum.IntEnum):
+    """Input forms of BASELINE.json's configs."""
+    equality = 0      # generator verbatim: artificial start basis
+    le_max = 1        # rows <=, maximize: slack start basis (config C1)
+    degenerate = 2    # C4 recipe: half the rows a_i - a_{i+1} with b_i = 0
+
+
+@dataclass
+class GenSpec:
+    """lps::GenSpec (generator.hpp:14-19) plus the input form."""
+    rows: int
+    cols: int
+    sparsity: SparsityClass = SparsityClass.dense
+    seed: int = 0
+    form: Form = Form.equality
+
+
+def generate(spec: GenSpec) -> StandardFormLP:
+    """lps::generate (generator.cpp:35-72) + canonicalize, straight to standard form."""
+    lib = L.load()
+    n = lib.lpsg_generated_n_total(spec.rows, spec.cols, int(spec.form))
+    if spec.rows <= 0 or spec.cols <= 0:
+        raise DegenerateSpec("generate: rows and cols must be positive")
+    A = np.empty((spec.rows, n)); b = np.empty(spec.rows); c = np.empty(n)
+    ck = np.empty(n, np.uint8)
+    _check(lib.lpsg_generate(spec.rows, spec.cols, int(spec.sparsity), spec.seed, int(spec.form),
+                             A.ctypes.data_as(C.POINTER(C.c_double)),
+                             b.ctypes.data_as(C.POINTER(C.c_double)),
+                             c.ctypes.data_as(C.POINTER(C.c_double)),
+                             ck.ctypes.data_as(C.POINTER(C.c_uint8))))
+    return StandardFormLP(spec.rows, n, A, b, c, ck,
+                          name=f"{spec.rows}_{spec.cols}_{spec.form.name}_s{spec.seed}",
+                          objective_sign=1.0 if spec.form == Form.equality else -1.0)
+
+
+class SimplexSolver:
+    """lps::SimplexSolver (solver.hpp:79-168) on one B200."""
+
+    def __init__(self, lp: StandardFormLP, cfg: Optional[SolverConfig] = None):
+        self.lib = L.load()
+        self.cfg = cfg or SolverConfig()
+        self.lp = lp
+        self._h = C.c_void_p()
+        self._prob = lp._c()
+        _check(self.lib.lpsg_create(C.byref(self._prob), C.byref(self.cfg._c()),
+                                    C.byref(self._h)))
+        self._cb = None
+        if self.cfg.observer is not None:
+            obs = self.cfg.observer
+
+            def _tramp(p, _user):
+                t = p.contents
+                obs(IterationView(t.phase, t.iteration, t.objective, t.row, t.leaving,
+                                  t.entering))
+
+            self._cb = L.OBSERVER(_tramp)
+            _check(self.lib.lpsg_set_observer(self._h, self._cb, None))
+
+    def close(self) -> None:
+        if self._h:
+            self.lib.lpsg_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---- driver
+    def keep_trace(self, keep: bool = True) -> None:
+        _check(self.lib.lpsg_keep_trace(self._h, int(keep)))
+
+    def trace(self) -> np.ndarray:
+        n = C.c_long()
+        _check(self.lib.lpsg_get_trace(self._h, None, 0, C.byref(n)))
+        out = np.zeros(n.value, TRACE_DTYPE)
+        _check(self.lib.lpsg_get_trace(self._h, out.ctypes.data_as(C.POINTER(L.Trace)), n.value,
+                                       C.byref(n)))
+        return out
+
+    def solve(self) -> SolveReport:
+        rep = L.Report()
+        _check(self.lib.lpsg_solve(self._h, C.byref(rep)))
+        x = np.zeros(self.lp.n_total)
+        _check(self.lib.lpsg_get_x(self._h, x.ctypes.data_as(C.POINTER(C.c_double)),
+                                   self.lp.n_total))
+        return SolveReport(SolveStatus(rep.status), rep.objective, x, rep.iterations_phase1,
+                           rep.iterations_phase2, rep.total_seconds, rep.tpi_seconds)
+
+    # ---- measurement (extensions; include/lpsg.h "measurement")
+    def set_max_iter(self, max_iter: int) -> None:
+        _check(self.lib.lpsg_set_max_iter(self._h, int(max_iter)))
+
+    def profile(self, enable: bool = True) -> None:
+        _check(self.lib.lpsg_profile(self._h, int(enable)))
+
+    def profile_stats(self) -> dict:
+        n = C.c_int()
+        buf = (L.KernelStat * 8)()
+        _check(self.lib.lpsg_profile_get(self._h, buf, 8, C.byref(n)))
+        return {buf[k].name.decode(): dict(launches=buf[k].launches, ms=buf[k].milliseconds,
+                                           bytes=buf[k].algorithmic_bytes)
+                for k in range(min(n.value, 8))}
+
+    def device_ms(self) -> float:
+        v = C.c_double()
+        _check(self.lib.lpsg_last_solve_device_ms(self._h, C.byref(v)))
+        return v.value
+
+    def counters(self) -> dict:
+        a, b, c = C.c_long(), C.c_longlong(), C.c_longlong()
+        _check(self.lib.lpsg_counters(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return dict(kernel_launches=a.value, h2d_bytes=b.value, d2h_bytes=c.value)
+
+    # ---- step API
+    @dataclass
+    class Pricing:
+        optimal: bool
+        entering: int
+        reduced_cost: float
+
+    @dataclass
+    class Ratio:
+        unbounded: bool
+        theta: float
+        candidates: List[int]
+
+    def price(self) -> "SimplexSolver.Pricing":
+        o, e, z = C.c_int(), C.c_int(), C.c_double()
+        _check(self.lib.lpsg_price(self._h, C.byref(o), C.byref(e), C.byref(z)))
+        return SimplexSolver.Pricing(bool(o.value), e.value, z.value)
+
+    def compute_direction(self, entering: int, reduced_cost: float) -> None:
+        _check(self.lib.lpsg_compute_direction(self._h, entering, reduced_cost))
+
+    def ratio_test(self) -> "SimplexSolver.Ratio":
+        u, t, n = C.c_int(), C.c_double(), C.c_int()
+        buf = (C.c_int * max(self.m(), 1))()
+        _check(self.lib.lpsg_ratio_test(self._h, C.byref(u), C.byref(t), buf, self.m(),
+                                        C.byref(n)))
+        return SimplexSolver.Ratio(bool(u.value), t.value, list(buf[: n.value]))
+
+    def select_leaving(self, candidates: List[int], entering: int) -> int:
+        arr = (C.c_int * len(candidates))(*candidates)
+        r = C.c_int()
+        _check(self.lib.lpsg_select_leaving(self._h, arr, len(candidates), entering, C.byref(r)))
+        return r.value
+
+    def lookahead_scores(self, rows: List[int], entering: int) -> np.ndarray:
+        arr = (C.c_int * max(len(rows), 1))(*rows)
+        out = np.zeros(len(rows))
+        _check(self.lib.lpsg_lookahead_scores(self._h, arr, len(rows), entering,
+                                              out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def pivot_update(self, leaving_row: int, entering: int) -> None:
+        _check(self.lib.lpsg_pivot_update(self._h, leaving_row, entering))
+
+    # ---- Figure-1 tableau accessors (solver.hpp:139-151)
+    def m(self) -> int:
+        return self.lp.m
+
+    def row(self, i: int) -> np.ndarray:
+        out = np.zeros(self.lp.m + 2)
+        _check(self.lib.lpsg_read_row(self._h, i, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
+    def objective_value(self) -> float:
+        return float(self.row(0)[self.lp.m])
+
+    def basis(self) -> np.ndarray:
+        out = np.zeros(self.lp.m, np.int32)
+        _check(self.lib.lpsg_basis(self._h, out.ctypes.data_as(C.POINTER(C.c_int)), self.lp.m))
+        return out
+
+    def phase(self) -> int:
+        return self.lib.lpsg_phase(self._h)
+
+
+def two_phase_solve(lp: StandardFormLP, cfg: Optional[SolverConfig] = None) -> SolveReport:
+    """lps::two_phase_solve (solver.hpp:173)."""
+    with SimplexSolver(lp, cfg) as s:
+        return s.solve()
+
+
+def device_count() -> int:
+    return L.load().lpsg_device_count()
