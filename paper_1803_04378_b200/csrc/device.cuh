@@ -14,7 +14,9 @@
 //          batches run without host round trips.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cstdint>
 
@@ -91,7 +93,38 @@ struct Dev {
     int anticycle;
     int price_grid;
     int update_grid;
+    long long ld_cm;       // column pitch of A_cm (even, 16-byte aligned columns)
+    // launch geometry of the streaming kernels (configure_kernels)
+    int upd_h, upd_C, upd_S, upd_U, upd_smem, upd_threads;
+    const CUtensorMap* tm_T;   // 2D TMA descriptor of T, box {h rows, C columns}
+    const CUtensorMap* tm_nb;  // 2D TMA descriptors of A_nb, box {wbx slots, price_rows(wbx) rows}
+    int price_nwc, price_S, price_smem, price_threads;
+    size_t price_stage_bytes;
 };
+
+// Pricing geometry for n_scan active slots over G CTAs: each CTA owns w slots
+// (multiple of 8) loaded as nb TMA boxes of wbx <= 256 slots x R rows.
+struct PriceGeom {
+    int w, nb, wbx, R;
+};
+__host__ __device__ inline int price_rows(int wbx) {
+    int R = (24 * 1024) / (8 * wbx);
+    R = R < 2 ? 2 : (R > 256 ? 256 : R);
+    return R & ~1;
+}
+__host__ __device__ inline PriceGeom price_geom(int n_scan, int G) {
+    int w = (n_scan + G - 1) / G;
+    if (w < 8) w = 8;
+    const int nb = (w + 255) / 256;
+    int wbx = (w + nb - 1) / nb;
+    wbx = (wbx + 7) & ~7;
+    PriceGeom g;
+    g.nb = nb;
+    g.wbx = wbx;
+    g.w = nb * wbx;
+    g.R = price_rows(wbx);
+    return g;
+}
 
 // Lookahead (solver.cpp:164-213) batch buffers.
 struct LookaheadDev {
@@ -114,13 +147,15 @@ struct LookaheadDev {
 };
 
 // ---- launchers (kernels.cu) -------------------------------------------------
+void configure_kernels(Dev& d);
+bool create_tensor_maps(Dev& d, CUtensorMap** dev_maps, int* count);
 void launch_init_tableau(const Dev& d, const double* b, cudaStream_t st);
 void launch_rebuild_top(const Dev& d, cudaStream_t st);
 void launch_price(const Dev& d, cudaStream_t st);
 void launch_update(const Dev& d, cudaStream_t st);
 void launch_ratio(const Dev& d, cudaStream_t st);
 void launch_pivot(const Dev& d, cudaStream_t st);
-void launch_transpose(const double* A_rm, double* A_cm, int m, int n, cudaStream_t st);
+void launch_transpose(const double* A_rm, double* A_cm, int m, int n, long long ld, cudaStream_t st);
 void launch_build_nb_from(const Dev& d, const double* A_rm, int n_scan, cudaStream_t st);
 void launch_drive_scan(const Dev& d, int row, double* scratch, cudaStream_t st);
 void launch_lookahead(const Dev& d, LookaheadDev& la, cudaStream_t st);

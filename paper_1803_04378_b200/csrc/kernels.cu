@@ -14,6 +14,8 @@
 #include <climits>
 #include <cmath>
 
+#include <vector>
+
 #include "device.cuh"
 
 namespace lpsg {
@@ -102,9 +104,9 @@ __global__ void k_init_tableau(Dev d, const double* __restrict__ b) {
     }
 }
 
-// A_cm[j*m + i] = A_rm[i*n + j]  (tiled transpose through shared memory)
+// A_cm[j*ld + i] = A_rm[i*n + j]  (tiled transpose through shared memory)
 __global__ void k_transpose(const double* __restrict__ A_rm, double* __restrict__ A_cm, int m,
-                            int n) {
+                            int n, long long ld) {
     __shared__ double tile[32][33];
     const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
     for (int k = threadIdx.y; k < 32; k += blockDim.y) {
@@ -114,7 +116,7 @@ __global__ void k_transpose(const double* __restrict__ A_rm, double* __restrict_
     __syncthreads();
     for (int k = threadIdx.y; k < 32; k += blockDim.y) {
         const int j = j0 + k, i = i0 + threadIdx.x;
-        if (i < m && j < n) A_cm[(size_t)j * m + i] = tile[threadIdx.x][k];
+        if (i < m && j < n) A_cm[(size_t)j * ld + i] = tile[threadIdx.x][k];
     }
 }
 
@@ -161,37 +163,139 @@ __global__ void k_rebuild_top(Dev d) {
     }
 }
 
+// ------------------------------------------------ async bulk-copy helpers ---
+// cp.async.bulk (TMA engine, SASS UBLKCP) moves global -> shared without
+// registers; mbarriers (SYNCS.*) carry the byte counts. One producer warp per
+// CTA keeps a ring of S stages in flight; consumer warps run the sequential
+// fp64 chains out of shared memory.
+__device__ __forceinline__ uint32_t su32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; "
+            "selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(su32(b)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(b))
+        : "memory");
+}
+__device__ __forceinline__ int even_up(int v) { return (v + 1) & ~1; }
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+        "{%2, %3}], [%4];" ::"r"(su32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- price ---
-// solver.cpp:79-129 (+ the loop-top budget check, solver.cpp:281): one thread
-// per nonbasic slot, z = dot(W, a_j) - c_j with ascending i, then a grid-wide
-// (max z, min j) reduction finished by the last CTA.
-__global__ void __launch_bounds__(256) k_price(Dev d) {
+// solver.cpp:79-129 (+ the loop-top budget check, solver.cpp:281).
+// One CTA per SM; CTA b owns the contiguous slot range [b*w, b*w + w) of the
+// row-major nonbasic matrix A_nb (w = ceil(n_scan/G) rounded up to 8, split
+// into nb TMA boxes of wbx <= 256 slots). A producer warp streams R-row tiles
+// through an S-stage ring with 2D TMA (one cp.async.bulk.tensor per box) plus a
+// 1D bulk copy of the matching W segment; consumer thread t accumulates
+// z_t = sum_i W_i * a_i,t strictly in ascending i. The grid-wide
+// (max z, min j) reduction is finished by the last CTA.
+__global__ void __launch_bounds__(512) k_price(Dev d) {
+    extern __shared__ __align__(1024) unsigned char smem[];
     Ctl* c = d.ctl;
     if (c->status != ST_RUNNING) return;
     const bool budget_hit = c->total_iter >= c->budget;
     const int n_scan = c->n_scan;
     const double* cost = phase_cost(d, c->phase);
     const int m = d.m;
-    const double* __restrict__ w = d.top;
+    const int G = gridDim.x;
+    const PriceGeom g = price_geom(n_scan, G);
+    const int s0 = blockIdx.x * g.w;
+    const int ns = max(0, min(g.w, n_scan - s0));
+    const int nwc = d.price_nwc;
+    const int S = d.price_S;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double bz = -kInf;
     int bj = INT_MAX;
-    if (!budget_hit) {
-        const int stride = gridDim.x * blockDim.x;
-        for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_scan; s += stride) {
-            const double* __restrict__ a = d.A_nb + s;
-            double acc = 0.0;
-            int i = 0;
-            for (; i + 8 <= m; i += 8) {
-                double v[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) v[u] = a[(size_t)(i + u) * d.ld_nb];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) acc = dadd(acc, dmul(w[i + u], v[u]));
+    if (!budget_hit && ns > 0) {
+        const int R = g.R, w = g.w;
+        const size_t stage_el = (size_t)R * w + R;  // tile + W segment (doubles)
+        const size_t stage_stride = (stage_el * 8 + 1023) / 1024 * 1024;
+        uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * d.price_stage_bytes);
+        uint64_t* empty = full + S;
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < S; ++k) {
+                mbar_init(&full[k], 1);
+                mbar_init(&empty[k], nwc);
             }
-            for (; i < m; ++i) acc = dadd(acc, dmul(w[i], a[(size_t)i * d.ld_nb]));
-            const int j = d.slot2col[s];
-            const double z = dsub(acc, cost[j]);
-            if (better(z, j, bz, bj)) { bz = z; bj = j; }
+            mbar_fence_init();
+        }
+        __syncthreads();
+        const int nst = (m + R - 1) / R;
+        const CUtensorMap* map = d.tm_nb + (g.wbx / 8 - 1);
+        if (warp == nwc) {
+            if (lane == 0) {
+                for (int k = 0; k < nst; ++k) {
+                    const int st = k % S;
+                    if (k >= S) mbar_wait(&empty[st], ((k / S) + 1) & 1);
+                    const int i0 = k * R;
+                    unsigned char* sb = smem + (size_t)st * stage_stride;
+                    double* ws = reinterpret_cast<double*>(sb) + (size_t)R * w;
+                    mbar_expect_tx(&full[st], (uint32_t)(R * w * 8 + R * 8));
+                    for (int q = 0; q < g.nb; ++q)
+                        tma_load_2d(sb + (size_t)q * g.wbx * R * 8, map, s0 + q * g.wbx, i0, &full[st]);
+                    bulk_g2s(ws, d.top + i0, (uint32_t)R * 8u, &full[st]);
+                }
+            }
+        } else if (warp < nwc) {
+            const int t = threadIdx.x;
+            // box q holds slots [q*wbx, (q+1)*wbx) as R rows of wbx doubles
+            const int q = t / g.wbx, tq = t - q * g.wbx;
+            double acc = 0.0;
+            for (int k = 0; k < nst; ++k) {
+                const int st = k % S;
+                mbar_wait(&full[st], (k / S) & 1);
+                const int nr = min(R, m - k * R);
+                const double* sb = reinterpret_cast<const double*>(smem + (size_t)st * stage_stride);
+                const double* ws = sb + (size_t)R * w;
+                if (t < ns) {
+                    const double* col = sb + (size_t)q * g.wbx * R + tq;
+#pragma unroll 8
+                    for (int rr = 0; rr < nr; ++rr) acc = dadd(acc, dmul(ws[rr], col[(size_t)rr * g.wbx]));
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
+            }
+            if (t < ns) {
+                const int j = d.slot2col[s0 + t];
+                bz = dsub(acc, cost[j]);
+                bj = j;
+            }
         }
     }
     block_argmax(bz, bj);
@@ -226,48 +330,133 @@ __global__ void __launch_bounds__(256) k_price(Dev d) {
 // --------------------------------------------------------- update+FTRAN ---
 // tiled_engine.cpp:230-266 with tile_kernel's cached mode (79-106) fused with the
 // NEXT pivot's compute_direction (solver.cpp:131-136), SURVEY.md Appendix B.
-// Thread per row i; columns j ascending: T_ij += (-y_i) * x_j unless that
-// product is 0; row r takes x. Then Y_i = sum_j T_new[i][j] * a_q[j] in order.
-__global__ void __launch_bounds__(128) k_update(Dev d) {
+// CTA b owns rows [b*h, b*h + h) of the column-major [B^-1 | b_bar]; a producer
+// lane streams h-row x C-column boxes with 2D TMA (+ the x and a_q segments).
+// Warp roles per stage:
+//   U update warps (warp-per-column, lane-per-row): T_ij += (-y_i) * x_j unless
+//     that product is 0, row r takes x_j; written back in place in shared
+//     memory and to HBM with coalesced stores;
+//   F FTRAN warps (thread-per-row): Y_i = sum_j T_new[i][j] * a_q[j] as one
+//     sequential chain in ascending j, reading the updated tile.
+__global__ void __launch_bounds__(512) k_update(Dev d) {
+    extern __shared__ __align__(1024) unsigned char smem[];
     Ctl* c = d.ctl;
     const int status = c->status;
     const bool up = c->pending != 0;
     const bool ft = status == ST_RUNNING && !c->no_ftran && c->q >= 0;
     if (!up && !ft) return;
-    const int m = d.m;
+    const int m = d.m, h = d.upd_h, C = d.upd_C, S = d.upd_S, U = d.upd_U;
+    const int F = (h + 31) >> 5;
     const int r = c->upd_r;
-    const double* __restrict__ x = d.xrow;
-    const double* __restrict__ a = ft ? d.A_cm + (size_t)c->q * m : nullptr;
-    const int stride = gridDim.x * blockDim.x;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += stride) {
-        const double yi = d.Y[i];
-        const double ny = -yi;
-        double acc = 0.0;
-        double* __restrict__ col = d.T + i;
-        for (int j = 0; j <= m; ++j) {
-            double v = col[(size_t)j * d.ldT];
+    const int i0 = blockIdx.x * h;
+    const int ncols = m + 1;
+    const int nst = (ncols + C - 1) / C;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t tile_el = (size_t)C * h;
+    const size_t stage_stride = ((tile_el + 2 * (size_t)C) * 8 + 1023) / 1024 * 1024;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_stride);
+    uint64_t* upd = full + S;
+    uint64_t* empty = upd + S;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < S; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&upd[k], U);
+            mbar_init(&empty[k], F);
+        }
+        mbar_fence_init();
+    }
+    __syncthreads();
+    const double* __restrict__ a = ft ? d.A_cm + (size_t)c->q * d.ld_cm : nullptr;
+    if (warp == U + F) {
+        // ---- producer
+        if (lane == 0) {
+            for (int k = 0; k < nst; ++k) {
+                const int st = k % S;
+                if (k >= S) mbar_wait(&empty[st], ((k / S) + 1) & 1);
+                const int j0 = k * C, nc = min(C, ncols - j0);
+                const uint32_t seg = (uint32_t)even_up(nc) * 8u;
+                unsigned char* sb = smem + (size_t)st * stage_stride;
+                double* xs = reinterpret_cast<double*>(sb) + tile_el;
+                double* as = xs + C;
+                mbar_expect_tx(&full[st], (uint32_t)(tile_el * 8) + (up ? seg : 0u) + (ft ? seg : 0u));
+                tma_load_2d(sb, d.tm_T, i0, j0, &full[st]);
+                if (up) bulk_g2s(xs, d.xrow + j0, seg, &full[st]);
+                if (ft) bulk_g2s(as, a + j0, seg, &full[st]);
+            }
+        }
+    } else if (warp < U) {
+        // ---- update warps: column jj = warp, warp+U, ...; rows t = lane, lane+32, ...
+        constexpr int kMaxRowIt = 8;  // h <= 256
+        const int nit = (h + 31) >> 5;
+        double ny[kMaxRowIt];
+        bool isr[kMaxRowIt];
+#pragma unroll
+        for (int u = 0; u < kMaxRowIt; ++u) {
+            const int t = lane + 32 * u;
+            const int i = i0 + t;
+            ny[u] = (u < nit && t < h && i < m) ? -d.Y[i] : 0.0;
+            isr[u] = (u < nit && t < h && i == r);
+        }
+        for (int k = 0; k < nst; ++k) {
+            const int st = k % S;
+            mbar_wait(&full[st], (k / S) & 1);
             if (up) {
-                if (i == r) {
-                    v = x[j];
-                    col[(size_t)j * d.ldT] = v;
-                } else {
-                    const double p = dmul(ny, x[j]);
-                    if (p != 0.0) {
-                        v = dadd(v, p);
-                        col[(size_t)j * d.ldT] = v;
+                const int j0 = k * C, nc = min(C, ncols - j0);
+                double* tile = reinterpret_cast<double*>(smem + (size_t)st * stage_stride);
+                const double* xs = tile + tile_el;
+                for (int jj = warp; jj < nc; jj += U) {
+                    const double xj = xs[jj];
+                    double* tc = tile + (size_t)jj * h;
+                    double* gc = d.T + (size_t)(j0 + jj) * d.ldT + i0;
+#pragma unroll
+                    for (int u = 0; u < kMaxRowIt; ++u) {
+                        const int t = lane + 32 * u;
+                        if (u < nit && t < h && i0 + t < m) {
+                            const double tv = tc[t];
+                            const double p = dmul(ny[u], xj);
+                            double v = (p != 0.0) ? dadd(tv, p) : tv;
+                            v = isr[u] ? xj : v;
+                            tc[t] = v;
+                            gc[t] = v;
+                        }
                     }
                 }
+                fence_proxy_async_smem();
             }
-            if (ft && j < m) acc = dadd(acc, dmul(v, a[j]));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&upd[st]);
         }
-        if (ft) {
-            d.Y[i] = acc;
-        } else {
-            // Reference post-pivot column m+1: row r = 1, others y + (-y)*1 (skip 0).
-            if (i == r) d.Y[i] = 1.0;
-            else {
-                const double p = dmul(ny, x[m + 1]);
-                if (p != 0.0) d.Y[i] = dadd(yi, p);
+    } else if (warp < U + F) {
+        // ---- FTRAN warps: thread-per-row sequential chains
+        const int t = threadIdx.x - U * 32;
+        const int i = i0 + t;
+        const bool valid = t < h && i < m;
+        double acc = 0.0;
+        for (int k = 0; k < nst; ++k) {
+            const int st = k % S;
+            mbar_wait(&upd[st], (k / S) & 1);
+            if (ft && valid) {
+                const int j0 = k * C, nf = min(C, m - j0);
+                const double* tile = reinterpret_cast<const double*>(smem + (size_t)st * stage_stride);
+                const double* as = tile + tile_el + C;
+                const double* col = tile + t;
+#pragma unroll 8
+                for (int jj = 0; jj < nf; ++jj) acc = dadd(acc, dmul(col[(size_t)jj * h], as[jj]));
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+        }
+        if (valid) {
+            if (ft) {
+                d.Y[i] = acc;
+            } else {
+                // Reference post-pivot column m+1: row r = 1, others y + (-y)*1 (skip 0).
+                const double yi = d.Y[i];
+                if (i == r) d.Y[i] = 1.0;
+                else {
+                    const double p = dmul(-yi, d.xrow[m + 1]);
+                    if (p != 0.0) d.Y[i] = dadd(yi, p);
+                }
             }
         }
     }
@@ -388,7 +577,7 @@ __global__ void __launch_bounds__(1024) k_pivot(Dev d) {
         src_col = d.slot2col[n_scan - 1];
     }
     if (dst >= 0) {
-        const double* __restrict__ src = d.A_cm + (size_t)src_col * m;
+        const double* __restrict__ src = d.A_cm + (size_t)src_col * d.ld_cm;
         for (int i = threadIdx.x; i < m; i += blockDim.x) d.A_nb[(size_t)i * d.ld_nb + dst] = src[i];
     }
     __syncthreads();
@@ -463,7 +652,7 @@ __global__ void __launch_bounds__(256) k_drive_scan(Dev d, const double* __restr
             c->found = -1;
         } else {
             const double* cost = phase_cost(d, c->phase);
-            const double* __restrict__ a = d.A_cm + (size_t)j * m;
+            const double* __restrict__ a = d.A_cm + (size_t)j * d.ld_cm;
             double acc = 0.0;
             for (int i = 0; i < m; ++i) acc = dadd(acc, dmul(d.top[i], a[i]));
             c->found_red = dsub(acc, cost[j]);
@@ -512,7 +701,7 @@ __global__ void __launch_bounds__(256) k_la_price(Dev d, LookaheadDev la) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         const int p = d.basic[la.rows[k]];
         if (p < d.n_total && p != la.q) {
-            const double* __restrict__ a = d.A_cm + (size_t)p * m;
+            const double* __restrict__ a = d.A_cm + (size_t)p * d.ld_cm;
             double acc = 0.0;
             for (int i = 0; i < m; ++i) acc = dadd(acc, dmul(w[i], a[i]));
             const double z = dsub(acc, cost[p]);
@@ -554,7 +743,7 @@ __global__ void __launch_bounds__(128) k_la_theta(Dev d, LookaheadDev la) {
     const int m = d.m;
     const int rk = la.rows[k];
     const double* __restrict__ X = la.X + (size_t)k * la.ldx;
-    const double* __restrict__ a = d.A_cm + (size_t)bj * m;
+    const double* __restrict__ a = d.A_cm + (size_t)bj * d.ld_cm;
     double theta = kInf;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
         if (d.frozen[i]) continue;
@@ -597,9 +786,9 @@ void launch_init_tableau(const Dev& d, const double* b, cudaStream_t st) {
     k_init_tableau<<<(d.m + 255) / 256, 256, 0, st>>>(d, b);
 }
 
-void launch_transpose(const double* A_rm, double* A_cm, int m, int n, cudaStream_t st) {
+void launch_transpose(const double* A_rm, double* A_cm, int m, int n, long long ld, cudaStream_t st) {
     dim3 grid((n + 31) / 32, (m + 31) / 32);
-    k_transpose<<<grid, dim3(32, 8), 0, st>>>(A_rm, A_cm, m, n);
+    k_transpose<<<grid, dim3(32, 8), 0, st>>>(A_rm, A_cm, m, n, ld);
 }
 
 void launch_build_nb_from(const Dev& d, const double* A_rm, int n_scan, cudaStream_t st) {
@@ -612,9 +801,107 @@ void launch_rebuild_top(const Dev& d, cudaStream_t st) {
     k_rebuild_top<<<(d.m + 1 + 31) / 32, dim3(32, 8), 0, st>>>(d);
 }
 
-void launch_price(const Dev& d, cudaStream_t st) { k_price<<<d.price_grid, 256, 0, st>>>(d); }
+void launch_price(const Dev& d, cudaStream_t st) {
+    k_price<<<d.price_grid, d.price_threads, d.price_smem, st>>>(d);
+}
 
-void launch_update(const Dev& d, cudaStream_t st) { k_update<<<d.update_grid, 128, 0, st>>>(d); }
+void launch_update(const Dev& d, cudaStream_t st) {
+    k_update<<<d.update_grid, d.upd_threads, d.upd_smem, st>>>(d);
+}
+
+// Launch geometry of the streaming kernels and their TMA
+// descriptors. Must run before the tableau is allocated: it fixes ldT.
+void configure_kernels(Dev& d) {
+    const int G = d.num_sms;
+    // update + FTRAN: h rows per CTA (even, so the TMA box row is a 16-byte multiple)
+    int h = (d.m + G - 1) / G;
+    h = std::min(256, std::max(2, (h + 1) & ~1));
+    d.upd_h = h;
+    d.update_grid = (d.m + h - 1) / h;
+    d.upd_C = h <= 64 ? 32 : h <= 160 ? 16 : 8;
+    d.upd_U = 8;
+    const size_t tile_el = (size_t)d.upd_C * h;
+    const size_t stage = ((tile_el + 2 * (size_t)d.upd_C) * 8 + 1023) / 1024 * 1024;
+    d.upd_S = (int)std::max<size_t>(2, std::min<size_t>(8, (size_t)(192 * 1024) / stage));
+    d.upd_smem = (int)(d.upd_S * stage + 3 * d.upd_S * 8);
+    d.upd_threads = (d.upd_U + (h + 31) / 32 + 1) * 32;
+    // pricing: one CTA per SM over contiguous slot ranges
+    const PriceGeom gm = price_geom(d.n_total, G);
+    d.price_grid = G;
+    d.price_nwc = (gm.w + 31) / 32;
+    d.price_threads = (d.price_nwc + 1) * 32;
+    d.price_stage_bytes = 0;
+    for (int n = 1; n <= d.n_total; n = (n < 64 ? n + 1 : n + n / 64)) {
+        const PriceGeom g = price_geom(n, G);
+        const size_t st = (((size_t)g.R * g.w + g.R) * 8 + 1023) / 1024 * 1024;
+        d.price_stage_bytes = std::max(d.price_stage_bytes, st);
+    }
+    {
+        const PriceGeom g = price_geom(d.n_total, G);
+        const size_t st = (((size_t)g.R * g.w + g.R) * 8 + 1023) / 1024 * 1024;
+        d.price_stage_bytes = std::max(d.price_stage_bytes, st);
+    }
+    d.price_S = (int)std::max<size_t>(2, std::min<size_t>(6, (size_t)(192 * 1024) / d.price_stage_bytes));
+    d.price_smem = (int)(d.price_S * d.price_stage_bytes + 2 * d.price_S * 8);
+    cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, d.upd_smem);
+    cudaFuncSetAttribute(k_price, cudaFuncAttributeMaxDynamicSharedMemorySize, d.price_smem);
+}
+
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !p)
+            return nullptr;
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+bool encode_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
+               uint32_t box_inner, uint32_t box_outer) {
+    auto fn = get_encode();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {inner, outer};
+    const cuuint64_t strides[1] = {pitch_bytes};
+    const cuuint32_t box[2] = {box_inner, box_outer};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+}  // namespace
+
+// Encodes the TMA descriptors (T: one box shape; A_nb: one per slot-box width
+// wbx = 8, 16, ..., 256) into device memory. Returns false on failure.
+bool create_tensor_maps(Dev& d, CUtensorMap** dev_maps, int* count) {
+    std::vector<CUtensorMap> maps;
+    CUtensorMap mt;
+    if (!encode_2d(&mt, d.T, (uint64_t)d.ldT, (uint64_t)d.m + 1, (uint64_t)d.ldT * 8, d.upd_h, d.upd_C))
+        return false;
+    maps.push_back(mt);
+    const int nwb = 32;  // wbx = 8 .. 256
+    for (int k = 1; k <= nwb; ++k) {
+        const int wbx = 8 * k;
+        CUtensorMap mp;
+        if (!encode_2d(&mp, d.A_nb, (uint64_t)d.ld_nb, (uint64_t)d.m, (uint64_t)d.ld_nb * 8, wbx,
+                       price_rows(wbx)))
+            return false;
+        maps.push_back(mp);
+    }
+    CUtensorMap* p = nullptr;
+    if (cudaMalloc(&p, maps.size() * sizeof(CUtensorMap)) != cudaSuccess) return false;
+    if (cudaMemcpy(p, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice) != cudaSuccess)
+        return false;
+    d.tm_T = p;
+    d.tm_nb = p + 1;
+    *dev_maps = p;
+    *count = (int)maps.size();
+    return true;
+}
 
 void launch_ratio(const Dev& d, cudaStream_t st) { k_ratio<<<1, 1024, 0, st>>>(d); }
 

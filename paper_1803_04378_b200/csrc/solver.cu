@@ -123,6 +123,8 @@ private:
     int* hone_ = nullptr;       // pinned constant 1 (stream-ordered flag writes)
     double* scratch_ = nullptr;
     double* cost_buf_ = nullptr;
+    CUtensorMap* tmaps_ = nullptr;
+    int n_tmaps_ = 0;
     int batch_ = 16;
 
 public:
@@ -277,24 +279,25 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
     d_.m = m;
     d_.n_total = n;
     d_.n_work = n_work_;
-    d_.ldT = round_up(m + 1, 32);
     d_.ld_nb = round_up(n, 32) + 32;
+    d_.ld_cm = round_up(m, 4);
     d_.num_sms = prop.multiProcessorCount;
     d_.opt_tol = cfg_.opt_tol;
     d_.pivot_tol = cfg_.pivot_tol;
     d_.feas_tol = cfg_.feas_tol;
     d_.ratio_tie_tol = cfg_.ratio_tie_tol;
     d_.anticycle = cfg_.anticycle;
-    d_.price_grid = 2 * d_.num_sms;
-    d_.update_grid = (m + 127) / 128;
+    configure_kernels(d_);
+    CK(cudaGetLastError());
+    d_.ldT = round_up(std::max<long long>(m + 1, (long long)d_.update_grid * d_.upd_h), 32);
     batch_ = cfg_.batch > 0 ? cfg_.batch : (m <= 1024 ? 64 : m <= 4096 ? 16 : 4);
     d_.log_cap = batch_ + 8;
 
-    d_.T = dalloc<double>((size_t)(m + 1) * d_.ldT);
-    d_.top = dalloc<double>(m + 2);
+    d_.T = dalloc<double>((size_t)(m + 1) * d_.ldT + 64);
+    d_.top = dalloc<double>(m + 520);  // + padding: TMA-side W segments may run past m+2
     d_.Y = dalloc<double>(m);
-    d_.xrow = dalloc<double>(m + 2);
-    double* A_cm = dalloc<double>((size_t)n * m);
+    d_.xrow = dalloc<double>(m + 4);
+    double* A_cm = dalloc<double>((size_t)n * d_.ld_cm + 64);
     d_.A_cm = A_cm;
     d_.A_nb = dalloc<double>((size_t)m * d_.ld_nb + 64);
     d_.slot2col = dalloc<int>(d_.ld_nb);
@@ -310,6 +313,8 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
     d_.pj = dalloc<int>(d_.price_grid);
     d_.log = dalloc<LogEntry>(d_.log_cap);
     scratch_ = dalloc<double>(m + 2);
+    if (!create_tensor_maps(d_, &tmaps_, &n_tmaps_))
+        throw Error(LPSG_CUDA_ERROR, "lpsg_create: cuTensorMapEncodeTiled failed");
     CK(cudaMallocHost(&hctl_, sizeof(Ctl)));
     CK(cudaMallocHost(&hlog_, sizeof(LogEntry) * d_.log_cap));
     CK(cudaMallocHost(&hone_, sizeof(int)));
@@ -330,7 +335,8 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
     {
         double* A_rm = dalloc<double>((size_t)m * n);
         CK(cudaMemcpyAsync(A_rm, lp.A, sizeof(double) * (size_t)m * n, cudaMemcpyHostToDevice, st_));
-        launch_transpose(A_rm, A_cm, m, n, st_);
+        CK(cudaMemsetAsync(A_cm, 0, sizeof(double) * ((size_t)n * d_.ld_cm + 64), st_));
+        launch_transpose(A_rm, A_cm, m, n, d_.ld_cm, st_);
         CK(cudaMemsetAsync(d_.slot2col, 0xff, sizeof(int) * d_.ld_nb, st_));
         if (n_scan)
             CK(cudaMemcpyAsync(d_.slot2col, slot2col.data(), sizeof(int) * n_scan, cudaMemcpyHostToDevice, st_));
@@ -345,7 +351,7 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
     CK(cudaMemsetAsync(d_.frozen, 0, m, st_));
     CK(cudaMemcpyAsync(cost_buf_, cost.data(), sizeof(double) * cost.size(), cudaMemcpyHostToDevice, st_));
     CK(cudaMemsetAsync(d_.Y, 0, sizeof(double) * m, st_));
-    CK(cudaMemsetAsync(d_.top, 0, sizeof(double) * (m + 2), st_));
+    CK(cudaMemsetAsync(d_.top, 0, sizeof(double) * (m + 520), st_));
 
     // ---- initial Figure-1 tableau B = I, b_bar = b (solver.cpp:66-72)
     CK(cudaMemsetAsync(d_.T, 0, sizeof(double) * (size_t)(m + 1) * d_.ldT, st_));
@@ -370,7 +376,7 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
 Solver::~Solver() {
     if (st_) cudaStreamSynchronize(st_);
     void* bufs[] = {d_.T, d_.top, d_.Y, d_.xrow, (void*)d_.A_cm, d_.A_nb, d_.slot2col, d_.col2slot,
-                    d_.basic, d_.frozen, cost_buf_, d_.ctl, d_.cand, d_.pz, d_.pj, d_.log, scratch_};
+                    d_.basic, d_.frozen, cost_buf_, d_.ctl, d_.cand, d_.pz, d_.pj, d_.log, scratch_, tmaps_};
     for (void* p : bufs)
         if (p) cudaFree(p);
     if (hctl_) cudaFreeHost(hctl_);
