@@ -260,9 +260,10 @@ __global__ void __launch_bounds__(512) k_price(Dev d) {
         const CUtensorMap* map = d.tm_nb + (g.wbx / 8 - 1);
         if (warp == nwc) {
             if (lane == 0) {
+                int st = 0;
+                uint32_t ph = 0;
                 for (int k = 0; k < nst; ++k) {
-                    const int st = k % S;
-                    if (k >= S) mbar_wait(&empty[st], ((k / S) + 1) & 1);
+                    if (k >= S) mbar_wait(&empty[st], ph ^ 1);
                     const int i0 = k * R;
                     unsigned char* sb = smem + (size_t)st * stage_stride;
                     double* ws = reinterpret_cast<double*>(sb) + (size_t)R * w;
@@ -270,26 +271,44 @@ __global__ void __launch_bounds__(512) k_price(Dev d) {
                     for (int q = 0; q < g.nb; ++q)
                         tma_load_2d(sb + (size_t)q * g.wbx * R * 8, map, s0 + q * g.wbx, i0, &full[st]);
                     bulk_g2s(ws, d.top + i0, (uint32_t)R * 8u, &full[st]);
+                    if (++st == S) { st = 0; ph ^= 1; }
                 }
             }
         } else if (warp < nwc) {
             const int t = threadIdx.x;
             // box q holds slots [q*wbx, (q+1)*wbx) as R rows of wbx doubles
             const int q = t / g.wbx, tq = t - q * g.wbx;
+            const int wbx = g.wbx;
             double acc = 0.0;
+            int st = 0;
+            uint32_t ph = 0;
             for (int k = 0; k < nst; ++k) {
-                const int st = k % S;
-                mbar_wait(&full[st], (k / S) & 1);
+                mbar_wait(&full[st], ph);
                 const int nr = min(R, m - k * R);
                 const double* sb = reinterpret_cast<const double*>(smem + (size_t)st * stage_stride);
                 const double* ws = sb + (size_t)R * w;
                 if (t < ns) {
-                    const double* col = sb + (size_t)q * g.wbx * R + tq;
-#pragma unroll 8
-                    for (int rr = 0; rr < nr; ++rr) acc = dadd(acc, dmul(ws[rr], col[(size_t)rr * g.wbx]));
+                    const double* col = sb + q * wbx * R + tq;
+                    int rr = 0;
+                    // loads of a group are issued before its (sequential) chain
+                    for (; rr + 8 <= nr; rr += 8) {
+                        double av[8], wv[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) av[u] = col[(rr + u) * wbx];
+#pragma unroll
+                        for (int u = 0; u < 8; u += 2) {
+                            const double2 w2 = *reinterpret_cast<const double2*>(ws + rr + u);
+                            wv[u] = w2.x;
+                            wv[u + 1] = w2.y;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) acc = dadd(acc, dmul(wv[u], av[u]));
+                    }
+                    for (; rr < nr; ++rr) acc = dadd(acc, dmul(ws[rr], col[rr * wbx]));
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[st]);
+                if (++st == S) { st = 0; ph ^= 1; }
             }
             if (t < ns) {
                 const int j = d.slot2col[s0 + t];
@@ -370,9 +389,10 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
     if (warp == U + F) {
         // ---- producer
         if (lane == 0) {
+            int st = 0;
+            uint32_t ph = 0;
             for (int k = 0; k < nst; ++k) {
-                const int st = k % S;
-                if (k >= S) mbar_wait(&empty[st], ((k / S) + 1) & 1);
+                if (k >= S) mbar_wait(&empty[st], ph ^ 1);
                 const int j0 = k * C, nc = min(C, ncols - j0);
                 const uint32_t seg = (uint32_t)even_up(nc) * 8u;
                 unsigned char* sb = smem + (size_t)st * stage_stride;
@@ -382,42 +402,51 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                 tma_load_2d(sb, d.tm_T, i0, j0, &full[st]);
                 if (up) bulk_g2s(xs, d.xrow + j0, seg, &full[st]);
                 if (ft) bulk_g2s(as, a + j0, seg, &full[st]);
+                if (++st == S) { st = 0; ph ^= 1; }
             }
         }
     } else if (warp < U) {
-        // ---- update warps: column jj = warp, warp+U, ...; rows t = lane, lane+32, ...
-        constexpr int kMaxRowIt = 8;  // h <= 256
-        const int nit = (h + 31) >> 5;
-        double ny[kMaxRowIt];
-        bool isr[kMaxRowIt];
+        // ---- update warps: warp-per-column, lane-per-row-pair (double2), rows
+        // 2*lane + 64*u. Row r was already replaced by x in place (k_pivot), so
+        // its multiplier is 0 and the skip leaves it untouched, exactly like the
+        // zeroed multiplier of tiled_engine.cpp:241.
+        constexpr int kMaxPairIt = 4;  // h <= 256
+        const int nit = (h + 63) >> 6;
+        double ny0[kMaxPairIt], ny1[kMaxPairIt];
 #pragma unroll
-        for (int u = 0; u < kMaxRowIt; ++u) {
-            const int t = lane + 32 * u;
+        for (int u = 0; u < kMaxPairIt; ++u) {
+            const int t = 2 * lane + 64 * u;
             const int i = i0 + t;
-            ny[u] = (u < nit && t < h && i < m) ? -d.Y[i] : 0.0;
-            isr[u] = (u < nit && t < h && i == r);
+            const bool ok = u < nit && t < h;
+            ny0[u] = (ok && i < m && i != r) ? -d.Y[i] : 0.0;
+            ny1[u] = (ok && i + 1 < m && i + 1 != r) ? -d.Y[i + 1] : 0.0;
         }
+        const long long ldT = d.ldT;
+        int st = 0;
+        uint32_t ph = 0;
         for (int k = 0; k < nst; ++k) {
-            const int st = k % S;
-            mbar_wait(&full[st], (k / S) & 1);
+            mbar_wait(&full[st], ph);
             if (up) {
                 const int j0 = k * C, nc = min(C, ncols - j0);
                 double* tile = reinterpret_cast<double*>(smem + (size_t)st * stage_stride);
                 const double* xs = tile + tile_el;
                 for (int jj = warp; jj < nc; jj += U) {
                     const double xj = xs[jj];
-                    double* tc = tile + (size_t)jj * h;
-                    double* gc = d.T + (size_t)(j0 + jj) * d.ldT + i0;
+                    double2* tc = reinterpret_cast<double2*>(tile + jj * h);
+                    double2* gc = reinterpret_cast<double2*>(d.T + (size_t)(j0 + jj) * ldT + i0);
 #pragma unroll
-                    for (int u = 0; u < kMaxRowIt; ++u) {
-                        const int t = lane + 32 * u;
-                        if (u < nit && t < h && i0 + t < m) {
-                            const double tv = tc[t];
-                            const double p = dmul(ny[u], xj);
-                            double v = (p != 0.0) ? dadd(tv, p) : tv;
-                            v = isr[u] ? xj : v;
-                            tc[t] = v;
-                            gc[t] = v;
+                    for (int u = 0; u < kMaxPairIt; ++u) {
+                        const int pidx = lane + 32 * u;
+                        if (u < nit && 2 * pidx < h) {
+                            double2 tv = tc[pidx];
+                            const double p0 = dmul(ny0[u], xj);
+                            const double p1 = dmul(ny1[u], xj);
+                            const double s0v = dadd(tv.x, p0);
+                            const double s1v = dadd(tv.y, p1);
+                            tv.x = (p0 != 0.0) ? s0v : tv.x;
+                            tv.y = (p1 != 0.0) ? s1v : tv.y;
+                            tc[pidx] = tv;
+                            gc[pidx] = tv;
                         }
                     }
                 }
@@ -425,26 +454,42 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&upd[st]);
+            if (++st == S) { st = 0; ph ^= 1; }
         }
     } else if (warp < U + F) {
-        // ---- FTRAN warps: thread-per-row sequential chains
+        // ---- FTRAN warps: thread-per-row sequential chains over the updated tile
         const int t = threadIdx.x - U * 32;
         const int i = i0 + t;
         const bool valid = t < h && i < m;
         double acc = 0.0;
+        int st = 0;
+        uint32_t ph = 0;
         for (int k = 0; k < nst; ++k) {
-            const int st = k % S;
-            mbar_wait(&upd[st], (k / S) & 1);
+            mbar_wait(&upd[st], ph);
             if (ft && valid) {
                 const int j0 = k * C, nf = min(C, m - j0);
                 const double* tile = reinterpret_cast<const double*>(smem + (size_t)st * stage_stride);
                 const double* as = tile + tile_el + C;
                 const double* col = tile + t;
-#pragma unroll 8
-                for (int jj = 0; jj < nf; ++jj) acc = dadd(acc, dmul(col[(size_t)jj * h], as[jj]));
+                int jj = 0;
+                for (; jj + 8 <= nf; jj += 8) {
+                    double tv[8], av[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) tv[u] = col[(jj + u) * h];
+#pragma unroll
+                    for (int u = 0; u < 8; u += 2) {
+                        const double2 a2 = *reinterpret_cast<const double2*>(as + jj + u);
+                        av[u] = a2.x;
+                        av[u + 1] = a2.y;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc = dadd(acc, dmul(tv[u], av[u]));
+                }
+                for (; jj < nf; ++jj) acc = dadd(acc, dmul(col[jj * h], as[jj]));
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
+            if (++st == S) { st = 0; ph ^= 1; }
         }
         if (valid) {
             if (ft) {
@@ -555,6 +600,7 @@ __global__ void __launch_bounds__(1024) k_pivot(Dev d) {
     for (int j = threadIdx.x; j <= m; j += blockDim.x) {
         const double xj = ddiv(d.T[(size_t)j * d.ldT + r], yr);
         d.xrow[j] = xj;
+        d.T[(size_t)j * d.ldT + r] = xj;  // in place, like pr[j] /= y_rk
         const double p = dmul(ndk, xj);
         if (p != 0.0) d.top[j] = dadd(d.top[j], p);
     }
