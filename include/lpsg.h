@@ -168,6 +168,11 @@ int lpsg_last_solve_device_ms(lpsg_solver* s, double* ms);
 int lpsg_counters(lpsg_solver* s, long* kernel_launches, long long* h2d_bytes,
                   long long* d2h_bytes);
 
+/* Page-locked host buffers (cudaHostAlloc) so lpsg_create's upload of A runs at
+ * full DMA bandwidth. Freed with lpsg_host_free. */
+int lpsg_host_alloc(size_t bytes, void** out);
+void lpsg_host_free(void* p);
+
 /* ---- input plumbing: lps::generate (generator.cpp:35-72) plus the
  *      BASELINE.json input forms and canonicalize (lp_model.cpp:43-163) for
  *      them. form: 0 equality (verbatim), 1 le + maximize, 2 degenerate.

@@ -80,6 +80,8 @@ SIGNATURES = [
     ("lpsg_last_solve_device_ms", C.c_int, [_P, _PD]),
     ("lpsg_counters", C.c_int, [_P, C.POINTER(C.c_long), C.POINTER(C.c_longlong),
                                 C.POINTER(C.c_longlong)]),
+    ("lpsg_host_alloc", C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    ("lpsg_host_free", None, [C.c_void_p]),
     ("lpsg_generated_n_total", C.c_int, [C.c_int, C.c_int, C.c_int]),
     ("lpsg_generate", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, _PD, _PD, _PD,
                                 C.POINTER(C.c_uint8)]),

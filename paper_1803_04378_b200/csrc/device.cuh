@@ -63,7 +63,8 @@ struct Ctl {
     unsigned int ticket_misc;
     int found;         // drive-out scan result
     double found_red;
-    int pad[2];
+    int no_ratio;      // FTRAN without the fused ratio test (drive-out, step API)
+    int pad;
 };
 
 struct Dev {
@@ -93,6 +94,13 @@ struct Dev {
     int anticycle;
     int price_grid;
     int update_grid;
+    int pivot_grid;
+    // fused ratio test partials (per update CTA): local theta, candidate count
+    // (-1: no eligible row), candidates (row, ratio) in row order
+    double* rc_theta;
+    int* rc_cnt;
+    int* rc_row;
+    double* rc_ratio;
     long long ld_cm;       // column pitch of A_cm (even, 16-byte aligned columns)
     // launch geometry of the streaming kernels (configure_kernels)
     int upd_h, upd_C, upd_S, upd_U, upd_smem, upd_threads;

@@ -346,6 +346,66 @@ __global__ void __launch_bounds__(512) k_price(Dev d) {
     }
 }
 
+// Update warps of k_update: warp-per-column, lane-per-row-pair (double2), rows
+// 2*lane + 64*u for u < NIT. Row r was already replaced by x in place
+// (k_pivot), so its multiplier is 0 and the skip leaves it untouched, exactly
+// like the zeroed multiplier of tiled_engine.cpp:241.
+template <int NIT>
+__device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, uint64_t* full,
+                                            uint64_t* upd, size_t stage_stride, size_t tile_el,
+                                            int nst, int S, int C, int h, int i0, int r, int U,
+                                            bool up, int warp, int lane) {
+    const int m = d.m;
+    double ny0[NIT], ny1[NIT];
+    bool ok[NIT];
+#pragma unroll
+    for (int u = 0; u < NIT; ++u) {
+        const int t = 2 * lane + 64 * u;
+        const int i = i0 + t;
+        ok[u] = t < h;
+        ny0[u] = (ok[u] && i < m && i != r) ? -d.Y[i] : 0.0;
+        ny1[u] = (ok[u] && i + 1 < m && i + 1 != r) ? -d.Y[i + 1] : 0.0;
+    }
+    const size_t ldT = (size_t)d.ldT;
+    double2* const gbase = reinterpret_cast<double2*>(d.T + i0) + lane;  // + col * ldT/2
+    const int ncols = m + 1;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int k = 0; k < nst; ++k) {
+        mbar_wait(&full[st], ph);
+        if (up) {
+            const int j0 = k * C, nc = min(C, ncols - j0);
+            double* tile = reinterpret_cast<double*>(smem + (size_t)st * stage_stride);
+            const double* xs = tile + tile_el;
+            double2* tcol = reinterpret_cast<double2*>(tile + warp * h) + lane;
+            double2* gcol = gbase + (size_t)(j0 + warp) * (ldT / 2);
+            const size_t gstep = (size_t)U * (ldT / 2);
+            const int tstep = U * h / 2;
+            for (int jj = warp; jj < nc; jj += U, tcol += tstep, gcol += gstep) {
+                const double xj = xs[jj];
+#pragma unroll
+                for (int u = 0; u < NIT; ++u) {
+                    if (ok[u]) {
+                        double2 tv = tcol[32 * u];
+                        const double p0 = dmul(ny0[u], xj);
+                        const double p1 = dmul(ny1[u], xj);
+                        const double s0v = dadd(tv.x, p0);
+                        const double s1v = dadd(tv.y, p1);
+                        tv.x = (p0 != 0.0) ? s0v : tv.x;
+                        tv.y = (p1 != 0.0) ? s1v : tv.y;
+                        tcol[32 * u] = tv;
+                        gcol[32 * u] = tv;
+                    }
+                }
+            }
+            fence_proxy_async_smem();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&upd[st]);
+        if (++st == S) { st = 0; ph ^= 1; }
+    }
+}
+
 // --------------------------------------------------------- update+FTRAN ---
 // tiled_engine.cpp:230-266 with tile_kernel's cached mode (79-106) fused with the
 // NEXT pivot's compute_direction (solver.cpp:131-136), SURVEY.md Appendix B.
@@ -386,6 +446,8 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
     }
     __syncthreads();
     const double* __restrict__ a = ft ? d.A_cm + (size_t)c->q * d.ld_cm : nullptr;
+    double f_y = 0.0, f_bbar = 0.0;  // this thread's y_i, b_bar_i (FTRAN warps)
+    bool f_ok = false;
     if (warp == U + F) {
         // ---- producer
         if (lane == 0) {
@@ -410,51 +472,12 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         // 2*lane + 64*u. Row r was already replaced by x in place (k_pivot), so
         // its multiplier is 0 and the skip leaves it untouched, exactly like the
         // zeroed multiplier of tiled_engine.cpp:241.
-        constexpr int kMaxPairIt = 4;  // h <= 256
         const int nit = (h + 63) >> 6;
-        double ny0[kMaxPairIt], ny1[kMaxPairIt];
-#pragma unroll
-        for (int u = 0; u < kMaxPairIt; ++u) {
-            const int t = 2 * lane + 64 * u;
-            const int i = i0 + t;
-            const bool ok = u < nit && t < h;
-            ny0[u] = (ok && i < m && i != r) ? -d.Y[i] : 0.0;
-            ny1[u] = (ok && i + 1 < m && i + 1 != r) ? -d.Y[i + 1] : 0.0;
-        }
-        const long long ldT = d.ldT;
-        int st = 0;
-        uint32_t ph = 0;
-        for (int k = 0; k < nst; ++k) {
-            mbar_wait(&full[st], ph);
-            if (up) {
-                const int j0 = k * C, nc = min(C, ncols - j0);
-                double* tile = reinterpret_cast<double*>(smem + (size_t)st * stage_stride);
-                const double* xs = tile + tile_el;
-                for (int jj = warp; jj < nc; jj += U) {
-                    const double xj = xs[jj];
-                    double2* tc = reinterpret_cast<double2*>(tile + jj * h);
-                    double2* gc = reinterpret_cast<double2*>(d.T + (size_t)(j0 + jj) * ldT + i0);
-#pragma unroll
-                    for (int u = 0; u < kMaxPairIt; ++u) {
-                        const int pidx = lane + 32 * u;
-                        if (u < nit && 2 * pidx < h) {
-                            double2 tv = tc[pidx];
-                            const double p0 = dmul(ny0[u], xj);
-                            const double p1 = dmul(ny1[u], xj);
-                            const double s0v = dadd(tv.x, p0);
-                            const double s1v = dadd(tv.y, p1);
-                            tv.x = (p0 != 0.0) ? s0v : tv.x;
-                            tv.y = (p1 != 0.0) ? s1v : tv.y;
-                            tc[pidx] = tv;
-                            gc[pidx] = tv;
-                        }
-                    }
-                }
-                fence_proxy_async_smem();
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&upd[st]);
-            if (++st == S) { st = 0; ph ^= 1; }
+        switch (nit) {
+            case 1: update_role<1>(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, warp, lane); break;
+            case 2: update_role<2>(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, warp, lane); break;
+            case 3: update_role<3>(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, warp, lane); break;
+            default: update_role<4>(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, warp, lane); break;
         }
     } else if (warp < U + F) {
         // ---- FTRAN warps: thread-per-row sequential chains over the updated tile
@@ -469,6 +492,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
             if (ft && valid) {
                 const int j0 = k * C, nf = min(C, m - j0);
                 const double* tile = reinterpret_cast<const double*>(smem + (size_t)st * stage_stride);
+                if (m - j0 < C) f_bbar = tile[(m - j0) * h + t];  // updated b_bar_i (column m)
                 const double* as = tile + tile_el + C;
                 const double* col = tile + t;
                 int jj = 0;
@@ -494,6 +518,8 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         if (valid) {
             if (ft) {
                 d.Y[i] = acc;
+                f_y = acc;
+                f_ok = true;
             } else {
                 // Reference post-pivot column m+1: row r = 1, others y + (-y)*1 (skip 0).
                 const double yi = d.Y[i];
@@ -505,11 +531,118 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
             }
         }
     }
+    // ---- fused ratio test, CTA-local part (solver.cpp:138-162): theta_b over this
+    // CTA's eligible rows and the rows within window(theta_b), in row order.
+    // The global theta <= theta_b and window() is monotone, so the union of the
+    // local lists is a superset of the global candidates; the last CTA filters it.
+    const bool do_ratio = ft && !c->no_ratio;
+    if (do_ratio) {
+        __shared__ int s_cnt[32];
+        __shared__ double s_theta;
+        __shared__ int s_any;
+        const int i = i0 + (threadIdx.x - U * 32);
+        bool elig = f_ok && !d.frozen[i] && !(f_y <= d.pivot_tol);
+        const double ratio = elig ? ddiv(f_bbar, f_y) : kInf;
+        const double th = block_min(elig ? ratio : kInf);
+        const int any = __syncthreads_or(elig);
+        if (threadIdx.x == 0) { s_theta = th; s_any = any; }
+        __syncthreads();
+        const double wloc = dadd(s_theta, dmul(d.ratio_tie_tol, fmax(1.0, fabs(s_theta))));
+        const bool cand = elig && ratio <= wloc;
+        const unsigned bal = __ballot_sync(0xffffffffu, cand);
+        if (lane == 0) s_cnt[warp] = __popc(bal);
+        __syncthreads();
+        if (cand) {
+            int off = __popc(bal & ((1u << lane) - 1u));
+            for (int w2 = U; w2 < warp; ++w2) off += s_cnt[w2];
+            const size_t slot = (size_t)blockIdx.x * h + off;
+            d.rc_row[slot] = i;
+            d.rc_ratio[slot] = ratio;
+        }
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w2 = U; w2 < U + F; ++w2) tot += s_cnt[w2];
+            d.rc_cnt[blockIdx.x] = s_any ? tot : -1;
+            d.rc_theta[blockIdx.x] = s_theta;
+        }
+    }
     if (!last_block(&c->ticket_update)) return;
     if (threadIdx.x == 0) {
         c->ticket_update = 0;
         if (up) c->pending = 0;
         if (ft) d.top[m + 1] = c->d;
+    }
+    if (!do_ratio) return;
+    // ---- fused ratio test, global part: the last CTA, one thread per producing
+    // CTA b (gridDim.x <= blockDim.x), then an ordered block scan.
+    __shared__ int s_pre[32];
+    __shared__ double s_th2;
+    __shared__ int s_first;
+    const int G = gridDim.x;
+    const int b = threadIdx.x;
+    const int cnt = b < G ? __ldcg(d.rc_cnt + b) : -1;
+    const double thb = cnt >= 0 ? __ldcg(d.rc_theta + b) : kInf;
+    const double th = block_min(thb);
+    const int any = __syncthreads_or(cnt >= 0);
+    if (threadIdx.x == 0) { s_th2 = th; s_first = -1; }
+    __syncthreads();
+    if (!any) {
+        if (threadIdx.x == 0) c->status = ST_UNBOUNDED;
+        return;
+    }
+    const double gth = s_th2;
+    const double window = dadd(gth, dmul(d.ratio_tie_tol, fmax(1.0, fabs(gth))));
+    constexpr int kMaxLocal = 8;
+    int n = 0;
+    int rows_keep[kMaxLocal];
+    for (int e = 0; e < cnt; ++e) {
+        const double ra = __ldcg(d.rc_ratio + (size_t)b * h + e);
+        if (ra <= window) {
+            if (n < kMaxLocal) rows_keep[n] = __ldcg(d.rc_row + (size_t)b * h + e);
+            ++n;
+        }
+    }
+    // exclusive scan of n over the block, in thread (= CTA = row) order
+    int incl = n;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_pre[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        int v = lane < nw ? s_pre[lane] : 0;
+        int inc2 = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, inc2, o);
+            if (lane >= o) inc2 += u;
+        }
+        if (lane < nw) s_pre[lane] = inc2 - v;  // exclusive warp offsets
+        if (lane == 31) s_pre[31] = inc2;       // total (nw <= 16 < 31)
+    }
+    __syncthreads();
+    int pos = s_pre[warp] + incl - n;
+    if (n > 0) {
+        if (pos == 0) s_first = n <= kMaxLocal ? rows_keep[0] : -2;
+        if (n <= kMaxLocal) {
+            for (int e = 0; e < n; ++e) d.cand[pos + e] = rows_keep[e];
+        } else {
+            for (int e = 0; e < cnt; ++e) {
+                const double ra = __ldcg(d.rc_ratio + (size_t)b * h + e);
+                if (ra <= window) d.cand[pos++] = __ldcg(d.rc_row + (size_t)b * h + e);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int total = s_pre[31];
+        c->ncand = total;
+        c->theta = gth;
+        if (total == 1 || d.anticycle == 1)
+            c->r = s_first >= 0 ? s_first : ((volatile int*)d.cand)[0];
+        else
+            c->status = ST_TIE;
     }
 }
 
@@ -585,49 +718,53 @@ __global__ void __launch_bounds__(1024) k_ratio(Dev d) {
 // (IEEE '/'), apply the row-0 part of the update (W, obj and the d slot; the
 // multiplier is T[0][m+1], tiled_engine.cpp:240), swap the basis, maintain the
 // nonbasic pricing slots, and log the pivot (note_iteration's observer data).
-__global__ void __launch_bounds__(1024) k_pivot(Dev d) {
+__global__ void __launch_bounds__(256) k_pivot(Dev d) {
     Ctl* c = d.ctl;
     if (c->status != ST_RUNNING) return;
     const int m = d.m;
     const int r = c->r, q = c->q;
     const double yr = d.Y[r];
     if (fabs(yr) <= d.pivot_tol) {
-        if (threadIdx.x == 0) c->status = ST_PIVOT_ERR;
+        if (blockIdx.x == 0 && threadIdx.x == 0) c->status = ST_PIVOT_ERR;
         return;
     }
     const double dk = d.top[m + 1];
     const double ndk = -dk;
-    for (int j = threadIdx.x; j <= m; j += blockDim.x) {
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gstride = gridDim.x * blockDim.x;
+    for (int j = gtid; j <= m; j += gstride) {
         const double xj = ddiv(d.T[(size_t)j * d.ldT + r], yr);
         d.xrow[j] = xj;
-        d.T[(size_t)j * d.ldT + r] = xj;  // in place, like pr[j] /= y_rk
+        d.T[(size_t)j * d.ldT + r] = xj;  // in place, like pr[j] /= y_rk (solver.cpp:246-247)
         const double p = dmul(ndk, xj);
         if (p != 0.0) d.top[j] = dadd(d.top[j], p);
     }
-    if (threadIdx.x == 0) {
+    if (gtid == 0) {
         const double xl = ddiv(yr, yr);
         d.xrow[m + 1] = xl;
         const double p = dmul(ndk, xl);
         if (p != 0.0) d.top[m + 1] = dadd(dk, p);
     }
-    // nonbasic slot maintenance
+    // nonbasic slot maintenance: the leaving column takes the entering column's
+    // slot (or, for an artificial leaver, the last slot moves into it)
     const int p_leave = d.basic[r];
     const int s_q = d.col2slot[q];
     const int n_scan = c->n_scan;
     int dst = -1, src_col = -1;
     if (p_leave < d.n_total) {
-        dst = s_q >= 0 ? s_q : n_scan;  // reuse q's slot, or append
+        dst = s_q >= 0 ? s_q : n_scan;
         src_col = p_leave;
     } else if (s_q >= 0 && s_q != n_scan - 1) {
-        dst = s_q;                      // artificial leaves: move the last slot in
+        dst = s_q;
         src_col = d.slot2col[n_scan - 1];
     }
     if (dst >= 0) {
         const double* __restrict__ src = d.A_cm + (size_t)src_col * d.ld_cm;
-        for (int i = threadIdx.x; i < m; i += blockDim.x) d.A_nb[(size_t)i * d.ld_nb + dst] = src[i];
+        for (int i = gtid; i < m; i += gstride) d.A_nb[(size_t)i * d.ld_nb + dst] = src[i];
     }
-    __syncthreads();
+    if (!last_block(&c->ticket_misc)) return;
     if (threadIdx.x == 0) {
+        c->ticket_misc = 0;
         int ns = n_scan;
         if (p_leave < d.n_total) {
             if (s_q < 0) ++ns;
@@ -652,7 +789,7 @@ __global__ void __launch_bounds__(1024) k_pivot(Dev d) {
             e.row = r;
             e.leaving = p_leave;
             e.entering = q;
-            e.objective = d.top[m];
+            e.objective = ((volatile double*)d.top)[m];
             d.log[li] = e;
         }
         c->log_len = li + 1;
@@ -873,6 +1010,7 @@ void configure_kernels(Dev& d) {
     d.upd_threads = (d.upd_U + (h + 31) / 32 + 1) * 32;
     // pricing: one CTA per SM over contiguous slot ranges
     const PriceGeom gm = price_geom(d.n_total, G);
+    d.pivot_grid = std::max(1, std::min(2 * G, (d.m + 1 + 255) / 256));
     d.price_grid = G;
     d.price_nwc = (gm.w + 31) / 32;
     d.price_threads = (d.price_nwc + 1) * 32;
@@ -951,7 +1089,7 @@ bool create_tensor_maps(Dev& d, CUtensorMap** dev_maps, int* count) {
 
 void launch_ratio(const Dev& d, cudaStream_t st) { k_ratio<<<1, 1024, 0, st>>>(d); }
 
-void launch_pivot(const Dev& d, cudaStream_t st) { k_pivot<<<1, 1024, 0, st>>>(d); }
+void launch_pivot(const Dev& d, cudaStream_t st) { k_pivot<<<d.pivot_grid, 256, 0, st>>>(d); }
 
 void launch_gather_row(const Dev& d, int i, double* out, cudaStream_t st) {
     k_gather_row<<<(d.m + 1 + 255) / 256, 256, 0, st>>>(d, i, out);

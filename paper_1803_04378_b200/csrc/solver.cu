@@ -126,6 +126,7 @@ private:
     CUtensorMap* tmaps_ = nullptr;
     int n_tmaps_ = 0;
     int batch_ = 16;
+    bool unfused_ratio_ = false;  // debug knob (cfg.reserved[0] & 1): standalone ratio kernel
 
 public:
     // ---- counters and optional per-kernel CUDA-event profile
@@ -151,6 +152,7 @@ private:
         double bytes;
     };
     std::vector<EvRec> ev_used_;
+    cudaEvent_t ev_chain_ = nullptr;  // last boundary event, reusable as the next start
     template <class F>
     void L(int kind, double bytes, F&& f);
     void flush_profile();
@@ -171,27 +173,40 @@ void Solver::L(int kind, double bytes, F&& f) {
             ev_pool_.push_back(e);
         }
     }
-    EvRec r{kind, ev_pool_.back(), nullptr, bytes};
-    ev_pool_.pop_back();
-    r.b = ev_pool_.back();
-    ev_pool_.pop_back();
-    CK(cudaEventRecord(r.a, st_));
+    // One event per kernel boundary: the previous kernel's end event is this
+    // kernel's start event unless another stream operation came in between.
+    cudaEvent_t a;
+    if (ev_chain_) {
+        a = ev_chain_;
+    } else {
+        a = ev_pool_.back();
+        ev_pool_.pop_back();
+        CK(cudaEventRecord(a, st_));
+    }
     f();
-    CK(cudaEventRecord(r.b, st_));
-    ev_used_.push_back(r);
+    cudaEvent_t b = ev_pool_.back();
+    ev_pool_.pop_back();
+    CK(cudaEventRecord(b, st_));
+    ev_used_.push_back(EvRec{kind, a, b, bytes});
+    ev_chain_ = b;
 }
 
 void Solver::flush_profile() {
+    std::vector<cudaEvent_t> seen;
     for (auto& r : ev_used_) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, r.a, r.b));
         kstat[r.kind].launches += 1;
         kstat[r.kind].ms += ms;
         kstat[r.kind].bytes += r.bytes;
-        ev_pool_.push_back(r.a);
-        ev_pool_.push_back(r.b);
+        seen.push_back(r.a);
+        seen.push_back(r.b);
     }
+    std::sort(seen.begin(), seen.end());
+    seen.erase(std::unique(seen.begin(), seen.end()), seen.end());
+    for (cudaEvent_t e : seen) ev_pool_.push_back(e);
     ev_used_.clear();
+    ev_chain_ = nullptr;
 }
 
 // Algorithmic HBM bytes per launch: what the reference's step
@@ -290,6 +305,7 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
     configure_kernels(d_);
     CK(cudaGetLastError());
     d_.ldT = round_up(std::max<long long>(m + 1, (long long)d_.update_grid * d_.upd_h), 32);
+    unfused_ratio_ = (cfg_.reserved[0] & 1) != 0;
     batch_ = cfg_.batch > 0 ? cfg_.batch : (m <= 1024 ? 64 : m <= 4096 ? 16 : 4);
     d_.log_cap = batch_ + 8;
 
@@ -312,6 +328,10 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
     d_.pz = dalloc<double>(d_.price_grid);
     d_.pj = dalloc<int>(d_.price_grid);
     d_.log = dalloc<LogEntry>(d_.log_cap);
+    d_.rc_theta = dalloc<double>(d_.update_grid);
+    d_.rc_cnt = dalloc<int>(d_.update_grid);
+    d_.rc_row = dalloc<int>((size_t)d_.update_grid * d_.upd_h);
+    d_.rc_ratio = dalloc<double>((size_t)d_.update_grid * d_.upd_h);
     scratch_ = dalloc<double>(m + 2);
     if (!create_tensor_maps(d_, &tmaps_, &n_tmaps_))
         throw Error(LPSG_CUDA_ERROR, "lpsg_create: cuTensorMapEncodeTiled failed");
@@ -376,7 +396,8 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
 Solver::~Solver() {
     if (st_) cudaStreamSynchronize(st_);
     void* bufs[] = {d_.T, d_.top, d_.Y, d_.xrow, (void*)d_.A_cm, d_.A_nb, d_.slot2col, d_.col2slot,
-                    d_.basic, d_.frozen, cost_buf_, d_.ctl, d_.cand, d_.pz, d_.pj, d_.log, scratch_, tmaps_};
+                    d_.basic, d_.frozen, cost_buf_, d_.ctl, d_.cand, d_.pz, d_.pj, d_.log, scratch_, tmaps_,
+                    d_.rc_theta, d_.rc_cnt, d_.rc_row, d_.rc_ratio};
     for (void* p : bufs)
         if (p) cudaFree(p);
     if (hctl_) cudaFreeHost(hctl_);
@@ -386,11 +407,13 @@ Solver::~Solver() {
 }
 
 void Solver::push() {
+    ev_chain_ = nullptr;
     CK(cudaMemcpyAsync(d_.ctl, hctl_, sizeof(Ctl), cudaMemcpyHostToDevice, st_));
     h2d_bytes += sizeof(Ctl);
 }
 
 void Solver::pull(bool with_log) {
+    ev_chain_ = nullptr;
     CK(cudaMemcpyAsync(hctl_, d_.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st_));
     d2h_bytes += sizeof(Ctl);
     if (with_log) {
@@ -435,7 +458,7 @@ void Solver::drain_log() {
 
 void Solver::enqueue_pivots(int n) {
     for (int k = 0; k < n; ++k) {
-        L(K_RATIO, bytes_of(K_RATIO), [&] { launch_ratio(d_, st_); });
+        if (unfused_ratio_) L(K_RATIO, bytes_of(K_RATIO), [&] { launch_ratio(d_, st_); });
         L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot(d_, st_); });
         L(K_PRICE, bytes_of(K_PRICE), [&] { launch_price(d_, st_); });
         L(K_UPDATE, bytes_of(K_UPDATE), [&] { launch_update(d_, st_); });
@@ -448,6 +471,7 @@ int Solver::run_phase() {
     hctl_->status = ST_RUNNING;
     hctl_->pending = 0;
     hctl_->no_ftran = 0;
+    hctl_->no_ratio = unfused_ratio_ ? 1 : 0;
     hctl_->log_len = 0;
     hctl_->phase = phase_;
     push();
@@ -570,6 +594,7 @@ void Solver::drive_out_artificials() {
         hctl_->status = ST_RUNNING;
         hctl_->pending = 0;
         hctl_->no_ftran = 0;
+        hctl_->no_ratio = 1;
         hctl_->log_len = 0;
         push();
         launch_update(d_, st_);  // FTRAN only
@@ -581,6 +606,7 @@ void Solver::drive_out_artificials() {
         if (hctl_->status == ST_PIVOT_ERR) throw Error(LPSG_PIVOT_TOO_SMALL, "pivot element below pivot_tol");
         drain_log();
         hctl_->no_ftran = 0;
+        hctl_->no_ratio = unfused_ratio_ ? 1 : 0;
         hctl_->status = ST_HOLD;
         push();
     }
@@ -691,6 +717,7 @@ void Solver::step_compute_direction(int entering, double red) {
     hctl_->status = ST_RUNNING;
     hctl_->pending = 0;
     hctl_->no_ftran = 0;
+    hctl_->no_ratio = 1;
     push();
     launch_update(d_, st_);
     CK(cudaGetLastError());
@@ -958,6 +985,21 @@ int lpsg_profile_get(lpsg_solver* s, lpsg_kernel_stat* out, int cap, int* n) {
         out[k].algorithmic_bytes = s->s->kstat[k].bytes;
     }
     return LPSG_OK;
+}
+
+int lpsg_host_alloc(size_t bytes, void** out) {
+    if (!out) return bad("lpsg_host_alloc: null argument");
+    return guard([&] {
+        const cudaError_t e = cudaHostAlloc(out, std::max<size_t>(bytes, 16), cudaHostAllocPortable);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw lpsg::Error(LPSG_CUDA_ERROR, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+        }
+    });
+}
+
+void lpsg_host_free(void* p) {
+    if (p) cudaFreeHost(p);
 }
 
 int lpsg_last_solve_device_ms(lpsg_solver* s, double* ms) {

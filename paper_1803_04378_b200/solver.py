@@ -89,6 +89,7 @@ class SolverConfig:
     device: int = 0
     batch: int = 0
     use_graphs: bool = True
+    debug_flags: int = 0     # bit 0: standalone ratio kernel instead of the fused epilogue
     observer: Optional[Callable[["IterationView"], None]] = None
 
     def _c(self) -> L.Config:
@@ -98,6 +99,7 @@ class SolverConfig:
         c.ratio_tie_tol, c.max_iter = self.ratio_tie_tol, int(self.max_iter)
         c.anticycle, c.kernel, c.workers = int(self.anticycle), int(self.kernel), int(self.workers)
         c.device, c.batch, c.use_graphs = int(self.device), int(self.batch), int(self.use_graphs)
+        c.reserved[0] = int(self.debug_flags)
         return c
 
 
@@ -181,22 +183,57 @@ class GenSpec:
     form: Form = Form.equality
 
 
-def generate(spec: GenSpec) -> StandardFormLP:
-    """lps::generate (generator.cpp:35-72) + canonicalize, straight to standard form."""
+class PinnedBuffer:
+    """Page-locked host memory from the library (lpsg_host_alloc), exposed as numpy."""
+
+    def __init__(self, nbytes: int):
+        self.lib = L.load()
+        self.ptr = C.c_void_p()
+        _check(self.lib.lpsg_host_alloc(max(int(nbytes), 16), C.byref(self.ptr)))
+        self.nbytes = int(nbytes)
+
+    def array(self, shape, dtype) -> np.ndarray:
+        dtype = np.dtype(dtype)
+        n = int(np.prod(shape))
+        buf = (C.c_byte * (n * dtype.itemsize)).from_address(self.ptr.value)
+        a = np.frombuffer(buf, dtype=dtype, count=n).reshape(shape)
+        a.flags.writeable = True
+        return a
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                self.lib.lpsg_host_free(self.ptr)
+                self.ptr = C.c_void_p()
+        except Exception:
+            pass
+
+
+def generate(spec: GenSpec, pinned: bool = False) -> StandardFormLP:
+    """lps::generate (generator.cpp:35-72) + canonicalize, straight to standard form.
+    With pinned=True, A lives in page-locked memory (fast upload in lpsg_create)."""
     lib = L.load()
     n = lib.lpsg_generated_n_total(spec.rows, spec.cols, int(spec.form))
     if spec.rows <= 0 or spec.cols <= 0:
         raise DegenerateSpec("generate: rows and cols must be positive")
-    A = np.empty((spec.rows, n)); b = np.empty(spec.rows); c = np.empty(n)
+    keep = None
+    if pinned:
+        keep = PinnedBuffer(8 * spec.rows * n)
+        A = keep.array((spec.rows, n), np.float64)
+    else:
+        A = np.empty((spec.rows, n))
+    b = np.empty(spec.rows); c = np.empty(n)
     ck = np.empty(n, np.uint8)
     _check(lib.lpsg_generate(spec.rows, spec.cols, int(spec.sparsity), spec.seed, int(spec.form),
                              A.ctypes.data_as(C.POINTER(C.c_double)),
                              b.ctypes.data_as(C.POINTER(C.c_double)),
                              c.ctypes.data_as(C.POINTER(C.c_double)),
                              ck.ctypes.data_as(C.POINTER(C.c_uint8))))
-    return StandardFormLP(spec.rows, n, A, b, c, ck,
-                          name=f"{spec.rows}_{spec.cols}_{spec.form.name}_s{spec.seed}",
-                          objective_sign=1.0 if spec.form == Form.equality else -1.0)
+    lp = StandardFormLP(spec.rows, n, A, b, c, ck,
+                        name=f"{spec.rows}_{spec.cols}_{spec.form.name}_s{spec.seed}",
+                        objective_sign=1.0 if spec.form == Form.equality else -1.0)
+    lp._pinned = keep  # keeps the page-locked buffer alive with the LP
+    return lp
 
 
 class SimplexSolver:
