@@ -2,7 +2,7 @@
 """Benchmark: simplex iterations/s on BASELINE.json's headline config.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
-                    [--tto] [--no-cpu-baseline]
+                    [--e2e-max-iter N] [--no-cpu-baseline]
 
 A "step" is one pivot of the dense revised simplex (one pass of the hot path:
 ratio test, pivot row, pricing, fused update + FTRAN) on a synthetic LP from
@@ -43,7 +43,33 @@ CONFIGS = {
     "c5": dict(rows=24000, cols=48000, form=0, seed=1, cpu_pivots=5,
                label="C5 random dense LP m=24000 n=48000 (generator verbatim), seed 1"),
 }
-METRIC = "simplex iterations/sec, dense LP m=8000"
+def _metric():
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as f:
+            return json.load(f)["metric"]
+    except Exception:
+        return "simplex iterations/sec & time-to-optimal, dense LP m=8000 @1/2/4/8 B200"
+
+
+METRIC = _metric()
+NCU_NAMES = {"price": "k_price", "update_ftran": "k_update", "pivot": "k_pivot", "ratio": "k_ratio"}
+
+
+def _ncu_traffic(kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the newest committed
+    `ncu --set full` summary under profiles/ (tools/ncu_summary.py), or None."""
+    import glob
+    best = None
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")),
+                    key=os.path.getmtime):
+        try:
+            with open(p) as f:
+                cap = json.load(f).get("captures", {}).get(kernel)
+            if cap and cap.get("traffic_bytes"):
+                best = (cap["traffic_bytes"], os.path.basename(p))
+        except Exception:
+            pass
+    return best
 
 
 def _peaks():
@@ -202,6 +228,7 @@ def run_ours(args, cfg):
     for v in kern.values():
         v["share"] = round(v["ms_total"] / tot, 4)
     roofline = None
+    traffic = None
     if kern:
         dom = max(kern, key=lambda k: kern[k]["ms_total"])
         ach = kern[dom]["gbs"]
@@ -214,23 +241,38 @@ def run_ours(args, cfg):
                     "kernels": kern, "instrumented_pivots": prof_range,
                     "note": "per-kernel CUDA events on the solver stream over a second window of "
                             "K pivots; the headline value is the un-instrumented window"}
+        t = _ncu_traffic(NCU_NAMES.get(dom, dom))
+        if t is not None:
+            traffic = t[0]
+            roofline["traffic_source"] = f"profiles/{t[1]} (ncu --set full, one launch, DRAM read+write bytes)"
 
-    # ---- end to end through the public API with host buffers (A in pinned
-    # host memory, copied by lpsg_create; x read back by solve())
+    # ---- end to end through the public API with host buffers: lpsg_create
+    # uploads A from pinned host memory, solve() runs to optimality (or the
+    # --e2e-max-iter budget) and reads x back. This is also time-to-optimal.
     lp_pinned = make_lp(cfg, pinned=True)
     t0 = time.perf_counter()
-    s2 = P.SimplexSolver(lp_pinned, P.SolverConfig(max_iter=K, **scfg))
+    s2 = P.SimplexSolver(lp_pinned, P.SolverConfig(max_iter=args.e2e_max_iter, **scfg))
     rep2 = s2.solve()
     x = rep2.x  # solve() already read x back (device -> host)
     t1 = time.perf_counter()
     cnt = s2.counters()
+    tto_dev = s2.device_ms() / 1e3
     s2.close()
     e2e_val = rep2.iterations / (t1 - t0)
     e2e = {"value": e2e_val, "unit": "iterations/s",
            "h2d_bytes_per_step": cnt["h2d_bytes"] / max(1, rep2.iterations),
            "d2h_bytes_per_step": (cnt["d2h_bytes"] + 8 * len(x)) / max(1, rep2.iterations),
-           "includes": "lpsg_create (A upload from host), solve, x readback; "
-                       f"{rep2.iterations} pivots from the start basis; A in pinned host memory"}
+           "includes": "lpsg_create (A upload from pinned host memory), full solve, x readback; "
+                       f"{rep2.iterations} pivots from the start basis"}
+    tto = {"status": rep2.status.name, "objective": rep2.objective,
+           "iterations_phase1": rep2.iterations_phase1,
+           "iterations_phase2": rep2.iterations_phase2,
+           "seconds_e2e": t1 - t0, "seconds_solve": rep2.total_seconds,
+           "seconds_device": tto_dev,
+           "note": "e2e = create (A upload) + solve + x readback; solve = the reference's "
+                   "solve() clock boundary (solver.cpp:332,363)"}
+    if traffic is not None and roofline is not None:
+        roofline["traffic"] = traffic
 
     line = {
         "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": done,
@@ -243,6 +285,7 @@ def run_ours(args, cfg):
                    "parallelism": f"single GPU"},
         "roofline": roofline,
         "e2e": e2e,
+        "time_to_optimal": tto,
         "gpu_launches": c1["kernel_launches"] - c0["kernel_launches"],
         "clocks": clk.summary(),
     }
@@ -252,15 +295,6 @@ def run_ours(args, cfg):
                                 "kind": info["kind"],
                                 "sample": f"first {info['pivots']} pivots of the same LP "
                                           f"({info['seconds']:.2f} s, {info['lib']})"}
-    if args.tto:
-        t0 = time.perf_counter()
-        s3 = P.SimplexSolver(lp, P.SolverConfig(**scfg))
-        rep3 = s3.solve()
-        t_dev = s3.device_ms()
-        s3.close()
-        line["time_to_optimal"] = {"status": rep3.status.name, "objective": rep3.objective,
-                                   "iterations": rep3.iterations, "device_s": t_dev / 1e3,
-                                   "wall_s": time.perf_counter() - t0}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -272,7 +306,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--tto", action="store_true", help="also time a full solve to optimality")
+    ap.add_argument("--e2e-max-iter", type=int, default=0,
+                    help="pivot budget of the end-to-end solve (0 = to optimality)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=0, help="pivots per host check (0 = auto)")
     ap.add_argument("--debug-flags", type=int, default=0)
