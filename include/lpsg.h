@@ -68,8 +68,15 @@ typedef struct {
     int workers;           /* ignored */
     int device;            /* CUDA device ordinal, default 0 */
     int batch;             /* pivots enqueued per host check (0 = auto) */
-    int use_graphs;        /* capture pivot batches in CUDA graphs (default 1) */
+    int use_graphs;        /* reserved (CUDA-graph capture of pivot batches) */
     int reserved[6];
+    /* Sharded solve over NCCL, one process (or thread) per GPU:
+     * world_size > 1 makes this handle shard `rank`; every rank passes the same
+     * problem, config and nccl_id (from lpsg_nccl_unique_id on rank 0) and must
+     * make the same sequence of calls. world_size <= 1: single GPU. */
+    int world_size;
+    int rank;
+    unsigned char nccl_id[128];
 } lpsg_config;
 
 /* lps::SolveReport (solver.hpp:47-57); x is fetched with lpsg_get_x. */
@@ -124,7 +131,25 @@ int lpsg_set_observer(lpsg_solver* s, lpsg_observer cb, void* user);
 int lpsg_keep_trace(lpsg_solver* s, int keep);
 int lpsg_get_trace(lpsg_solver* s, lpsg_trace* out, long cap, long* len);
 
-/* ---- step API: SimplexSolver's public steps (solver.hpp:79-168) ---------- */
+/* ---- multi-GPU -------------------------
+ * NCCL unique id for lpsg_config.nccl_id (rank 0 creates it, the caller
+ * distributes it, e.g. over torch.distributed / MPI). */
+int lpsg_nccl_unique_id(unsigned char out[128]);
+/* One process, `shards` host threads: the sharded solver with in-process
+ * device-to-device exchanges. spread_devices = 0 puts every shard on
+ * cfg->device (parity testing on one GPU); 1 puts shard g on device
+ * (cfg->device + g) % device_count. Report, x (may be NULL) and trace (may be
+ * NULL) are shard 0's; all shards reach the same decisions. */
+int lpsg_solve_sharded(const lpsg_problem* lp, const lpsg_config* cfg, int shards, int spread_devices,
+                       lpsg_report* report, double* x, lpsg_trace* trace, long cap, long* len);
+/* Exchange accounting of this handle's shard: collectives issued and payload bytes. */
+int lpsg_comm_stats(lpsg_solver* s, long long* calls, double* bytes);
+/* Shard geometry: this handle's rows [row0, row0+rows) of T and pricing
+ * columns [col0, col1). */
+int lpsg_shard_info(lpsg_solver* s, int* world, int* rank, int* row0, int* rows, int* col0, int* col1);
+
+/* ---- step API: SimplexSolver's public steps (solver.hpp:79-168) ----------
+ * Single GPU only (a sharded handle returns LPSG_INVALID_ARGUMENT). */
 /* price (solver.cpp:79-129) */
 int lpsg_price(lpsg_solver* s, int* optimal, int* entering, double* reduced_cost);
 /* compute_direction (solver.cpp:131-136) */

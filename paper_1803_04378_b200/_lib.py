@@ -24,7 +24,8 @@ class Config(C.Structure):
     _fields_ = [("opt_tol", C.c_double), ("pivot_tol", C.c_double), ("feas_tol", C.c_double),
                 ("ratio_tie_tol", C.c_double), ("max_iter", C.c_long), ("anticycle", C.c_int),
                 ("kernel", C.c_int), ("workers", C.c_int), ("device", C.c_int),
-                ("batch", C.c_int), ("use_graphs", C.c_int), ("reserved", C.c_int * 6)]
+                ("batch", C.c_int), ("use_graphs", C.c_int), ("reserved", C.c_int * 6),
+                ("world_size", C.c_int), ("rank", C.c_int), ("nccl_id", C.c_ubyte * 128)]
 
 
 class Report(C.Structure):
@@ -81,6 +82,12 @@ SIGNATURES = [
     ("lpsg_counters", C.c_int, [_P, C.POINTER(C.c_long), C.POINTER(C.c_longlong),
                                 C.POINTER(C.c_longlong)]),
     ("lpsg_host_alloc", C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    ("lpsg_nccl_unique_id", C.c_int, [C.POINTER(C.c_ubyte)]),
+    ("lpsg_solve_sharded", C.c_int, [C.POINTER(Problem), C.POINTER(Config), C.c_int, C.c_int,
+                                     C.POINTER(Report), _PD, C.POINTER(Trace), C.c_long,
+                                     C.POINTER(C.c_long)]),
+    ("lpsg_comm_stats", C.c_int, [_P, C.POINTER(C.c_longlong), _PD]),
+    ("lpsg_shard_info", C.c_int, [_P, _PI, _PI, _PI, _PI, _PI, _PI]),
     ("lpsg_host_free", None, [C.c_void_p]),
     ("lpsg_generated_n_total", C.c_int, [C.c_int, C.c_int, C.c_int]),
     ("lpsg_generate", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, _PD, _PD, _PD,

@@ -18,8 +18,8 @@ OUT_DIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(OUT_DIR, "liblpsg.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["kernels.cu", "solver.cu", "generator.cpp"]
-HEADERS = ["device.cuh"]
+SOURCES = ["kernels.cu", "solver.cu", "comm.cu", "generator.cpp"]
+HEADERS = ["device.cuh", "comm.h"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-ffp-contract=off", "-Xptxas", "-v"]

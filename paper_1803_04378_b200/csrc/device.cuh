@@ -29,7 +29,25 @@ enum CtlStatus : int {
     ST_TIE = 3,          // ratio test tied under tabu: host runs select_leaving
     ST_ITER_LIMIT = 4,
     ST_PIVOT_ERR = 5,    // |y_rk| <= pivot_tol
-    ST_HOLD = 6          // step API / phase boundary: kernels idle
+    ST_HOLD = 6,         // step API / phase boundary: kernels idle
+    ST_OVERFLOW = 7      // sharded ratio test: a shard's local candidate list exceeds
+                         // kRatioMsgCap; the host gathers the full lists
+};
+
+// Sharded solves (world > 1): fixed-size messages exchanged by
+// all-gather after the local pricing and ratio passes.
+constexpr int kRatioMsgCap = 6;
+struct PriceMsg {
+    double z;
+    int j;
+    int pad;
+};
+struct RatioMsg {
+    double theta;   // local min ratio (valid when any)
+    int any;        // any eligible local row
+    int n;          // local candidates within the LOCAL window
+    int rows[kRatioMsgCap];
+    double ratios[kRatioMsgCap];
 };
 
 struct LogEntry {
@@ -69,6 +87,14 @@ struct Ctl {
 
 struct Dev {
     int m, n_total, n_work;
+    // sharding. world == 1: row0 = 0, mloc = m, col0 = 0, col1 = n_total.
+    int world, rank;
+    int row0, mloc;        // this shard's rows of T = [B^-1 | b_bar] and of Y
+    int col0, col1;        // this shard's pricing columns (original index range)
+    double* xbuf;          // world > 1: pivot row exchange, m+3 slots summed as int64 bits
+    PriceMsg* pmsg;        // world > 1: [0] local result, [1..world] gathered
+    RatioMsg* rmsg;        // world > 1: [0] local result, [1..world] gathered
+    double* cand_ratio;    // ratios of the candidates in cand (same order)
     long long ldT;
     long long ld_nb;
     double* T;
@@ -149,6 +175,10 @@ struct LookaheadDev {
     double* part_z;   // partials
     int* part_j;
     double* part_t;
+    PriceMsg* pm;     // K local (z, j) per candidate; world > 1: gathered into pm_all
+    PriceMsg* pm_all; // world x K
+    double* tl;       // K local theta'
+    double* tl_all;   // world x K
     int nblk;         // partial blocks per candidate
     int q;            // entering column
     double d;         // entering reduced cost
@@ -158,15 +188,31 @@ struct LookaheadDev {
 void configure_kernels(Dev& d);
 bool create_tensor_maps(Dev& d, CUtensorMap** dev_maps, int* count);
 void launch_init_tableau(const Dev& d, const double* b, cudaStream_t st);
-void launch_rebuild_top(const Dev& d, cudaStream_t st);
+// rebuild_top_row over this shard's rows, continuing the ascending-i chain
+// from `init` (nullptr: start at 0.0), into `out` (d.top: also zero the d slot).
+void launch_rebuild_top(const Dev& d, const double* init, double* out, cudaStream_t st);
 void launch_price(const Dev& d, cudaStream_t st);
+void launch_price_final(const Dev& d, cudaStream_t st);       // world > 1
+void launch_ratio_final(const Dev& d, cudaStream_t st);       // world > 1
+void launch_pivot_row(const Dev& d, cudaStream_t st);         // world > 1
 void launch_update(const Dev& d, cudaStream_t st);
 void launch_ratio(const Dev& d, cudaStream_t st);
 void launch_pivot(const Dev& d, cudaStream_t st);
 void launch_transpose(const double* A_rm, double* A_cm, int m, int n, long long ld, cudaStream_t st);
 void launch_build_nb_from(const Dev& d, const double* A_rm, int n_scan, cudaStream_t st);
-void launch_drive_scan(const Dev& d, int row, double* scratch, cudaStream_t st);
-void launch_lookahead(const Dev& d, LookaheadDev& la, cudaStream_t st);
+// drive-out: scan this shard's slots against g = B^-1 row (m doubles) -> ctl.found
+// (local min j); then, after the cross-shard min, the entering reduced cost.
+void launch_drive_scan(const Dev& d, const double* g, cudaStream_t st);
+void launch_drive_red(const Dev& d, cudaStream_t st);
+// lookahead phases; world > 1 exchanges between them (solver.cu)
+void launch_la_x(const Dev& d, LookaheadDev& la, cudaStream_t st);
+void launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st);
+void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int nsrc, cudaStream_t st);
+void launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st);
+void launch_la_score(const Dev& d, LookaheadDev& la, const double* tl, int nsrc, cudaStream_t st);
+// in-process shard exchange helpers (LocalComm): out[k] = sum_g in[g*n + k] / min_g
+void launch_sum_i64(const long long* in, int nsrc, size_t n, long long* out, cudaStream_t st);
+void launch_min_i32(const int* in, int nsrc, size_t n, int* out, cudaStream_t st);
 void launch_gather_row(const Dev& d, int i, double* out, cudaStream_t st);
 
 }  // namespace lpsg

@@ -63,6 +63,25 @@ __device__ void block_argmax(double& z, int& j) {
     }
 }
 
+__device__ __forceinline__ void warp_argmax(double& z, int& j) {
+    for (int o = 16; o > 0; o >>= 1) {
+        const double oz = __shfl_down_sync(0xffffffffu, z, o);
+        const int oj = __shfl_down_sync(0xffffffffu, j, o);
+        if (better(oz, oj, z, j)) { z = oz; j = oj; }
+    }
+}
+
+// price's outcome (solver.cpp:124-127) and the loop-top budget check (281).
+__device__ __forceinline__ void price_decide(const Dev& d, Ctl* c, bool budget_hit, double z, int j) {
+    if (budget_hit) {
+        c->status = ST_ITER_LIMIT;
+    } else {
+        c->q = j == INT_MAX ? -1 : j;
+        c->d = j == INT_MAX ? 0.0 : z;
+        if (j == INT_MAX || z <= d.opt_tol) c->status = ST_OPTIMAL;
+    }
+}
+
 // std::min(theta, r) semantics: r replaces theta only when r < theta (NaN never does).
 __device__ __forceinline__ double min_keep(double theta, double r) { return (r < theta) ? r : theta; }
 
@@ -96,11 +115,13 @@ __device__ bool last_block(unsigned int* ticket) {
 }
 
 // ---------------------------------------------------------------- init ---
+// Shard rows li < mloc hold global rows i = row0 + li: B^-1 = I, b_bar = b.
 __global__ void k_init_tableau(Dev d, const double* __restrict__ b) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < d.m) {
-        d.T[(size_t)i * d.ldT + i] = 1.0;
-        d.T[(size_t)d.m * d.ldT + i] = b[i];
+    const int li = blockIdx.x * blockDim.x + threadIdx.x;
+    if (li < d.mloc) {
+        const int i = d.row0 + li;
+        d.T[(size_t)i * d.ldT + li] = 1.0;
+        d.T[(size_t)d.m * d.ldT + li] = b[i];
     }
 }
 
@@ -132,34 +153,38 @@ __global__ void k_build_nb(const double* __restrict__ A_rm, Dev d, int n_scan) {
 // ------------------------------------------------------ rebuild_top_row ---
 // solver.cpp:318-329: W_j = sum_i c_B[i] * B^-1[i][j] (ascending i); obj likewise
 // over b_bar (column m). One output per lane of warp 0; 32x32 tiles of T are
-// staged through shared memory so the column walk stays coalesced.
-__global__ void k_rebuild_top(Dev d) {
+// staged through shared memory so the column walk stays coalesced. A shard
+// sums its own rows, continuing the chain from the previous shard's partials
+// (`init`), so the sharded result is the same sequential sum.
+__global__ void k_rebuild_top(Dev d, const double* __restrict__ init, double* __restrict__ out) {
     __shared__ double tile[32][33];
     __shared__ double cb[32];
     const int j0 = blockIdx.x * 32;
     const int ncols = d.m + 1;
+    const int mloc = d.mloc;
     const double* cost = phase_cost(d, d.ctl->phase);
     double acc = 0.0;
-    for (int i0 = 0; i0 < d.m; i0 += 32) {
+    if (init && threadIdx.y == 0 && j0 + (int)threadIdx.x < ncols) acc = init[j0 + threadIdx.x];
+    for (int i0 = 0; i0 < mloc; i0 += 32) {
         __syncthreads();
         for (int k = threadIdx.y; k < 32; k += blockDim.y) {
             const int j = j0 + k, i = i0 + threadIdx.x;
-            tile[k][threadIdx.x] = (j < ncols && i < d.m) ? d.T[(size_t)j * d.ldT + i] : 0.0;
+            tile[k][threadIdx.x] = (j < ncols && i < mloc) ? d.T[(size_t)j * d.ldT + i] : 0.0;
         }
         if (threadIdx.y == 0) {
             const int i = i0 + threadIdx.x;
-            cb[threadIdx.x] = i < d.m ? cost[d.basic[i]] : 0.0;
+            cb[threadIdx.x] = i < mloc ? cost[d.basic[d.row0 + i]] : 0.0;
         }
         __syncthreads();
         if (threadIdx.y == 0) {
-            const int lim = min(32, d.m - i0);
+            const int lim = min(32, mloc - i0);
             for (int k = 0; k < lim; ++k) acc = dadd(acc, dmul(cb[k], tile[threadIdx.x][k]));
         }
     }
     if (threadIdx.y == 0) {
         const int j = j0 + threadIdx.x;
-        if (j < ncols) d.top[j] = acc;
-        if (j == 0) d.top[d.m + 1] = 0.0;
+        if (j < ncols) out[j] = acc;
+        if (j == 0 && out == d.top) d.top[d.m + 1] = 0.0;
     }
 }
 
@@ -328,22 +353,31 @@ __global__ void __launch_bounds__(512) k_price(Dev d) {
             const int oj = ((volatile int*)d.pj)[b];
             if (better(oz, oj, z, j)) { z = oz; j = oj; }
         }
-        for (int o = 16; o > 0; o >>= 1) {
-            const double oz = __shfl_down_sync(0xffffffffu, z, o);
-            const int oj = __shfl_down_sync(0xffffffffu, j, o);
-            if (better(oz, oj, z, j)) { z = oz; j = oj; }
-        }
+        warp_argmax(z, j);
         if (threadIdx.x == 0) {
             c->ticket_price = 0;
-            if (budget_hit) {
-                c->status = ST_ITER_LIMIT;
+            if (d.world > 1) {
+                d.pmsg[0] = PriceMsg{z, j, 0};  // merged across shards by k_price_final
             } else {
-                c->q = j == INT_MAX ? -1 : j;
-                c->d = j == INT_MAX ? 0.0 : z;
-                if (j == INT_MAX || z <= d.opt_tol) c->status = ST_OPTIMAL;
+                price_decide(d, c, budget_hit, z, j);
             }
         }
     }
+}
+
+// world > 1: (max z, min j) over the gathered shard results, then the same
+// decision as the single-GPU epilogue. Exact, so independent of shard order.
+__global__ void k_price_final(Dev d) {
+    Ctl* c = d.ctl;
+    if (c->status != ST_RUNNING) return;
+    double z = -kInf;
+    int j = INT_MAX;
+    for (int g = threadIdx.x; g < d.world; g += 32) {
+        const PriceMsg mm = d.pmsg[1 + g];
+        if (better(mm.z, mm.j, z, j)) { z = mm.z; j = mm.j; }
+    }
+    warp_argmax(z, j);
+    if (threadIdx.x == 0) price_decide(d, c, c->total_iter >= c->budget, z, j);
 }
 
 // Update warps of k_update: warp-per-column, lane-per-row-pair (double2), rows
@@ -355,16 +389,16 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
                                             uint64_t* upd, size_t stage_stride, size_t tile_el,
                                             int nst, int S, int C, int h, int i0, int r, int U,
                                             bool up, int warp, int lane) {
-    const int m = d.m;
+    const int m = d.m, mloc = d.mloc;
     double ny0[NIT], ny1[NIT];
     bool ok[NIT];
 #pragma unroll
     for (int u = 0; u < NIT; ++u) {
         const int t = 2 * lane + 64 * u;
-        const int i = i0 + t;
+        const int i = i0 + t;  // local row
         ok[u] = t < h;
-        ny0[u] = (ok[u] && i < m && i != r) ? -d.Y[i] : 0.0;
-        ny1[u] = (ok[u] && i + 1 < m && i + 1 != r) ? -d.Y[i + 1] : 0.0;
+        ny0[u] = (ok[u] && i < mloc && i != r) ? -d.Y[i] : 0.0;
+        ny1[u] = (ok[u] && i + 1 < mloc && i + 1 != r) ? -d.Y[i + 1] : 0.0;
     }
     const size_t ldT = (size_t)d.ldT;
     double2* const gbase = reinterpret_cast<double2*>(d.T + i0) + lane;  // + col * ldT/2
@@ -424,9 +458,10 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
     const bool up = c->pending != 0;
     const bool ft = status == ST_RUNNING && !c->no_ftran && c->q >= 0;
     if (!up && !ft) return;
-    const int m = d.m, h = d.upd_h, C = d.upd_C, S = d.upd_S, U = d.upd_U;
+    const int m = d.m, mloc = d.mloc, h = d.upd_h, C = d.upd_C, S = d.upd_S, U = d.upd_U;
     const int F = (h + 31) >> 5;
-    const int r = c->upd_r;
+    // pivot row in shard-local numbering (-1: another shard owns it)
+    const int r = (c->upd_r >= d.row0 && c->upd_r < d.row0 + mloc) ? c->upd_r - d.row0 : -1;
     const int i0 = blockIdx.x * h;
     const int ncols = m + 1;
     const int nst = (ncols + C - 1) / C;
@@ -482,8 +517,8 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
     } else if (warp < U + F) {
         // ---- FTRAN warps: thread-per-row sequential chains over the updated tile
         const int t = threadIdx.x - U * 32;
-        const int i = i0 + t;
-        const bool valid = t < h && i < m;
+        const int i = i0 + t;  // local row
+        const bool valid = t < h && i < mloc;
         double acc = 0.0;
         int st = 0;
         uint32_t ph = 0;
@@ -540,7 +575,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         __shared__ int s_cnt[32];
         __shared__ double s_theta;
         __shared__ int s_any;
-        const int i = i0 + (threadIdx.x - U * 32);
+        const int i = d.row0 + i0 + (threadIdx.x - U * 32);  // global row
         bool elig = f_ok && !d.frozen[i] && !(f_y <= d.pivot_tol);
         const double ratio = elig ? ddiv(f_bbar, f_y) : kInf;
         const double th = block_min(elig ? ratio : kInf);
@@ -587,7 +622,15 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
     if (threadIdx.x == 0) { s_th2 = th; s_first = -1; }
     __syncthreads();
     if (!any) {
-        if (threadIdx.x == 0) c->status = ST_UNBOUNDED;
+        if (threadIdx.x == 0) {
+            if (d.world > 1) {
+                d.rmsg->any = 0;
+                d.rmsg->n = 0;
+                d.rmsg->theta = kInf;
+            } else {
+                c->status = ST_UNBOUNDED;
+            }
+        }
         return;
     }
     const double gth = s_th2;
@@ -595,10 +638,14 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
     constexpr int kMaxLocal = 8;
     int n = 0;
     int rows_keep[kMaxLocal];
+    double ratio_keep[kMaxLocal];
     for (int e = 0; e < cnt; ++e) {
         const double ra = __ldcg(d.rc_ratio + (size_t)b * h + e);
         if (ra <= window) {
-            if (n < kMaxLocal) rows_keep[n] = __ldcg(d.rc_row + (size_t)b * h + e);
+            if (n < kMaxLocal) {
+                rows_keep[n] = __ldcg(d.rc_row + (size_t)b * h + e);
+                ratio_keep[n] = ra;
+            }
             ++n;
         }
     }
@@ -626,21 +673,97 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
     if (n > 0) {
         if (pos == 0) s_first = n <= kMaxLocal ? rows_keep[0] : -2;
         if (n <= kMaxLocal) {
-            for (int e = 0; e < n; ++e) d.cand[pos + e] = rows_keep[e];
+            for (int e = 0; e < n; ++e) {
+                d.cand[pos + e] = rows_keep[e];
+                d.cand_ratio[pos + e] = ratio_keep[e];
+            }
         } else {
             for (int e = 0; e < cnt; ++e) {
                 const double ra = __ldcg(d.rc_ratio + (size_t)b * h + e);
-                if (ra <= window) d.cand[pos++] = __ldcg(d.rc_row + (size_t)b * h + e);
+                if (ra <= window) {
+                    d.cand_ratio[pos] = ra;
+                    d.cand[pos++] = __ldcg(d.rc_row + (size_t)b * h + e);
+                }
             }
         }
     }
     __syncthreads();
+    if (d.world > 1) {
+        // this shard's theta and its candidates within the shard-local window
+        // (a superset of its rows inside the global window): k_ratio_final merges
+        if (threadIdx.x < kRatioMsgCap) {
+            const int e = threadIdx.x;
+            const int total = s_pre[31];
+            RatioMsg* mm = d.rmsg;
+            mm->rows[e] = e < total ? ((volatile int*)d.cand)[e] : -1;
+            const double rv = e < total ? (double)((volatile double*)d.cand_ratio)[e] : (double)kInf;
+            mm->ratios[e] = rv;
+            if (e == 0) {
+                mm->theta = gth;
+                mm->any = 1;
+                mm->n = total;
+            }
+        }
+        return;
+    }
     if (threadIdx.x == 0) {
         const int total = s_pre[31];
         c->ncand = total;
         c->theta = gth;
         if (total == 1 || d.anticycle == 1)
             c->r = s_first >= 0 ? s_first : ((volatile int*)d.cand)[0];
+        else
+            c->status = ST_TIE;
+    }
+}
+
+// world > 1: global ratio test over the gathered shard messages
+// (solver.cpp:138-162). theta = min over shards (exact); shards are contiguous
+// row blocks in rank order, so concatenating their in-window candidates in rank
+// order is the ascending candidate list. A shard with more local candidates
+// than a message holds sends the host the full lists (ST_OVERFLOW).
+__global__ void k_ratio_final(Dev d) {
+    Ctl* c = d.ctl;
+    if (c->status != ST_RUNNING || c->no_ratio || c->no_ftran || c->q < 0) return;
+    const int g = threadIdx.x;  // one lane per shard (world <= 32)
+    const bool have = g < d.world;
+    RatioMsg mm;
+    if (have) mm = d.rmsg[1 + g];
+    const bool any_g = have && mm.any;
+    double th = any_g ? mm.theta : kInf;
+    for (int o = 16; o > 0; o >>= 1) th = min_keep(th, __shfl_xor_sync(0xffffffffu, th, o));
+    const unsigned anyb = __ballot_sync(0xffffffffu, any_g);
+    if (!anyb) {
+        if (g == 0) c->status = ST_UNBOUNDED;
+        return;
+    }
+    const double window = dadd(th, dmul(d.ratio_tie_tol, fmax(1.0, fabs(th))));
+    const bool over = any_g && mm.n > kRatioMsgCap;
+    int n = 0;
+    if (any_g && !over)
+        for (int e = 0; e < mm.n; ++e) n += mm.ratios[e] <= window;
+    const unsigned overb = __ballot_sync(0xffffffffu, over);
+    int incl = n;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (g >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    if (!overb && n > 0) {
+        int pos = incl - n;
+        for (int e = 0; e < mm.n; ++e)
+            if (mm.ratios[e] <= window) d.cand[pos++] = mm.rows[e];
+    }
+    __syncwarp();
+    if (g == 0) {
+        c->theta = th;
+        if (overb) {
+            c->status = ST_OVERFLOW;
+            return;
+        }
+        c->ncand = total;
+        if (total == 1 || d.anticycle == 1)
+            c->r = ((volatile int*)d.cand)[0];
         else
             c->status = ST_TIE;
     }
@@ -718,12 +841,42 @@ __global__ void __launch_bounds__(1024) k_ratio(Dev d) {
 // (IEEE '/'), apply the row-0 part of the update (W, obj and the d slot; the
 // multiplier is T[0][m+1], tiled_engine.cpp:240), swap the basis, maintain the
 // nonbasic pricing slots, and log the pivot (note_iteration's observer data).
+//
+// world > 1: the owner of row r divides it in k_pivot_row and the shards sum
+// their xbuf as int64 bit patterns (the others contribute 0), which delivers
+// the owner's doubles bit for bit; k_pivot then runs on every shard from xbuf.
+__global__ void __launch_bounds__(256) k_pivot_row(Dev d) {
+    Ctl* c = d.ctl;
+    if (c->status != ST_RUNNING) return;
+    const int m = d.m;
+    const int li = c->r - d.row0;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gstride = gridDim.x * blockDim.x;
+    long long* xb = reinterpret_cast<long long*>(d.xbuf);
+    if (li < 0 || li >= d.mloc) {
+        for (int j = gtid; j <= m + 2; j += gstride) xb[j] = 0;
+        return;
+    }
+    const double yr = d.Y[li];
+    const bool ok = fabs(yr) > d.pivot_tol;
+    for (int j = gtid; j <= m; j += gstride) {
+        const double xj = ddiv(d.T[(size_t)j * d.ldT + li], yr);
+        d.xbuf[j] = xj;
+        if (ok) d.T[(size_t)j * d.ldT + li] = xj;  // in place (solver.cpp:246-247)
+    }
+    if (gtid == 0) {
+        d.xbuf[m + 1] = ddiv(yr, yr);
+        d.xbuf[m + 2] = yr;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_pivot(Dev d) {
     Ctl* c = d.ctl;
     if (c->status != ST_RUNNING) return;
     const int m = d.m;
     const int r = c->r, q = c->q;
-    const double yr = d.Y[r];
+    const bool sharded = d.world > 1;
+    const double yr = sharded ? d.xbuf[m + 2] : d.Y[r];
     if (fabs(yr) <= d.pivot_tol) {
         if (blockIdx.x == 0 && threadIdx.x == 0) c->status = ST_PIVOT_ERR;
         return;
@@ -733,28 +886,37 @@ __global__ void __launch_bounds__(256) k_pivot(Dev d) {
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const int gstride = gridDim.x * blockDim.x;
     for (int j = gtid; j <= m; j += gstride) {
-        const double xj = ddiv(d.T[(size_t)j * d.ldT + r], yr);
-        d.xrow[j] = xj;
-        d.T[(size_t)j * d.ldT + r] = xj;  // in place, like pr[j] /= y_rk (solver.cpp:246-247)
+        double xj;
+        if (sharded) {
+            xj = d.xbuf[j];  // d.xrow == d.xbuf
+        } else {
+            xj = ddiv(d.T[(size_t)j * d.ldT + r], yr);
+            d.xrow[j] = xj;
+            d.T[(size_t)j * d.ldT + r] = xj;  // in place, like pr[j] /= y_rk (solver.cpp:246-247)
+        }
         const double p = dmul(ndk, xj);
         if (p != 0.0) d.top[j] = dadd(d.top[j], p);
     }
+    double xl = 0.0;
     if (gtid == 0) {
-        const double xl = ddiv(yr, yr);
-        d.xrow[m + 1] = xl;
-        const double p = dmul(ndk, xl);
-        if (p != 0.0) d.top[m + 1] = dadd(dk, p);
+        xl = sharded ? d.xbuf[m + 1] : ddiv(yr, yr);
+        if (!sharded) d.xrow[m + 1] = xl;
     }
-    // nonbasic slot maintenance: the leaving column takes the entering column's
-    // slot (or, for an artificial leaver, the last slot moves into it)
+    // nonbasic slot maintenance for this shard's columns [col0, col1): the
+    // leaving column takes the entering column's slot, or is appended when the
+    // entering column lives on another shard; an entering column whose leaver
+    // is not ours (artificial or another shard's) is removed by moving the
+    // last slot into its place.
     const int p_leave = d.basic[r];
     const int s_q = d.col2slot[q];
     const int n_scan = c->n_scan;
+    const bool p_local = p_leave < d.n_total && p_leave >= d.col0 && p_leave < d.col1;
+    const bool q_local = s_q >= 0;
     int dst = -1, src_col = -1;
-    if (p_leave < d.n_total) {
-        dst = s_q >= 0 ? s_q : n_scan;
+    if (p_local) {
+        dst = q_local ? s_q : n_scan;
         src_col = p_leave;
-    } else if (s_q >= 0 && s_q != n_scan - 1) {
+    } else if (q_local && s_q != n_scan - 1) {
         dst = s_q;
         src_col = d.slot2col[n_scan - 1];
     }
@@ -765,12 +927,19 @@ __global__ void __launch_bounds__(256) k_pivot(Dev d) {
     if (!last_block(&c->ticket_misc)) return;
     if (threadIdx.x == 0) {
         c->ticket_misc = 0;
+        // the d slot (T[0][m+1]) is every CTA's multiplier source: update it
+        // only after all of them have read it
+        {
+            const double x_l = sharded ? d.xbuf[m + 1] : ((volatile double*)d.xrow)[m + 1];
+            const double p = dmul(ndk, x_l);
+            if (p != 0.0) d.top[m + 1] = dadd(dk, p);
+        }
         int ns = n_scan;
-        if (p_leave < d.n_total) {
-            if (s_q < 0) ++ns;
+        if (p_local) {
+            if (!q_local) ++ns;
             d.slot2col[dst] = p_leave;
             d.col2slot[p_leave] = dst;
-        } else if (s_q >= 0) {
+        } else if (q_local) {
             if (dst >= 0) {
                 d.slot2col[dst] = src_col;
                 d.col2slot[src_col] = dst;
@@ -801,11 +970,12 @@ __global__ void __launch_bounds__(256) k_pivot(Dev d) {
 
 // --------------------------------------------------------- drive-out scan ---
 // solver.cpp:295-316: first j < n_total, nonbasic, with |dot(B^-1 row i, a_j)| >
-// pivot_tol (ascending i in the dot), as a min-j reduction; the last CTA also
-// computes the entering reduced cost dot(W, a_j) - c_j.
-__global__ void k_gather_row(Dev d, int i, double* out) {
+// pivot_tol (ascending i in the dot), as a min-j reduction over this shard's
+// slots into ctl.found (the host pre-sets INT_MAX; shards then take the min);
+// k_drive_red computes the entering reduced cost dot(W, a_j) - c_j.
+__global__ void k_gather_row(Dev d, int li, double* out) {
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k <= d.m; k += gridDim.x * blockDim.x)
-        out[k] = d.T[(size_t)k * d.ldT + i];
+        out[k] = d.T[(size_t)k * d.ldT + li];
 }
 
 __global__ void __launch_bounds__(256) k_drive_scan(Dev d, const double* __restrict__ g) {
@@ -827,20 +997,21 @@ __global__ void __launch_bounds__(256) k_drive_scan(Dev d, const double* __restr
         for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = min(best, sb[w]);
         atomicMin(&c->found, best);
     }
-    if (!last_block(&c->ticket_misc)) return;
-    if (threadIdx.x == 0) {
-        c->ticket_misc = 0;
-        const int j = ((volatile int*)&c->found)[0];
-        if (j == INT_MAX) {
-            c->found = -1;
-        } else {
-            const double* cost = phase_cost(d, c->phase);
-            const double* __restrict__ a = d.A_cm + (size_t)j * d.ld_cm;
-            double acc = 0.0;
-            for (int i = 0; i < m; ++i) acc = dadd(acc, dmul(d.top[i], a[i]));
-            c->found_red = dsub(acc, cost[j]);
-        }
+}
+
+__global__ void k_drive_red(Dev d) {
+    Ctl* c = d.ctl;
+    const int j = c->found;
+    if (j == INT_MAX) {
+        if (threadIdx.x == 0) c->found = -1;
+        return;
     }
+    if (threadIdx.x != 0) return;
+    const double* cost = phase_cost(d, c->phase);
+    const double* __restrict__ a = d.A_cm + (size_t)j * d.ld_cm;
+    double acc = 0.0;
+    for (int i = 0; i < d.m; ++i) acc = dadd(acc, dmul(d.top[i], a[i]));
+    c->found_red = dsub(acc, cost[j]);
 }
 
 // ------------------------------------------------------------ lookahead ---
@@ -848,18 +1019,28 @@ __global__ void __launch_bounds__(256) k_drive_scan(Dev d, const double* __restr
 // K pivoted tableaus: (1) X_k = T_r / piv, W'_k = W - d*X_k; (2) pricing of
 // W'_k over the nonbasic set with q removed and basic[r_k] added; (3) y'_ik =
 // sum_j (T_ij - y_i X_kj) a_best[j] (ascending j) and theta'_k; (4) score.
-__global__ void k_la_prep(Dev d, LookaheadDev la) {
+// Sharded: X_k comes from the owner of row r_k (int64 bit-pattern sum, like
+// k_pivot_row); pricing and theta' run over the shard's columns / rows and are
+// merged exactly (max/min) across shards.
+__global__ void k_la_x(Dev d, LookaheadDev la) {
     const int k = blockIdx.y;
-    const int r = la.rows[k];
-    const double piv = d.Y[r];
-    const double dk = d.top[d.m + 1];
+    const int li = la.rows[k] - d.row0;
+    const bool own = li >= 0 && li < d.mloc;
+    double* X = la.X + (size_t)k * la.ldx;
+    const double piv = own ? d.Y[li] : 0.0;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= d.m; j += gridDim.x * blockDim.x) {
-        const double xj = ddiv(d.T[(size_t)j * d.ldT + r], piv);
-        la.X[(size_t)k * la.ldx + j] = xj;
-        if (j < d.m) {
-            const double w = d.top[j];
-            la.Wp[(size_t)k * la.ldx + j] = dk == 0.0 ? w : dsub(w, dmul(dk, xj));
-        }
+        if (own) X[j] = ddiv(d.T[(size_t)j * d.ldT + li], piv);
+        else reinterpret_cast<long long*>(X)[j] = 0;
+    }
+}
+
+__global__ void k_la_wp(Dev d, LookaheadDev la) {
+    const int k = blockIdx.y;
+    const double dk = d.top[d.m + 1];
+    const double* X = la.X + (size_t)k * la.ldx;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d.m; j += gridDim.x * blockDim.x) {
+        const double w = d.top[j];
+        la.Wp[(size_t)k * la.ldx + j] = dk == 0.0 ? w : dsub(w, dmul(dk, X[j]));
     }
 }
 
@@ -880,10 +1061,11 @@ __global__ void __launch_bounds__(256) k_la_price(Dev d, LookaheadDev la) {
         const double z = dsub(acc, cost[j]);
         if (better(z, j, bz, bj)) { bz = z; bj = j; }
     }
-    // the leaving variable becomes nonbasic (solver.cpp:186-188)
+    // the leaving variable becomes nonbasic (solver.cpp:186-188); priced by the
+    // shard that owns its column
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         const int p = d.basic[la.rows[k]];
-        if (p < d.n_total && p != la.q) {
+        if (p < d.n_total && p != la.q && p >= d.col0 && p < d.col1) {
             const double* __restrict__ a = d.A_cm + (size_t)p * d.ld_cm;
             double acc = 0.0;
             for (int i = 0; i < m; ++i) acc = dadd(acc, dmul(w[i], a[i]));
@@ -898,7 +1080,7 @@ __global__ void __launch_bounds__(256) k_la_price(Dev d, LookaheadDev la) {
     }
 }
 
-__global__ void k_la_price_final(Dev d, LookaheadDev la) {
+__global__ void k_la_price_local(Dev d, LookaheadDev la) {
     const int k = blockIdx.x;
     if (threadIdx.x >= 32) return;
     double z = -kInf;
@@ -908,15 +1090,23 @@ __global__ void k_la_price_final(Dev d, LookaheadDev la) {
         const int oj = la.part_j[(size_t)k * la.nblk + b];
         if (better(oz, oj, z, j)) { z = oz; j = oj; }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-        const double oz = __shfl_down_sync(0xffffffffu, z, o);
-        const int oj = __shfl_down_sync(0xffffffffu, j, o);
-        if (better(oz, oj, z, j)) { z = oz; j = oj; }
+    warp_argmax(z, j);
+    if (threadIdx.x == 0) la.pm[k] = PriceMsg{z, j, 0};
+}
+
+// msgs: nsrc x K (shard-major); lookahead_score's "best_j" and its 0-score rule
+// (solver.cpp:190-201)
+__global__ void k_la_decide(Dev d, LookaheadDev la, const PriceMsg* __restrict__ msgs, int nsrc) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= la.K) return;
+    double z = -kInf;
+    int j = INT_MAX;
+    for (int g = 0; g < nsrc; ++g) {
+        const PriceMsg mm = msgs[(size_t)g * la.K + k];
+        if (better(mm.z, mm.j, z, j)) { z = mm.z; j = mm.j; }
     }
-    if (threadIdx.x == 0) {
-        la.bz[k] = z;
-        la.bj[k] = (j == INT_MAX || z <= d.opt_tol) ? -1 : j;
-    }
+    la.bz[k] = z;
+    la.bj[k] = (j == INT_MAX || z <= d.opt_tol) ? -1 : j;
 }
 
 __global__ void __launch_bounds__(128) k_la_theta(Dev d, LookaheadDev la) {
@@ -928,10 +1118,11 @@ __global__ void __launch_bounds__(128) k_la_theta(Dev d, LookaheadDev la) {
     const double* __restrict__ X = la.X + (size_t)k * la.ldx;
     const double* __restrict__ a = d.A_cm + (size_t)bj * d.ld_cm;
     double theta = kInf;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    for (int li = blockIdx.x * blockDim.x + threadIdx.x; li < d.mloc; li += gridDim.x * blockDim.x) {
+        const int i = d.row0 + li;
         if (d.frozen[i]) continue;
-        const double yi = d.Y[i];
-        const double* __restrict__ col = d.T + i;
+        const double yi = d.Y[li];
+        const double* __restrict__ col = d.T + li;
         double acc = 0.0;
         double bb;
         if (i == rk) {
@@ -952,21 +1143,48 @@ __global__ void __launch_bounds__(128) k_la_theta(Dev d, LookaheadDev la) {
     if (threadIdx.x == 0) la.part_t[(size_t)k * la.nblk + blockIdx.x] = theta;
 }
 
-__global__ void k_la_final(Dev d, LookaheadDev la) {
+__global__ void k_la_theta_local(Dev d, LookaheadDev la) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= la.K) return;
+    double t = kInf;
+    if (la.bj[k] >= 0)
+        for (int b = 0; b < la.nblk; ++b) t = min_keep(t, la.part_t[(size_t)k * la.nblk + b]);
+    la.tl[k] = t;
+}
+
+// tl: nsrc x K local theta' (shard-major); score = best_z * theta' (solver.cpp:211-212)
+__global__ void k_la_score(Dev d, LookaheadDev la, const double* __restrict__ tl, int nsrc) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= la.K) return;
     if (la.bj[k] < 0) { la.score[k] = 0.0; return; }
     double t = kInf;
-    for (int b = 0; b < la.nblk; ++b) t = min_keep(t, la.part_t[(size_t)k * la.nblk + b]);
+    for (int g = 0; g < nsrc; ++g) t = min_keep(t, tl[(size_t)g * la.K + k]);
     la.theta[k] = t;
     la.score[k] = isinf(t) ? kInf : dmul(la.bz[k], t);
+}
+
+// ------------------------------------------------- in-process exchange ---
+__global__ void k_sum_i64(const long long* __restrict__ in, int nsrc, size_t n, long long* out) {
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
+        long long v = 0;
+        for (int g = 0; g < nsrc; ++g) v += in[(size_t)g * n + k];
+        out[k] = v;
+    }
+}
+
+__global__ void k_min_i32(const int* __restrict__ in, int nsrc, size_t n, int* out) {
+    for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n; k += (size_t)gridDim.x * blockDim.x) {
+        int v = INT_MAX;
+        for (int g = 0; g < nsrc; ++g) v = min(v, in[(size_t)g * n + k]);
+        out[k] = v;
+    }
 }
 
 }  // namespace
 
 // ------------------------------------------------------------- launchers ---
 void launch_init_tableau(const Dev& d, const double* b, cudaStream_t st) {
-    k_init_tableau<<<(d.m + 255) / 256, 256, 0, st>>>(d, b);
+    k_init_tableau<<<(d.mloc + 255) / 256, 256, 0, st>>>(d, b);
 }
 
 void launch_transpose(const double* A_rm, double* A_cm, int m, int n, long long ld, cudaStream_t st) {
@@ -980,9 +1198,13 @@ void launch_build_nb_from(const Dev& d, const double* A_rm, int n_scan, cudaStre
     k_build_nb<<<grid, 256, 0, st>>>(A_rm, d, n_scan);
 }
 
-void launch_rebuild_top(const Dev& d, cudaStream_t st) {
-    k_rebuild_top<<<(d.m + 1 + 31) / 32, dim3(32, 8), 0, st>>>(d);
+void launch_rebuild_top(const Dev& d, const double* init, double* out, cudaStream_t st) {
+    k_rebuild_top<<<(d.m + 1 + 31) / 32, dim3(32, 8), 0, st>>>(d, init, out);
 }
+
+void launch_price_final(const Dev& d, cudaStream_t st) { k_price_final<<<1, 32, 0, st>>>(d); }
+
+void launch_ratio_final(const Dev& d, cudaStream_t st) { k_ratio_final<<<1, 32, 0, st>>>(d); }
 
 void launch_price(const Dev& d, cudaStream_t st) {
     k_price<<<d.price_grid, d.price_threads, d.price_smem, st>>>(d);
@@ -997,10 +1219,10 @@ void launch_update(const Dev& d, cudaStream_t st) {
 void configure_kernels(Dev& d) {
     const int G = d.num_sms;
     // update + FTRAN: h rows per CTA (even, so the TMA box row is a 16-byte multiple)
-    int h = (d.m + G - 1) / G;
+    int h = (d.mloc + G - 1) / G;
     h = std::min(256, std::max(2, (h + 1) & ~1));
     d.upd_h = h;
-    d.update_grid = (d.m + h - 1) / h;
+    d.update_grid = (d.mloc + h - 1) / h;
     d.upd_C = h <= 64 ? 32 : h <= 160 ? 16 : 8;
     d.upd_U = 8;
     const size_t tile_el = (size_t)d.upd_C * h;
@@ -1008,20 +1230,21 @@ void configure_kernels(Dev& d) {
     d.upd_S = (int)std::max<size_t>(2, std::min<size_t>(8, (size_t)(192 * 1024) / stage));
     d.upd_smem = (int)(d.upd_S * stage + 3 * d.upd_S * 8);
     d.upd_threads = (d.upd_U + (h + 31) / 32 + 1) * 32;
-    // pricing: one CTA per SM over contiguous slot ranges
-    const PriceGeom gm = price_geom(d.n_total, G);
+    // pricing: one CTA per SM over contiguous slot ranges of this shard's columns
+    const int ncols_local = d.col1 - d.col0;
+    const PriceGeom gm = price_geom(ncols_local, G);
     d.pivot_grid = std::max(1, std::min(2 * G, (d.m + 1 + 255) / 256));
     d.price_grid = G;
     d.price_nwc = (gm.w + 31) / 32;
     d.price_threads = (d.price_nwc + 1) * 32;
     d.price_stage_bytes = 0;
-    for (int n = 1; n <= d.n_total; n = (n < 64 ? n + 1 : n + n / 64)) {
+    for (int n = 1; n <= ncols_local; n = (n < 64 ? n + 1 : n + n / 64)) {
         const PriceGeom g = price_geom(n, G);
         const size_t st = (((size_t)g.R * g.w + g.R) * 8 + 1023) / 1024 * 1024;
         d.price_stage_bytes = std::max(d.price_stage_bytes, st);
     }
     {
-        const PriceGeom g = price_geom(d.n_total, G);
+        const PriceGeom g = price_geom(ncols_local, G);
         const size_t st = (((size_t)g.R * g.w + g.R) * 8 + 1023) / 1024 * 1024;
         d.price_stage_bytes = std::max(d.price_stage_bytes, st);
     }
@@ -1091,21 +1314,47 @@ void launch_ratio(const Dev& d, cudaStream_t st) { k_ratio<<<1, 1024, 0, st>>>(d
 
 void launch_pivot(const Dev& d, cudaStream_t st) { k_pivot<<<d.pivot_grid, 256, 0, st>>>(d); }
 
+void launch_pivot_row(const Dev& d, cudaStream_t st) { k_pivot_row<<<d.pivot_grid, 256, 0, st>>>(d); }
+
 void launch_gather_row(const Dev& d, int i, double* out, cudaStream_t st) {
     k_gather_row<<<(d.m + 1 + 255) / 256, 256, 0, st>>>(d, i, out);
 }
 
-void launch_drive_scan(const Dev& d, int row, double* scratch, cudaStream_t st) {
-    launch_gather_row(d, row, scratch, st);
-    k_drive_scan<<<d.price_grid, 256, 0, st>>>(d, scratch);
+void launch_drive_scan(const Dev& d, const double* g, cudaStream_t st) {
+    k_drive_scan<<<d.price_grid, 256, 0, st>>>(d, g);
 }
 
-void launch_lookahead(const Dev& d, LookaheadDev& la, cudaStream_t st) {
-    k_la_prep<<<dim3((d.m + 1 + 255) / 256, la.K), 256, 0, st>>>(d, la);
+void launch_drive_red(const Dev& d, cudaStream_t st) { k_drive_red<<<1, 32, 0, st>>>(d); }
+
+void launch_la_x(const Dev& d, LookaheadDev& la, cudaStream_t st) {
+    k_la_x<<<dim3((d.m + 1 + 255) / 256, la.K), 256, 0, st>>>(d, la);
+}
+
+void launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st) {
+    k_la_wp<<<dim3((d.m + 255) / 256, la.K), 256, 0, st>>>(d, la);
     k_la_price<<<dim3(la.nblk, la.K), 256, 0, st>>>(d, la);
-    k_la_price_final<<<la.K, 32, 0, st>>>(d, la);
+    k_la_price_local<<<la.K, 32, 0, st>>>(d, la);
+}
+
+void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int nsrc, cudaStream_t st) {
+    k_la_decide<<<(la.K + 127) / 128, 128, 0, st>>>(d, la, msgs, nsrc);
+}
+
+void launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     k_la_theta<<<dim3(la.nblk, la.K), 128, 0, st>>>(d, la);
-    k_la_final<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);
+    k_la_theta_local<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);
+}
+
+void launch_la_score(const Dev& d, LookaheadDev& la, const double* tl, int nsrc, cudaStream_t st) {
+    k_la_score<<<(la.K + 127) / 128, 128, 0, st>>>(d, la, tl, nsrc);
+}
+
+void launch_sum_i64(const long long* in, int nsrc, size_t n, long long* out, cudaStream_t st) {
+    k_sum_i64<<<(unsigned)std::min<size_t>(1024, (n + 255) / 256), 256, 0, st>>>(in, nsrc, n, out);
+}
+
+void launch_min_i32(const int* in, int nsrc, size_t n, int* out, cudaStream_t st) {
+    k_min_i32<<<(unsigned)std::min<size_t>(1024, (n + 255) / 256), 256, 0, st>>>(in, nsrc, n, out);
 }
 
 }  // namespace lpsg

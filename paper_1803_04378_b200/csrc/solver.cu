@@ -23,9 +23,11 @@
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
+#include <thread>
 #include <unordered_set>
 #include <vector>
 
+#include "comm.h"
 #include "device.cuh"
 #include "lpsg.h"
 
@@ -47,6 +49,7 @@ void ck(cudaError_t e, const char* what) {
     }
 }
 #define CK(x) ck((x), #x)
+#define CK_SET_DEVICE(dev) ::lpsg::ck(cudaSetDevice(dev), "cudaSetDevice")
 
 template <class T>
 T* dalloc(size_t n) {
@@ -64,7 +67,9 @@ long long round_up(long long v, long long a) { return (v + a - 1) / a * a; }
 
 class Solver {
 public:
-    Solver(const lpsg_problem& lp, const lpsg_config& cfg);
+    // comm == nullptr: single GPU. Otherwise this object is shard comm->rank of
+    // comm->size; every rank must make the same calls.
+    Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm = nullptr);
     ~Solver();
 
     void solve(lpsg_report* rep);
@@ -83,6 +88,7 @@ public:
     int n_total() const { return n_total_; }
     int n_work() const { return n_work_; }
     int phase() const { return phase_; }
+    const Dev& dev() const { return d_; }
     const std::vector<int>& basic() const { return basic_; }
 
     lpsg_observer observer = nullptr;
@@ -100,6 +106,13 @@ private:
     void drain_log();
     void note_pivot(const LogEntry& e);
     void enqueue_pivots(int n);
+    void seq_pivot();
+    void seq_price();
+    void seq_update();
+    void resume_with_row(int r);
+    std::vector<int> gather_overflow_candidates();
+    void single_gpu_only(const char* what) const;
+    int owner_of_row(int i) const;
     double objective_value();
 
     lpsg_config cfg_;
@@ -127,10 +140,13 @@ private:
     int n_tmaps_ = 0;
     int batch_ = 16;
     bool unfused_ratio_ = false;  // debug knob (cfg.reserved[0] & 1): standalone ratio kernel
+    Comm* comm_ = nullptr;
+    int world_ = 1, rank_ = 0;
+    double* chain_ = nullptr;     // world > 1: rebuild_top_row partial sums (m+1)
 
 public:
     // ---- counters and optional per-kernel CUDA-event profile
-    enum Kind { K_RATIO = 0, K_PIVOT, K_PRICE, K_UPDATE, K_OTHER, K_NUM };
+    enum Kind { K_RATIO = 0, K_PIVOT, K_PRICE, K_UPDATE, K_OTHER, K_COMM, K_NUM };
     struct KStat {
         long launches = 0;
         double ms = 0.0;
@@ -215,8 +231,8 @@ double Solver::bytes_of(int kind) const {
     const double m = m_;
     switch (kind) {
         case K_PRICE: return 8.0 * m * (double)n_scan_host_ + 8.0 * m;       // A_nb slots + W
-        case K_UPDATE: return 16.0 * m * (m + 1.0) + 16.0 * m;               // T read+write, y, a_q
-        case K_RATIO: return 16.0 * m;                                       // y, b_bar
+        case K_UPDATE: return 16.0 * d_.mloc * (m + 1.0) + 16.0 * d_.mloc;   // T read+write, y, a_q
+        case K_RATIO: return 16.0 * d_.mloc;                                 // y, b_bar
         case K_PIVOT: return 8.0 * (m + 1.0) * 3.0 + 16.0 * m;               // row r, x, W; slot copy
         default: return 0.0;
     }
@@ -234,7 +250,12 @@ void Solver::set_max_iter(long long v) {
     CK(cudaStreamSynchronize(st_));
 }
 
-Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(lp.m), n_total_(lp.n_total) {
+Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
+    : cfg_(cfg), m_(lp.m), n_total_(lp.n_total), comm_(comm) {
+    if (comm_) {
+        world_ = comm_->size;
+        rank_ = comm_->rank;
+    }
     if (lp.m <= 0 || lp.n_total <= 0)
         throw Error(LPSG_EMPTY_PROBLEM, "lpsg_create: problem has no rows or no columns");
     if (!lp.A || !lp.b || !lp.c || !lp.col_kind)
@@ -245,6 +266,8 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
         throw Error(LPSG_CUDA_ERROR, "lpsg_create: no CUDA device available (the solver has no CPU fallback)");
     }
     if (cfg.device < 0 || cfg.device >= ndev) throw Error(LPSG_INVALID_ARGUMENT, "lpsg_create: bad device ordinal");
+    if (world_ > lp.m || world_ > 32)
+        throw Error(LPSG_INVALID_ARGUMENT, "lpsg_create: more shards than rows (or than 32)");
     CK(cudaSetDevice(cfg.device));
     CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     const int m = m_, n = n_total_;
@@ -294,7 +317,15 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
     d_.m = m;
     d_.n_total = n;
     d_.n_work = n_work_;
-    d_.ld_nb = round_up(n, 32) + 32;
+    // shard geometry: contiguous row blocks of T, contiguous
+    // original-column blocks for pricing
+    d_.world = world_;
+    d_.rank = rank_;
+    d_.row0 = (int)((long long)m * rank_ / world_);
+    d_.mloc = (int)((long long)m * (rank_ + 1) / world_) - d_.row0;
+    d_.col0 = (int)((long long)n * rank_ / world_);
+    d_.col1 = (int)((long long)n * (rank_ + 1) / world_);
+    d_.ld_nb = round_up(std::max(1, d_.col1 - d_.col0), 32) + 32;
     d_.ld_cm = round_up(m, 4);
     d_.num_sms = prop.multiProcessorCount;
     d_.opt_tol = cfg_.opt_tol;
@@ -304,15 +335,21 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
     d_.anticycle = cfg_.anticycle;
     configure_kernels(d_);
     CK(cudaGetLastError());
-    d_.ldT = round_up(std::max<long long>(m + 1, (long long)d_.update_grid * d_.upd_h), 32);
-    unfused_ratio_ = (cfg_.reserved[0] & 1) != 0;
+    d_.ldT = round_up(std::max<long long>(d_.mloc + 1, (long long)d_.update_grid * d_.upd_h), 32);
+    unfused_ratio_ = world_ == 1 && (cfg_.reserved[0] & 1) != 0;
     batch_ = cfg_.batch > 0 ? cfg_.batch : (m <= 1024 ? 64 : m <= 4096 ? 16 : 4);
     d_.log_cap = batch_ + 8;
 
     d_.T = dalloc<double>((size_t)(m + 1) * d_.ldT + 64);
     d_.top = dalloc<double>(m + 520);  // + padding: TMA-side W segments may run past m+2
-    d_.Y = dalloc<double>(m);
+    d_.Y = dalloc<double>(d_.mloc);
     d_.xrow = dalloc<double>(m + 4);
+    if (world_ > 1) {
+        d_.xbuf = dalloc<double>(m + 4);
+        d_.pmsg = dalloc<PriceMsg>(world_ + 1);
+        d_.rmsg = dalloc<RatioMsg>(world_ + 1);
+        chain_ = dalloc<double>(m + 1);
+    }
     double* A_cm = dalloc<double>((size_t)n * d_.ld_cm + 64);
     d_.A_cm = A_cm;
     d_.A_nb = dalloc<double>((size_t)m * d_.ld_nb + 64);
@@ -325,6 +362,7 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
     d_.cost_true = cost_buf_ + n_work_;
     d_.ctl = dalloc<Ctl>(1);
     d_.cand = dalloc<int>(m);
+    d_.cand_ratio = dalloc<double>(m);
     d_.pz = dalloc<double>(d_.price_grid);
     d_.pj = dalloc<int>(d_.price_grid);
     d_.log = dalloc<LogEntry>(d_.log_cap);
@@ -332,7 +370,7 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
     d_.rc_cnt = dalloc<int>(d_.update_grid);
     d_.rc_row = dalloc<int>((size_t)d_.update_grid * d_.upd_h);
     d_.rc_ratio = dalloc<double>((size_t)d_.update_grid * d_.upd_h);
-    scratch_ = dalloc<double>(m + 2);
+    scratch_ = dalloc<double>(m + 4);
     if (!create_tensor_maps(d_, &tmaps_, &n_tmaps_))
         throw Error(LPSG_CUDA_ERROR, "lpsg_create: cuTensorMapEncodeTiled failed");
     CK(cudaMallocHost(&hctl_, sizeof(Ctl)));
@@ -345,7 +383,7 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
     std::vector<char> in_basis(n_work_, 0);
     for (int i = 0; i < m; ++i) in_basis[basic_[i]] = 1;
     std::vector<int> slot2col, col2slot(n, -1);
-    for (int j = 0; j < n; ++j)
+    for (int j = d_.col0; j < d_.col1; ++j)
         if (!in_basis[j]) {
             col2slot[j] = (int)slot2col.size();
             slot2col.push_back(j);
@@ -370,11 +408,18 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg) : cfg_(cfg), m_(l
     CK(cudaMemcpyAsync(d_.basic, basic_.data(), sizeof(int) * m, cudaMemcpyHostToDevice, st_));
     CK(cudaMemsetAsync(d_.frozen, 0, m, st_));
     CK(cudaMemcpyAsync(cost_buf_, cost.data(), sizeof(double) * cost.size(), cudaMemcpyHostToDevice, st_));
-    CK(cudaMemsetAsync(d_.Y, 0, sizeof(double) * m, st_));
+    CK(cudaMemsetAsync(d_.Y, 0, sizeof(double) * d_.mloc, st_));
     CK(cudaMemsetAsync(d_.top, 0, sizeof(double) * (m + 520), st_));
 
     // ---- initial Figure-1 tableau B = I, b_bar = b (solver.cpp:66-72)
     CK(cudaMemsetAsync(d_.T, 0, sizeof(double) * (size_t)(m + 1) * d_.ldT, st_));
+    if (world_ > 1) {
+        // the sharded pivot row travels in xbuf; k_update reads it as xrow
+        CK(cudaFree(d_.xrow));
+        d_.xrow = d_.xbuf;
+        CK(cudaMemsetAsync(d_.xbuf, 0, sizeof(double) * (m + 4), st_));
+        CK(cudaMemsetAsync(d_.rmsg, 0, sizeof(RatioMsg) * (world_ + 1), st_));
+    }
     CK(cudaMemcpyAsync(scratch_, lp.b, sizeof(double) * m, cudaMemcpyHostToDevice, st_));
     launch_init_tableau(d_, scratch_, st_);
 
@@ -397,7 +442,8 @@ Solver::~Solver() {
     if (st_) cudaStreamSynchronize(st_);
     void* bufs[] = {d_.T, d_.top, d_.Y, d_.xrow, (void*)d_.A_cm, d_.A_nb, d_.slot2col, d_.col2slot,
                     d_.basic, d_.frozen, cost_buf_, d_.ctl, d_.cand, d_.pz, d_.pj, d_.log, scratch_, tmaps_,
-                    d_.rc_theta, d_.rc_cnt, d_.rc_row, d_.rc_ratio};
+                    d_.rc_theta, d_.rc_cnt, d_.rc_row, d_.rc_ratio, d_.cand_ratio, d_.pmsg, d_.rmsg,
+                    chain_};
     for (void* p : bufs)
         if (p) cudaFree(p);
     if (hctl_) cudaFreeHost(hctl_);
@@ -431,9 +477,34 @@ double Solver::objective_value() {
     return v;
 }
 
+// rebuild_top_row (solver.cpp:318-329). Sharded: an ordered chain, shard g
+// continuing shard g-1's partial sums (an allreduce would reorder the sum).
 void Solver::rebuild_top_row() {
-    launch_rebuild_top(d_, st_);
-    CK(cudaGetLastError());
+    if (world_ == 1) {
+        launch_rebuild_top(d_, nullptr, d_.top, st_);
+        CK(cudaGetLastError());
+        return;
+    }
+    for (int g = 0; g < world_; ++g) {
+        if (g == rank_) launch_rebuild_top(d_, g == 0 ? nullptr : chain_, chain_, st_);
+        CK(cudaGetLastError());
+        comm_->bcast(chain_, sizeof(double) * (m_ + 1), g, st_);
+    }
+    CK(cudaMemcpyAsync(d_.top, chain_, sizeof(double) * (m_ + 1), cudaMemcpyDeviceToDevice, st_));
+    CK(cudaMemsetAsync(d_.top + m_ + 1, 0, sizeof(double), st_));
+}
+
+int Solver::owner_of_row(int i) const {
+    // inverse of row0(g) = floor(m g / G)
+    int g = (int)(((long long)i * world_ + world_ - 1) / std::max(1, m_));
+    g = std::min(std::max(g, 0), world_ - 1);
+    while (g > 0 && (long long)m_ * g / world_ > i) --g;
+    while (g + 1 < world_ && (long long)m_ * (g + 1) / world_ <= i) ++g;
+    return g;
+}
+
+void Solver::single_gpu_only(const char* what) const {
+    if (world_ > 1) throw Error(LPSG_INVALID_ARGUMENT, std::string(what) + ": step API is single-GPU only");
 }
 
 // note_iteration (solver.cpp:256-276) for one logged pivot.
@@ -441,7 +512,9 @@ void Solver::note_pivot(const LogEntry& e) {
     ++total_iter_;
     ++phase_iter_[phase_ - 1];
     basic_[e.row] = e.entering;
-    if (e.leaving >= n_total_) --n_scan_host_;
+    const bool q_local = e.entering >= d_.col0 && e.entering < d_.col1;
+    const bool p_local = e.leaving < n_total_ && e.leaving >= d_.col0 && e.leaving < d_.col1;
+    n_scan_host_ += (p_local ? 1 : 0) - (q_local ? 1 : 0);
     if (last_objective_ - e.objective > cfg_.opt_tol) banned_.clear();
     last_objective_ = e.objective;
     lpsg_trace t{(long)e.iteration, e.phase, e.row, e.leaving, e.entering, e.objective};
@@ -456,14 +529,83 @@ void Solver::drain_log() {
     hctl_->log_len = 0;
 }
 
+// One pivot's device work in the fused schedule; world > 1 adds the three
+// per-pivot exchanges: the pivot row from its owner, the
+// pricing (z, j) and the ratio-test messages.
+void Solver::seq_pivot() {
+    if (world_ == 1) {
+        L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot(d_, st_); });
+        return;
+    }
+    L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot_row(d_, st_); });
+    L(K_COMM, 0.0, [&] { comm_->sum_i64(reinterpret_cast<long long*>(d_.xbuf), (size_t)m_ + 3, st_); });
+    L(K_PIVOT, 0.0, [&] { launch_pivot(d_, st_); });
+}
+
+void Solver::seq_price() {
+    L(K_PRICE, bytes_of(K_PRICE), [&] { launch_price(d_, st_); });
+    if (world_ > 1) {
+        L(K_COMM, 0.0, [&] { comm_->allgather(d_.pmsg, d_.pmsg + 1, sizeof(PriceMsg), st_); });
+        L(K_OTHER, 0.0, [&] { launch_price_final(d_, st_); });
+    }
+}
+
+void Solver::seq_update() {
+    L(K_UPDATE, bytes_of(K_UPDATE), [&] { launch_update(d_, st_); });
+    if (world_ > 1) {
+        L(K_COMM, 0.0, [&] { comm_->allgather(d_.rmsg, d_.rmsg + 1, sizeof(RatioMsg), st_); });
+        L(K_OTHER, 0.0, [&] { launch_ratio_final(d_, st_); });
+    }
+}
+
 void Solver::enqueue_pivots(int n) {
     for (int k = 0; k < n; ++k) {
         if (unfused_ratio_) L(K_RATIO, bytes_of(K_RATIO), [&] { launch_ratio(d_, st_); });
-        L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot(d_, st_); });
-        L(K_PRICE, bytes_of(K_PRICE), [&] { launch_price(d_, st_); });
-        L(K_UPDATE, bytes_of(K_UPDATE), [&] { launch_update(d_, st_); });
+        seq_pivot();
+        seq_price();
+        seq_update();
     }
     CK(cudaGetLastError());
+}
+
+void Solver::resume_with_row(int r) {
+    hctl_->r = r;
+    hctl_->status = ST_RUNNING;
+    push();
+    seq_pivot();
+    seq_price();
+    seq_update();
+}
+
+// ST_OVERFLOW (world > 1): a shard had more local candidates than a RatioMsg
+// holds. Gather every shard's full local list and apply the global window on
+// the host with the device's formula (solver.cpp:154-160).
+std::vector<int> Solver::gather_overflow_candidates() {
+    const int G = world_;
+    std::vector<RatioMsg> msgs(G);
+    CK(cudaMemcpy(msgs.data(), d_.rmsg + 1, sizeof(RatioMsg) * G, cudaMemcpyDeviceToHost));
+    int maxn = 1;
+    for (auto& mm : msgs) maxn = std::max(maxn, mm.any ? mm.n : 0);
+    int* rows_d = dalloc<int>((size_t)G * maxn);
+    double* rat_d = dalloc<double>((size_t)G * maxn);
+    comm_->allgather(d_.cand, rows_d, sizeof(int) * maxn, st_);
+    comm_->allgather(d_.cand_ratio, rat_d, sizeof(double) * maxn, st_);
+    std::vector<int> rows((size_t)G * maxn);
+    std::vector<double> rat((size_t)G * maxn);
+    CK(cudaMemcpyAsync(rows.data(), rows_d, sizeof(int) * rows.size(), cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(rat.data(), rat_d, sizeof(double) * rat.size(), cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
+    cudaFree(rows_d);
+    cudaFree(rat_d);
+    const double th = hctl_->theta;
+    const double window = th + cfg_.ratio_tie_tol * std::max(1.0, std::fabs(th));
+    std::vector<int> cand;
+    for (int g = 0; g < G; ++g) {
+        if (!msgs[g].any) continue;
+        for (int e = 0; e < msgs[g].n; ++e)
+            if (rat[(size_t)g * maxn + e] <= window) cand.push_back(rows[(size_t)g * maxn + e]);
+    }
+    return cand;
 }
 
 // run_phase (solver.cpp:278-293) in the fused schedule.
@@ -475,8 +617,8 @@ int Solver::run_phase() {
     hctl_->log_len = 0;
     hctl_->phase = phase_;
     push();
-    L(K_PRICE, bytes_of(K_PRICE), [&] { launch_price(d_, st_); });  // price(W_t), first pivot of the phase
-    L(K_OTHER, 8.0 * m_ * (m_ + 1.0), [&] { launch_update(d_, st_); });  // standalone FTRAN (pending == 0)
+    seq_price();   // price(W_t), first pivot of the phase
+    seq_update();  // standalone FTRAN (pending == 0) + ratio test
     CK(cudaGetLastError());
     for (;;) {
         enqueue_pivots(batch_);
@@ -491,13 +633,14 @@ int Solver::run_phase() {
         if (st == ST_TIE) {
             std::vector<int> cand(hctl_->ncand);
             CK(cudaMemcpy(cand.data(), d_.cand, sizeof(int) * cand.size(), cudaMemcpyDeviceToHost));
-            const int r = select_leaving(cand, hctl_->q);
-            hctl_->r = r;
-            hctl_->status = ST_RUNNING;
-            push();
-            L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot(d_, st_); });
-            L(K_PRICE, bytes_of(K_PRICE), [&] { launch_price(d_, st_); });
-            L(K_UPDATE, bytes_of(K_UPDATE), [&] { launch_update(d_, st_); });
+            resume_with_row(select_leaving(cand, hctl_->q));
+            continue;
+        }
+        if (st == ST_OVERFLOW) {
+            const std::vector<int> cand = gather_overflow_candidates();
+            if (cand.empty()) throw Error(LPSG_CUDA_ERROR, "sharded ratio test lost its candidates");
+            resume_with_row(cand.size() == 1 || cfg_.anticycle == 1 ? cand.front()
+                                                                    : select_leaving(cand, hctl_->q));
             continue;
         }
         if (st == ST_PIVOT_ERR) throw Error(LPSG_PIVOT_TOO_SMALL, "pivot element below pivot_tol");
@@ -532,12 +675,15 @@ int Solver::select_leaving(const std::vector<int>& cand, int entering) {
     return chosen;
 }
 
-// lookahead_score (solver.cpp:164-213) for every row in `rows`, batched on the device.
+// lookahead_score (solver.cpp:164-213) for every row in `rows`, batched on the
+// device. Sharded: pivot rows from their owners, pricing and theta' per shard,
+// exact max / min merges (every rank computes the same scores).
 void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<double>& scores) {
     const int K = (int)rows.size();
     scores.assign(K, 0.0);
     if (K == 0) return;
     const int m = m_;
+    const int G = world_;
     const int ldx = (int)round_up(m + 1, 32);
     const size_t per = (size_t)2 * ldx * sizeof(double);
     const int kmax = (int)std::max<size_t>(1, std::min<size_t>(4096, ((size_t)2 << 30) / per));
@@ -545,7 +691,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     LookaheadDev la{};
     la.ldx = ldx;
     la.q = entering;
-    la.nblk = (int)std::min<long long>(64, std::max<long long>((hctl_->n_scan + 255) / 256, (m + 127) / 128));
+    la.nblk = (int)std::min<long long>(64, std::max<long long>((hctl_->n_scan + 255) / 256, (d_.mloc + 127) / 128));
     la.nblk = std::max(la.nblk, 1);
     int* rows_d = dalloc<int>(kb);
     la.rows = rows_d;
@@ -558,16 +704,30 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     la.part_z = dalloc<double>((size_t)kb * la.nblk);
     la.part_j = dalloc<int>((size_t)kb * la.nblk);
     la.part_t = dalloc<double>((size_t)kb * la.nblk);
+    la.pm = dalloc<PriceMsg>((size_t)kb);
+    la.pm_all = G > 1 ? dalloc<PriceMsg>((size_t)kb * G) : nullptr;
+    la.tl = dalloc<double>(kb);
+    la.tl_all = G > 1 ? dalloc<double>((size_t)kb * G) : nullptr;
+    CK(cudaMemsetAsync(la.X, 0, sizeof(double) * (size_t)kb * ldx, st_));
     for (int k0 = 0; k0 < K; k0 += kb) {
         la.K = std::min(kb, K - k0);
         CK(cudaMemcpyAsync(rows_d, rows.data() + k0, sizeof(int) * la.K, cudaMemcpyHostToDevice, st_));
-        launch_lookahead(d_, la, st_);
+        launch_la_x(d_, la, st_);
+        if (G > 1) comm_->sum_i64(reinterpret_cast<long long*>(la.X), (size_t)la.K * ldx, st_);
+        launch_la_price(d_, la, st_);
+        if (G > 1) comm_->allgather(la.pm, la.pm_all, sizeof(PriceMsg) * la.K, st_);
+        launch_la_decide(d_, la, G > 1 ? la.pm_all : la.pm, G, st_);
+        launch_la_theta(d_, la, st_);
+        if (G > 1) comm_->allgather(la.tl, la.tl_all, sizeof(double) * la.K, st_);
+        launch_la_score(d_, la, G > 1 ? la.tl_all : la.tl, G, st_);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(scores.data() + k0, la.score, sizeof(double) * la.K, cudaMemcpyDeviceToHost, st_));
         CK(cudaStreamSynchronize(st_));
     }
-    void* bufs[] = {rows_d, la.X, la.Wp, la.bz, la.bj, la.theta, la.score, la.part_z, la.part_j, la.part_t};
-    for (void* p : bufs) cudaFree(p);
+    void* bufs[] = {rows_d, la.X, la.Wp, la.bz, la.bj, la.theta, la.score, la.part_z, la.part_j, la.part_t,
+                    la.pm, la.pm_all, la.tl, la.tl_all};
+    for (void* p : bufs)
+        if (p) cudaFree(p);
 }
 
 // drive_out_artificials (solver.cpp:295-316)
@@ -577,7 +737,12 @@ void Solver::drive_out_artificials() {
         hctl_->found = INT_MAX;
         hctl_->status = ST_HOLD;
         push();
-        launch_drive_scan(d_, i, scratch_, st_);
+        const int owner = owner_of_row(i);
+        if (owner == rank_) launch_gather_row(d_, i - d_.row0, scratch_, st_);
+        if (world_ > 1) comm_->bcast(scratch_, sizeof(double) * (m_ + 1), owner, st_);
+        launch_drive_scan(d_, scratch_, st_);
+        if (world_ > 1) comm_->min_i32(&d_.ctl->found, 1, st_);
+        launch_drive_red(d_, st_);
         CK(cudaGetLastError());
         pull(false);
         const int found = hctl_->found;
@@ -597,10 +762,10 @@ void Solver::drive_out_artificials() {
         hctl_->no_ratio = 1;
         hctl_->log_len = 0;
         push();
-        launch_update(d_, st_);  // FTRAN only
-        launch_pivot(d_, st_);
+        seq_update();  // FTRAN only
+        seq_pivot();
         CK(cudaMemcpyAsync(&d_.ctl->no_ftran, hone_, sizeof(int), cudaMemcpyHostToDevice, st_));
-        launch_update(d_, st_);  // update only
+        seq_update();  // update only
         CK(cudaGetLastError());
         pull(true);
         if (hctl_->status == ST_PIVOT_ERR) throw Error(LPSG_PIVOT_TOO_SMALL, "pivot element below pivot_tol");
@@ -687,7 +852,24 @@ void Solver::get_x(double* x, int n) {
     std::fill(x, x + n, 0.0);
     if (solved_ && !(final_status_ == LPSG_OPTIMAL || final_status_ == LPSG_ITERATION_LIMIT)) return;
     std::vector<double> bbar(m_);
-    CK(cudaMemcpyAsync(bbar.data(), d_.T + (size_t)m_ * d_.ldT, sizeof(double) * m_, cudaMemcpyDeviceToHost, st_));
+    const double* bcol = d_.T + (size_t)m_ * d_.ldT;
+    if (world_ == 1) {
+        CK(cudaMemcpyAsync(bbar.data(), bcol, sizeof(double) * m_, cudaMemcpyDeviceToHost, st_));
+    } else {
+        // every shard's b_bar rows, padded to the largest shard, in rank order
+        const int pad = m_ / world_ + 1;
+        double* tmp = dalloc<double>((size_t)pad * (world_ + 1));
+        CK(cudaMemcpyAsync(tmp, bcol, sizeof(double) * d_.mloc, cudaMemcpyDeviceToDevice, st_));
+        comm_->allgather(tmp, tmp + pad, sizeof(double) * pad, st_);
+        std::vector<double> all((size_t)pad * world_);
+        CK(cudaMemcpyAsync(all.data(), tmp + pad, sizeof(double) * all.size(), cudaMemcpyDeviceToHost, st_));
+        CK(cudaStreamSynchronize(st_));
+        cudaFree(tmp);
+        for (int g = 0; g < world_; ++g) {
+            const int r0 = (int)((long long)m_ * g / world_), r1 = (int)((long long)m_ * (g + 1) / world_);
+            for (int i = r0; i < r1; ++i) bbar[i] = all[(size_t)g * pad + (i - r0)];
+        }
+    }
     d2h_bytes += 8LL * m_;
     CK(cudaStreamSynchronize(st_));
     for (int i = 0; i < m_; ++i)
@@ -696,6 +878,7 @@ void Solver::get_x(double* x, int n) {
 
 // ---- step API ---------------------------------------------------------------
 void Solver::step_price(int* optimal, int* entering, double* red) {
+    single_gpu_only("price");
     hctl_->status = ST_RUNNING;
     hctl_->budget = LLONG_MAX;
     push();
@@ -711,6 +894,7 @@ void Solver::step_price(int* optimal, int* entering, double* red) {
 }
 
 void Solver::step_compute_direction(int entering, double red) {
+    single_gpu_only("compute_direction");
     if (entering < 0 || entering >= n_total_) throw Error(LPSG_INVALID_ARGUMENT, "compute_direction: bad column");
     hctl_->q = entering;
     hctl_->d = red;
@@ -727,6 +911,7 @@ void Solver::step_compute_direction(int entering, double red) {
 }
 
 void Solver::step_ratio(int* unbounded, double* theta, std::vector<int>& cand) {
+    single_gpu_only("ratio_test");
     hctl_->status = ST_RUNNING;
     hctl_->pending = 0;
     push();
@@ -746,6 +931,7 @@ void Solver::step_ratio(int* unbounded, double* theta, std::vector<int>& cand) {
 }
 
 void Solver::step_pivot(int r, int q) {
+    single_gpu_only("pivot_update");
     if (r < 0 || r >= m_ || q < 0 || q >= n_work_) throw Error(LPSG_INVALID_ARGUMENT, "pivot_update: bad index");
     hctl_->r = r;
     hctl_->q = q;
@@ -778,9 +964,14 @@ void Solver::read_row(int i, double* out) {
     if (i == 0) {
         CK(cudaMemcpyAsync(out, d_.top, sizeof(double) * (m_ + 2), cudaMemcpyDeviceToHost, st_));
     } else {
-        launch_gather_row(d_, i - 1, scratch_, st_);
-        CK(cudaMemcpyAsync(out, scratch_, sizeof(double) * (m_ + 1), cudaMemcpyDeviceToHost, st_));
-        CK(cudaMemcpyAsync(out + m_ + 1, d_.Y + (i - 1), sizeof(double), cudaMemcpyDeviceToHost, st_));
+        const int owner = owner_of_row(i - 1);
+        if (owner == rank_) {
+            const int li = i - 1 - d_.row0;
+            launch_gather_row(d_, li, scratch_, st_);
+            CK(cudaMemcpyAsync(scratch_ + m_ + 1, d_.Y + li, sizeof(double), cudaMemcpyDeviceToDevice, st_));
+        }
+        if (world_ > 1) comm_->bcast(scratch_, sizeof(double) * (m_ + 2), owner, st_);
+        CK(cudaMemcpyAsync(out, scratch_, sizeof(double) * (m_ + 2), cudaMemcpyDeviceToHost, st_));
     }
     CK(cudaStreamSynchronize(st_));
 }
@@ -790,6 +981,7 @@ void Solver::read_row(int i, double* out) {
 // ============================================================== C ABI ===
 struct lpsg_solver {
     lpsg::Solver* s;
+    std::unique_ptr<lpsg::Comm> comm;
 };
 
 namespace {
@@ -801,6 +993,9 @@ int guard(F&& f) {
     } catch (const lpsg::Error& e) {
         lpsg::g_err = e.what();
         return e.code;
+    } catch (const lpsg::CommError& e) {
+        lpsg::g_err = e.what();
+        return LPSG_NCCL_ERROR;
     } catch (const std::bad_alloc&) {
         lpsg::g_err = "host out of memory";
         return LPSG_OUT_OF_MEMORY;
@@ -843,11 +1038,17 @@ int lpsg_create(const lpsg_problem* lp, const lpsg_config* cfg, lpsg_solver** ou
     lpsg_config c;
     if (cfg) c = *cfg;
     else lpsg_config_default(&c);
+    if (c.world_size > 1 && (c.rank < 0 || c.rank >= c.world_size)) return bad("lpsg_create: bad rank");
     return guard([&] {
-        auto* h = new lpsg_solver{nullptr};
+        auto* h = new lpsg_solver{nullptr, nullptr};
         try {
-            h->s = new lpsg::Solver(*lp, c);
+            if (c.world_size > 1) {
+                h->comm = lpsg::make_nccl_comm(c.nccl_id, c.rank, c.world_size, c.device);
+                if (!h->comm) throw lpsg::CommError("NCCL communicator");
+            }
+            h->s = new lpsg::Solver(*lp, c, h->comm.get());
         } catch (...) {
+            delete h->s;
             delete h;
             throw;
         }
@@ -868,7 +1069,86 @@ int lpsg_get_x(lpsg_solver* s, double* x, int n) {
 void lpsg_destroy(lpsg_solver* s) {
     if (!s) return;
     delete s->s;
+    s->comm.reset();
     delete s;
+}
+
+int lpsg_nccl_unique_id(unsigned char out[128]) {
+    if (!out) return bad("lpsg_nccl_unique_id: null argument");
+    std::string err;
+    if (!lpsg::nccl_unique_id(out, &err)) {
+        lpsg::g_err = "lpsg_nccl_unique_id: " + err;
+        return LPSG_NCCL_ERROR;
+    }
+    return LPSG_OK;
+}
+
+int lpsg_solve_sharded(const lpsg_problem* lp, const lpsg_config* cfg, int shards, int spread, lpsg_report* rep,
+                       double* x, lpsg_trace* trace, long cap, long* len) {
+    if (!lp || !rep || shards < 1 || shards > 32) return bad("lpsg_solve_sharded: bad argument");
+    lpsg_config c;
+    if (cfg) c = *cfg;
+    else lpsg_config_default(&c);
+    const int ndev = lpsg_device_count();
+    if (ndev <= 0) {
+        lpsg::g_err = "lpsg_solve_sharded: no CUDA device available (the solver has no CPU fallback)";
+        return LPSG_CUDA_ERROR;
+    }
+    lpsg::LocalHub hub(shards);
+    std::vector<int> rc(shards, LPSG_OK);
+    std::vector<std::string> msg(shards);
+    std::vector<std::thread> th;
+    for (int g = 0; g < shards; ++g) {
+        th.emplace_back([&, g] {
+            lpsg_config cg = c;
+            cg.world_size = 1;  // the in-process comm below, not NCCL
+            cg.device = spread ? (c.device + g) % ndev : c.device;
+            rc[g] = guard([&] {
+                CK_SET_DEVICE(cg.device);
+                std::unique_ptr<lpsg::Comm> comm = lpsg::make_local_comm(&hub, g);
+                lpsg::Solver s(*lp, cg, comm.get());
+                s.keep_trace = g == 0 && trace != nullptr;
+                lpsg_report r{};
+                s.solve(&r);
+                std::vector<double> xv(lp->n_total);
+                s.get_x(xv.data(), lp->n_total);
+                if (g == 0) {
+                    *rep = r;
+                    if (x) std::copy(xv.begin(), xv.end(), x);
+                    if (len) *len = (long)s.trace.size();
+                    if (trace)
+                        for (long k = 0; k < std::min<long>(cap, (long)s.trace.size()); ++k) trace[k] = s.trace[k];
+                }
+            });
+            msg[g] = lpsg::g_err;
+        });
+    }
+    for (auto& t : th) t.join();
+    for (int g = 0; g < shards; ++g)
+        if (rc[g] != LPSG_OK) {
+            lpsg::g_err = "shard " + std::to_string(g) + ": " + msg[g];
+            return rc[g];
+        }
+    return LPSG_OK;
+}
+
+int lpsg_comm_stats(lpsg_solver* s, long long* calls, double* bytes) {
+    if (!s) return bad("lpsg_comm_stats: null solver");
+    if (calls) *calls = s->comm ? s->comm->calls : 0;
+    if (bytes) *bytes = s->comm ? s->comm->bytes : 0.0;
+    return LPSG_OK;
+}
+
+int lpsg_shard_info(lpsg_solver* s, int* world, int* rank, int* row0, int* rows, int* col0, int* col1) {
+    if (!s) return bad("lpsg_shard_info: null solver");
+    const lpsg::Dev& d = s->s->dev();
+    if (world) *world = d.world;
+    if (rank) *rank = d.rank;
+    if (row0) *row0 = d.row0;
+    if (rows) *rows = d.mloc;
+    if (col0) *col0 = d.col0;
+    if (col1) *col1 = d.col1;
+    return LPSG_OK;
 }
 
 int lpsg_two_phase_solve(const lpsg_problem* lp, const lpsg_config* cfg, lpsg_report* rep, double* x) {
@@ -976,7 +1256,7 @@ int lpsg_profile(lpsg_solver* s, int enable) {
 
 int lpsg_profile_get(lpsg_solver* s, lpsg_kernel_stat* out, int cap, int* n) {
     if (!s || !n) return bad("lpsg_profile_get: null argument");
-    static const char* names[] = {"ratio", "pivot", "price", "update_ftran", "other"};
+    static const char* names[] = {"ratio", "pivot", "price", "update_ftran", "other", "exchange"};
     *n = lpsg::Solver::K_NUM;
     for (int k = 0; out && k < std::min(cap, (int)lpsg::Solver::K_NUM); ++k) {
         out[k].name = names[k];

@@ -91,6 +91,11 @@ class SolverConfig:
     use_graphs: bool = True
     debug_flags: int = 0     # bit 0: standalone ratio kernel instead of the fused epilogue
     observer: Optional[Callable[["IterationView"], None]] = None
+    # sharded solve over NCCL: one process per GPU, same problem
+    # and config on every rank, nccl_id from nccl_unique_id() on rank 0
+    world_size: int = 1
+    rank: int = 0
+    nccl_id: bytes = b""
 
     def _c(self) -> L.Config:
         c = L.Config()
@@ -100,6 +105,11 @@ class SolverConfig:
         c.anticycle, c.kernel, c.workers = int(self.anticycle), int(self.kernel), int(self.workers)
         c.device, c.batch, c.use_graphs = int(self.device), int(self.batch), int(self.use_graphs)
         c.reserved[0] = int(self.debug_flags)
+        c.world_size, c.rank = int(self.world_size), int(self.rank)
+        if self.nccl_id:
+            if len(self.nccl_id) != 128:
+                raise Error("nccl_id must be 128 bytes")
+            C.memmove(c.nccl_id, bytes(self.nccl_id), 128)
         return c
 
 
@@ -317,6 +327,16 @@ class SimplexSolver:
         _check(self.lib.lpsg_last_solve_device_ms(self._h, C.byref(v)))
         return v.value
 
+    def comm_stats(self) -> dict:
+        n, b = C.c_longlong(), C.c_double()
+        _check(self.lib.lpsg_comm_stats(self._h, C.byref(n), C.byref(b)))
+        return dict(calls=n.value, bytes=b.value)
+
+    def shard_info(self) -> dict:
+        v = [C.c_int() for _ in range(6)]
+        _check(self.lib.lpsg_shard_info(self._h, *[C.byref(x) for x in v]))
+        return dict(zip(("world", "rank", "row0", "rows", "col0", "col1"), (x.value for x in v)))
+
     def counters(self) -> dict:
         a, b, c = C.c_long(), C.c_longlong(), C.c_longlong()
         _check(self.lib.lpsg_counters(self._h, C.byref(a), C.byref(b), C.byref(c)))
@@ -395,3 +415,32 @@ def two_phase_solve(lp: StandardFormLP, cfg: Optional[SolverConfig] = None) -> S
 
 def device_count() -> int:
     return L.load().lpsg_device_count()
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId for SolverConfig.nccl_id (call on rank 0, share with the others)."""
+    buf = (C.c_ubyte * 128)()
+    _check(L.load().lpsg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def solve_sharded(lp: StandardFormLP, cfg: Optional[SolverConfig] = None, shards: int = 2,
+                  spread_devices: bool = False, trace: bool = False):
+    """The sharded solver in one process: `shards` host threads with in-process
+    device-to-device exchanges (all on cfg.device, or spread over the visible
+    GPUs). Returns (SolveReport, trace or None) of shard 0."""
+    cfg = cfg or SolverConfig()
+    lib = L.load()
+    rep = L.Report()
+    x = np.zeros(lp.n_total)
+    cap = 50 * (lp.m + 2 * lp.n_total) + 16 if trace else 0
+    tr = np.zeros(cap, TRACE_DTYPE)
+    n = C.c_long()
+    prob = lp._c()
+    _check(lib.lpsg_solve_sharded(C.byref(prob), C.byref(cfg._c()), int(shards), int(spread_devices),
+                                  C.byref(rep), x.ctypes.data_as(C.POINTER(C.c_double)),
+                                  tr.ctypes.data_as(C.POINTER(L.Trace)) if trace else None, cap,
+                                  C.byref(n)))
+    out = SolveReport(SolveStatus(rep.status), rep.objective, x, rep.iterations_phase1,
+                      rep.iterations_phase2, rep.total_seconds, rep.tpi_seconds)
+    return out, (tr[: min(n.value, cap)].copy() if trace else None)
