@@ -180,32 +180,81 @@ def run_reference_arm(args, cfg):
     print(json.dumps(line), flush=True)
 
 
-def run_ours(args, cfg):
-    import paper_1803_04378_b200 as P
+# ---- multi-GPU control plane (torchrun: one process per GPU). The solver's
+# data path is NCCL inside liblpsg; torch.distributed (gloo) only hands out the
+# NCCL unique id and takes the max of the per-rank device times.
+def dist_ctx():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
     if world > 1:
-        raise SystemExit("multi-GPU sharding is not implemented yet (single-GPU solver only)")
-    device = 0
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            dist.init_process_group("gloo")
+    return world, rank, local
+
+
+def share_nccl_id(world: int, rank: int) -> bytes:
+    """A fresh NCCL unique id from rank 0, identical on every rank."""
+    import paper_1803_04378_b200 as P
+    import torch.distributed as dist
+    obj = [P.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def max_over_ranks(v: float, world: int) -> float:
+    if world == 1:
+        return float(v)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int) -> None:
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def solver_config(P, args, world, rank, local, **kw):
+    extra = {}
+    if world > 1:
+        extra = dict(world_size=world, rank=rank, nccl_id=share_nccl_id(world, rank))
+    return P.SolverConfig(device=local if world > 1 else 0, batch=args.batch,
+                          debug_flags=args.debug_flags, **extra, **kw)
+
+
+def run_ours(args, cfg):
+    import paper_1803_04378_b200 as P
+    world, rank, local = dist_ctx()
+    device = local if world > 1 else 0
     lp = make_lp(cfg)
     W, K = args.warmup, args.steps
 
     # ---- device-resident timing: W warm-up pivots, then K timed pivots (the
     # value; no per-kernel events), then K more pivots with per-kernel CUDA
-    # events on the solver stream (the roofline).
-    scfg = dict(device=device, batch=args.batch, debug_flags=args.debug_flags)
-    s = P.SimplexSolver(lp, P.SolverConfig(max_iter=W, **scfg))
+    # events on the solver stream (the roofline). The time is the max over ranks
+    # of each rank's CUDA-event span on its solver stream.
+    s = P.SimplexSolver(lp, solver_config(P, args, world, rank, local, max_iter=W))
     s.solve()
     c0 = s.counters()
+    x0 = s.comm_stats()
     s.set_max_iter(W + K)
+    barrier(world)
     with ClockSampler(device) as clk:
         rep = s.solve()
-    dev_ms = s.device_ms()
+    barrier(world)
+    dev_ms = max_over_ranks(s.device_ms(), world)
     c1 = s.counters()
+    x1 = s.comm_stats()
     done = rep.iterations - W
     value = done / (dev_ms / 1e3)
     stats = {}
     prof_range = None
+    done_p = 0
     if not args.no_profile:
         s.set_max_iter(W + 2 * K)
         s.profile(True)
@@ -215,14 +264,14 @@ def run_ours(args, cfg):
         done_p = rep_p.iterations - W - done
     s.close()
 
-    # ---- roofline of the dominant kernel
+    # ---- roofline of the dominant kernel (per GPU) and of the whole pivot
     peak, peak_kind = _peaks()
     kern = {}
     for name, st in stats.items():
         if st["launches"] and st["ms"] > 0:
             kern[name] = dict(launches=st["launches"], ms_total=round(st["ms"], 4),
                               us_per_launch=round(1e3 * st["ms"] / st["launches"], 3),
-                              gbs=round(st["bytes"] / (st["ms"] / 1e3) / 1e9, 1),
+                              gbs=round(st["bytes"] / (st["ms"] / 1e3) / 1e9, 1) if st["bytes"] else None,
                               share=None)
     tot = sum(v["ms_total"] for v in kern.values()) or 1.0
     for v in kern.values():
@@ -230,49 +279,65 @@ def run_ours(args, cfg):
     roofline = None
     traffic = None
     if kern:
-        dom = max(kern, key=lambda k: kern[k]["ms_total"])
+        hbm = {k: v for k, v in kern.items() if v["gbs"]}
+        dom = max(hbm, key=lambda k: hbm[k]["ms_total"])
         ach = kern[dom]["gbs"]
+        # algorithmic bytes of one pivot on this rank; the whole job moves world x that
         pivot_bytes = sum(stats[k]["bytes"] for k in stats) / max(1, done_p)
+        job_gbs = pivot_bytes * world * value / 1e9
         roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                     "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_kind,
-                    "per_pivot": {"algorithmic_bytes": pivot_bytes,
-                                  "achieved_gbs": round(pivot_bytes * value / 1e9, 1),
-                                  "frac": round(pivot_bytes * value / 1e9 / peak, 4)},
+                    "per_pivot": {"algorithmic_bytes_per_gpu": pivot_bytes,
+                                  "achieved_gbs_per_gpu": round(job_gbs / world, 1),
+                                  "frac": round(job_gbs / world / peak, 4)},
                     "kernels": kern, "instrumented_pivots": prof_range,
                     "note": "per-kernel CUDA events on the solver stream over a second window of "
-                            "K pivots; the headline value is the un-instrumented window"}
+                            "K pivots (rank 0); the headline value is the un-instrumented window"}
         t = _ncu_traffic(NCU_NAMES.get(dom, dom))
-        if t is not None:
+        if t is not None and world == 1:
             traffic = t[0]
             roofline["traffic_source"] = f"profiles/{t[1]} (ncu --set full, one launch, DRAM read+write bytes)"
+        if traffic is not None:
+            roofline["traffic"] = traffic
+    exchange = None
+    if world > 1:
+        calls = (x1["calls"] - x0["calls"]) / max(1, done)
+        nbytes = (x1["bytes"] - x0["bytes"]) / max(1, done)
+        ex = kern.get("exchange")
+        exchange = {"transport": "NCCL (NVLink/NVSwitch)", "collectives_per_pivot": round(calls, 2),
+                    "payload_bytes_per_pivot_per_rank": round(nbytes, 1),
+                    "us_per_pivot": round(1e3 * ex["ms_total"] / max(1, done_p), 2) if ex else None,
+                    "note": "per pivot: pivot-row int64 allreduce (m+3 words), (z, j) all-gather, "
+                            "ratio-message all-gather"}
 
     # ---- end to end through the public API with host buffers: lpsg_create
     # uploads A from pinned host memory, solve() runs to optimality (or the
     # --e2e-max-iter budget) and reads x back. This is also time-to-optimal.
     lp_pinned = make_lp(cfg, pinned=True)
+    cfg2 = solver_config(P, args, world, rank, local, max_iter=args.e2e_max_iter)
+    barrier(world)
     t0 = time.perf_counter()
-    s2 = P.SimplexSolver(lp_pinned, P.SolverConfig(max_iter=args.e2e_max_iter, **scfg))
+    s2 = P.SimplexSolver(lp_pinned, cfg2)
     rep2 = s2.solve()
     x = rep2.x  # solve() already read x back (device -> host)
     t1 = time.perf_counter()
     cnt = s2.counters()
-    tto_dev = s2.device_ms() / 1e3
+    tto_dev = max_over_ranks(s2.device_ms() / 1e3, world)
     s2.close()
-    e2e_val = rep2.iterations / (t1 - t0)
+    wall = max_over_ranks(t1 - t0, world)
+    e2e_val = rep2.iterations / wall
     e2e = {"value": e2e_val, "unit": "iterations/s",
            "h2d_bytes_per_step": cnt["h2d_bytes"] / max(1, rep2.iterations),
            "d2h_bytes_per_step": (cnt["d2h_bytes"] + 8 * len(x)) / max(1, rep2.iterations),
            "includes": "lpsg_create (A upload from pinned host memory), full solve, x readback; "
-                       f"{rep2.iterations} pivots from the start basis"}
+                       f"{rep2.iterations} pivots from the start basis; max over ranks"}
     tto = {"status": rep2.status.name, "objective": rep2.objective,
            "iterations_phase1": rep2.iterations_phase1,
            "iterations_phase2": rep2.iterations_phase2,
-           "seconds_e2e": t1 - t0, "seconds_solve": rep2.total_seconds,
+           "seconds_e2e": wall, "seconds_solve": rep2.total_seconds,
            "seconds_device": tto_dev,
            "note": "e2e = create (A upload) + solve + x readback; solve = the reference's "
                    "solve() clock boundary (solver.cpp:332,363)"}
-    if traffic is not None and roofline is not None:
-        roofline["traffic"] = traffic
 
     line = {
         "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": done,
@@ -282,13 +347,16 @@ def run_ours(args, cfg):
         "config": {"workload": cfg["label"], "m": lp.m, "n_total": lp.n_total,
                    "pivots_timed": [W, W + done],
                    "l2": "working set > L2 (A 8*m*n_total B, B^-1 8*m^2 B); no flush needed",
-                   "parallelism": f"single GPU"},
+                   "parallelism": "single GPU" if world == 1 else
+                   f"{world} shards: rows of B^-1 and pricing columns split, NCCL exchanges"},
         "roofline": roofline,
         "e2e": e2e,
         "time_to_optimal": tto,
         "gpu_launches": c1["kernel_launches"] - c0["kernel_launches"],
         "clocks": clk.summary(),
     }
+    if exchange:
+        line["exchange"] = exchange
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         val, info = cpu_reference(lp, cfg["cpu_pivots"])
         line["cpu_baseline"] = {"value": val, "unit": "iterations/s", "cores": info["cores"],
@@ -297,6 +365,9 @@ def run_ours(args, cfg):
                                           f"({info['seconds']:.2f} s, {info['lib']})"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
 
 
 def main():

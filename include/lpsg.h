@@ -69,7 +69,9 @@ typedef struct {
     int device;            /* CUDA device ordinal, default 0 */
     int batch;             /* pivots enqueued per host check (0 = auto) */
     int use_graphs;        /* reserved (CUDA-graph capture of pivot batches) */
-    int reserved[6];
+    int reserved[6];       /* [0] bit 0: standalone ratio kernel (debug);
+                              [1] bit 0: attach the NCCL exchange path even for
+                                  world_size 1 (exercises NCCL on one GPU) */
     /* Sharded solve over NCCL, one process (or thread) per GPU:
      * world_size > 1 makes this handle shard `rank`; every rank passes the same
      * problem, config and nccl_id (from lpsg_nccl_unique_id on rank 0) and must
@@ -142,6 +144,10 @@ int lpsg_nccl_unique_id(unsigned char out[128]);
  * NULL) are shard 0's; all shards reach the same decisions. */
 int lpsg_solve_sharded(const lpsg_problem* lp, const lpsg_config* cfg, int shards, int spread_devices,
                        lpsg_report* report, double* x, lpsg_trace* trace, long cap, long* len);
+/* Shard partition used by every sharded solve: shard `rank` of `world` owns the
+ * contiguous range [*lo, *hi) of n items (rows of T: n = m; pricing columns:
+ * n = n_total), lo = floor(n*rank/world). Pure host arithmetic. */
+int lpsg_shard_range(int n, int world, int rank, int* lo, int* hi);
 /* Exchange accounting of this handle's shard: collectives issued and payload bytes. */
 int lpsg_comm_stats(lpsg_solver* s, long long* calls, double* bytes);
 /* Shard geometry: this handle's rows [row0, row0+rows) of T and pricing

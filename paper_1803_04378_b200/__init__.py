@@ -8,12 +8,12 @@ kernels behind the C ABI in include/lpsg.h.
 from .solver import (  # noqa: F401
     Anticycle, ColKind, CudaError, DegenerateSpec, Error, Form, GenSpec, IterationView,
     PivotTooSmall, SimplexSolver, SolveReport, SolverConfig, SolveStatus, SparsityClass,
-    StandardFormLP, TRACE_DTYPE, device_count, generate, nccl_unique_id, solve_sharded,
+    StandardFormLP, TRACE_DTYPE, device_count, generate, nccl_unique_id, shard_range, solve_sharded,
     two_phase_solve)
 
 __all__ = [
     "Anticycle", "ColKind", "CudaError", "DegenerateSpec", "Error", "Form", "GenSpec",
     "IterationView", "PivotTooSmall", "SimplexSolver", "SolveReport", "SolverConfig",
     "SolveStatus", "SparsityClass", "StandardFormLP", "TRACE_DTYPE", "device_count",
-    "generate", "nccl_unique_id", "solve_sharded", "two_phase_solve",
+    "generate", "nccl_unique_id", "shard_range", "solve_sharded", "two_phase_solve",
 ]

@@ -86,6 +86,7 @@ SIGNATURES = [
     ("lpsg_solve_sharded", C.c_int, [C.POINTER(Problem), C.POINTER(Config), C.c_int, C.c_int,
                                      C.POINTER(Report), _PD, C.POINTER(Trace), C.c_long,
                                      C.POINTER(C.c_long)]),
+    ("lpsg_shard_range", C.c_int, [C.c_int, C.c_int, C.c_int, _PI, _PI]),
     ("lpsg_comm_stats", C.c_int, [_P, C.POINTER(C.c_longlong), _PD]),
     ("lpsg_shard_info", C.c_int, [_P, _PI, _PI, _PI, _PI, _PI, _PI]),
     ("lpsg_host_free", None, [C.c_void_p]),

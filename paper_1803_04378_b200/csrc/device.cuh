@@ -87,8 +87,9 @@ struct Ctl {
 
 struct Dev {
     int m, n_total, n_work;
-    // sharding. world == 1: row0 = 0, mloc = m, col0 = 0, col1 = n_total.
+    // sharding. Unsharded: world == 1, row0 = 0, mloc = m, col0 = 0, col1 = n_total.
     int world, rank;
+    int sharded;           // 1: a communicator is attached (even with world == 1)
     int row0, mloc;        // this shard's rows of T = [B^-1 | b_bar] and of Y
     int col0, col1;        // this shard's pricing columns (original index range)
     double* xbuf;          // world > 1: pivot row exchange, m+3 slots summed as int64 bits

@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(512) k_price(Dev d) {
         warp_argmax(z, j);
         if (threadIdx.x == 0) {
             c->ticket_price = 0;
-            if (d.world > 1) {
+            if (d.sharded) {
                 d.pmsg[0] = PriceMsg{z, j, 0};  // merged across shards by k_price_final
             } else {
                 price_decide(d, c, budget_hit, z, j);
@@ -623,7 +623,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
     __syncthreads();
     if (!any) {
         if (threadIdx.x == 0) {
-            if (d.world > 1) {
+            if (d.sharded) {
                 d.rmsg->any = 0;
                 d.rmsg->n = 0;
                 d.rmsg->theta = kInf;
@@ -688,7 +688,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         }
     }
     __syncthreads();
-    if (d.world > 1) {
+    if (d.sharded) {
         // this shard's theta and its candidates within the shard-local window
         // (a superset of its rows inside the global window): k_ratio_final merges
         if (threadIdx.x < kRatioMsgCap) {
@@ -875,7 +875,7 @@ __global__ void __launch_bounds__(256) k_pivot(Dev d) {
     if (c->status != ST_RUNNING) return;
     const int m = d.m;
     const int r = c->r, q = c->q;
-    const bool sharded = d.world > 1;
+    const bool sharded = d.sharded != 0;
     const double yr = sharded ? d.xbuf[m + 2] : d.Y[r];
     if (fabs(yr) <= d.pivot_tol) {
         if (blockIdx.x == 0 && threadIdx.x == 0) c->status = ST_PIVOT_ERR;

@@ -141,6 +141,7 @@ private:
     int batch_ = 16;
     bool unfused_ratio_ = false;  // debug knob (cfg.reserved[0] & 1): standalone ratio kernel
     Comm* comm_ = nullptr;
+    bool sharded_ = false;        // comm_ attached: the exchange path runs even for one rank
     int world_ = 1, rank_ = 0;
     double* chain_ = nullptr;     // world > 1: rebuild_top_row partial sums (m+1)
 
@@ -253,6 +254,7 @@ void Solver::set_max_iter(long long v) {
 Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     : cfg_(cfg), m_(lp.m), n_total_(lp.n_total), comm_(comm) {
     if (comm_) {
+        sharded_ = true;
         world_ = comm_->size;
         rank_ = comm_->rank;
     }
@@ -321,10 +323,13 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     // original-column blocks for pricing
     d_.world = world_;
     d_.rank = rank_;
-    d_.row0 = (int)((long long)m * rank_ / world_);
-    d_.mloc = (int)((long long)m * (rank_ + 1) / world_) - d_.row0;
-    d_.col0 = (int)((long long)n * rank_ / world_);
-    d_.col1 = (int)((long long)n * (rank_ + 1) / world_);
+    d_.sharded = sharded_ ? 1 : 0;
+    {
+        int r1 = 0;
+        lpsg_shard_range(m, world_, rank_, &d_.row0, &r1);
+        d_.mloc = r1 - d_.row0;
+        lpsg_shard_range(n, world_, rank_, &d_.col0, &d_.col1);
+    }
     d_.ld_nb = round_up(std::max(1, d_.col1 - d_.col0), 32) + 32;
     d_.ld_cm = round_up(m, 4);
     d_.num_sms = prop.multiProcessorCount;
@@ -336,7 +341,7 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     configure_kernels(d_);
     CK(cudaGetLastError());
     d_.ldT = round_up(std::max<long long>(d_.mloc + 1, (long long)d_.update_grid * d_.upd_h), 32);
-    unfused_ratio_ = world_ == 1 && (cfg_.reserved[0] & 1) != 0;
+    unfused_ratio_ = !sharded_ && (cfg_.reserved[0] & 1) != 0;
     batch_ = cfg_.batch > 0 ? cfg_.batch : (m <= 1024 ? 64 : m <= 4096 ? 16 : 4);
     d_.log_cap = batch_ + 8;
 
@@ -344,7 +349,7 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     d_.top = dalloc<double>(m + 520);  // + padding: TMA-side W segments may run past m+2
     d_.Y = dalloc<double>(d_.mloc);
     d_.xrow = dalloc<double>(m + 4);
-    if (world_ > 1) {
+    if (sharded_) {
         d_.xbuf = dalloc<double>(m + 4);
         d_.pmsg = dalloc<PriceMsg>(world_ + 1);
         d_.rmsg = dalloc<RatioMsg>(world_ + 1);
@@ -413,7 +418,7 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
 
     // ---- initial Figure-1 tableau B = I, b_bar = b (solver.cpp:66-72)
     CK(cudaMemsetAsync(d_.T, 0, sizeof(double) * (size_t)(m + 1) * d_.ldT, st_));
-    if (world_ > 1) {
+    if (sharded_) {
         // the sharded pivot row travels in xbuf; k_update reads it as xrow
         CK(cudaFree(d_.xrow));
         d_.xrow = d_.xbuf;
@@ -480,7 +485,7 @@ double Solver::objective_value() {
 // rebuild_top_row (solver.cpp:318-329). Sharded: an ordered chain, shard g
 // continuing shard g-1's partial sums (an allreduce would reorder the sum).
 void Solver::rebuild_top_row() {
-    if (world_ == 1) {
+    if (!sharded_) {
         launch_rebuild_top(d_, nullptr, d_.top, st_);
         CK(cudaGetLastError());
         return;
@@ -504,7 +509,7 @@ int Solver::owner_of_row(int i) const {
 }
 
 void Solver::single_gpu_only(const char* what) const {
-    if (world_ > 1) throw Error(LPSG_INVALID_ARGUMENT, std::string(what) + ": step API is single-GPU only");
+    if (sharded_) throw Error(LPSG_INVALID_ARGUMENT, std::string(what) + ": step API is single-GPU only");
 }
 
 // note_iteration (solver.cpp:256-276) for one logged pivot.
@@ -533,7 +538,7 @@ void Solver::drain_log() {
 // per-pivot exchanges: the pivot row from its owner, the
 // pricing (z, j) and the ratio-test messages.
 void Solver::seq_pivot() {
-    if (world_ == 1) {
+    if (!sharded_) {
         L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot(d_, st_); });
         return;
     }
@@ -544,7 +549,7 @@ void Solver::seq_pivot() {
 
 void Solver::seq_price() {
     L(K_PRICE, bytes_of(K_PRICE), [&] { launch_price(d_, st_); });
-    if (world_ > 1) {
+    if (sharded_) {
         L(K_COMM, 0.0, [&] { comm_->allgather(d_.pmsg, d_.pmsg + 1, sizeof(PriceMsg), st_); });
         L(K_OTHER, 0.0, [&] { launch_price_final(d_, st_); });
     }
@@ -552,7 +557,7 @@ void Solver::seq_price() {
 
 void Solver::seq_update() {
     L(K_UPDATE, bytes_of(K_UPDATE), [&] { launch_update(d_, st_); });
-    if (world_ > 1) {
+    if (sharded_) {
         L(K_COMM, 0.0, [&] { comm_->allgather(d_.rmsg, d_.rmsg + 1, sizeof(RatioMsg), st_); });
         L(K_OTHER, 0.0, [&] { launch_ratio_final(d_, st_); });
     }
@@ -705,21 +710,21 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     la.part_j = dalloc<int>((size_t)kb * la.nblk);
     la.part_t = dalloc<double>((size_t)kb * la.nblk);
     la.pm = dalloc<PriceMsg>((size_t)kb);
-    la.pm_all = G > 1 ? dalloc<PriceMsg>((size_t)kb * G) : nullptr;
+    la.pm_all = sharded_ ? dalloc<PriceMsg>((size_t)kb * G) : nullptr;
     la.tl = dalloc<double>(kb);
-    la.tl_all = G > 1 ? dalloc<double>((size_t)kb * G) : nullptr;
+    la.tl_all = sharded_ ? dalloc<double>((size_t)kb * G) : nullptr;
     CK(cudaMemsetAsync(la.X, 0, sizeof(double) * (size_t)kb * ldx, st_));
     for (int k0 = 0; k0 < K; k0 += kb) {
         la.K = std::min(kb, K - k0);
         CK(cudaMemcpyAsync(rows_d, rows.data() + k0, sizeof(int) * la.K, cudaMemcpyHostToDevice, st_));
         launch_la_x(d_, la, st_);
-        if (G > 1) comm_->sum_i64(reinterpret_cast<long long*>(la.X), (size_t)la.K * ldx, st_);
+        if (sharded_) comm_->sum_i64(reinterpret_cast<long long*>(la.X), (size_t)la.K * ldx, st_);
         launch_la_price(d_, la, st_);
-        if (G > 1) comm_->allgather(la.pm, la.pm_all, sizeof(PriceMsg) * la.K, st_);
-        launch_la_decide(d_, la, G > 1 ? la.pm_all : la.pm, G, st_);
+        if (sharded_) comm_->allgather(la.pm, la.pm_all, sizeof(PriceMsg) * la.K, st_);
+        launch_la_decide(d_, la, sharded_ ? la.pm_all : la.pm, G, st_);
         launch_la_theta(d_, la, st_);
-        if (G > 1) comm_->allgather(la.tl, la.tl_all, sizeof(double) * la.K, st_);
-        launch_la_score(d_, la, G > 1 ? la.tl_all : la.tl, G, st_);
+        if (sharded_) comm_->allgather(la.tl, la.tl_all, sizeof(double) * la.K, st_);
+        launch_la_score(d_, la, sharded_ ? la.tl_all : la.tl, G, st_);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(scores.data() + k0, la.score, sizeof(double) * la.K, cudaMemcpyDeviceToHost, st_));
         CK(cudaStreamSynchronize(st_));
@@ -739,9 +744,9 @@ void Solver::drive_out_artificials() {
         push();
         const int owner = owner_of_row(i);
         if (owner == rank_) launch_gather_row(d_, i - d_.row0, scratch_, st_);
-        if (world_ > 1) comm_->bcast(scratch_, sizeof(double) * (m_ + 1), owner, st_);
+        if (sharded_) comm_->bcast(scratch_, sizeof(double) * (m_ + 1), owner, st_);
         launch_drive_scan(d_, scratch_, st_);
-        if (world_ > 1) comm_->min_i32(&d_.ctl->found, 1, st_);
+        if (sharded_) comm_->min_i32(&d_.ctl->found, 1, st_);
         launch_drive_red(d_, st_);
         CK(cudaGetLastError());
         pull(false);
@@ -853,7 +858,7 @@ void Solver::get_x(double* x, int n) {
     if (solved_ && !(final_status_ == LPSG_OPTIMAL || final_status_ == LPSG_ITERATION_LIMIT)) return;
     std::vector<double> bbar(m_);
     const double* bcol = d_.T + (size_t)m_ * d_.ldT;
-    if (world_ == 1) {
+    if (!sharded_) {
         CK(cudaMemcpyAsync(bbar.data(), bcol, sizeof(double) * m_, cudaMemcpyDeviceToHost, st_));
     } else {
         // every shard's b_bar rows, padded to the largest shard, in rank order
@@ -866,7 +871,8 @@ void Solver::get_x(double* x, int n) {
         CK(cudaStreamSynchronize(st_));
         cudaFree(tmp);
         for (int g = 0; g < world_; ++g) {
-            const int r0 = (int)((long long)m_ * g / world_), r1 = (int)((long long)m_ * (g + 1) / world_);
+            int r0 = 0, r1 = 0;
+            lpsg_shard_range(m_, world_, g, &r0, &r1);
             for (int i = r0; i < r1; ++i) bbar[i] = all[(size_t)g * pad + (i - r0)];
         }
     }
@@ -970,7 +976,7 @@ void Solver::read_row(int i, double* out) {
             launch_gather_row(d_, li, scratch_, st_);
             CK(cudaMemcpyAsync(scratch_ + m_ + 1, d_.Y + li, sizeof(double), cudaMemcpyDeviceToDevice, st_));
         }
-        if (world_ > 1) comm_->bcast(scratch_, sizeof(double) * (m_ + 2), owner, st_);
+        if (sharded_) comm_->bcast(scratch_, sizeof(double) * (m_ + 2), owner, st_);
         CK(cudaMemcpyAsync(out, scratch_, sizeof(double) * (m_ + 2), cudaMemcpyDeviceToHost, st_));
     }
     CK(cudaStreamSynchronize(st_));
@@ -1042,8 +1048,8 @@ int lpsg_create(const lpsg_problem* lp, const lpsg_config* cfg, lpsg_solver** ou
     return guard([&] {
         auto* h = new lpsg_solver{nullptr, nullptr};
         try {
-            if (c.world_size > 1) {
-                h->comm = lpsg::make_nccl_comm(c.nccl_id, c.rank, c.world_size, c.device);
+            if (c.world_size > 1 || (c.reserved[1] & 1)) {
+                h->comm = lpsg::make_nccl_comm(c.nccl_id, c.rank, std::max(1, c.world_size), c.device);
                 if (!h->comm) throw lpsg::CommError("NCCL communicator");
             }
             h->s = new lpsg::Solver(*lp, c, h->comm.get());
@@ -1129,6 +1135,13 @@ int lpsg_solve_sharded(const lpsg_problem* lp, const lpsg_config* cfg, int shard
             lpsg::g_err = "shard " + std::to_string(g) + ": " + msg[g];
             return rc[g];
         }
+    return LPSG_OK;
+}
+
+int lpsg_shard_range(int n, int world, int rank, int* lo, int* hi) {
+    if (n < 0 || world < 1 || rank < 0 || rank >= world || !lo || !hi) return bad("lpsg_shard_range: bad argument");
+    *lo = (int)((long long)n * rank / world);
+    *hi = (int)((long long)n * (rank + 1) / world);
     return LPSG_OK;
 }
 

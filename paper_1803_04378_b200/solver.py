@@ -96,6 +96,7 @@ class SolverConfig:
     world_size: int = 1
     rank: int = 0
     nccl_id: bytes = b""
+    nccl_single: bool = False  # run the NCCL exchange path even for world_size 1 (testing)
 
     def _c(self) -> L.Config:
         c = L.Config()
@@ -106,6 +107,7 @@ class SolverConfig:
         c.device, c.batch, c.use_graphs = int(self.device), int(self.batch), int(self.use_graphs)
         c.reserved[0] = int(self.debug_flags)
         c.world_size, c.rank = int(self.world_size), int(self.rank)
+        c.reserved[1] = 1 if self.nccl_single else 0
         if self.nccl_id:
             if len(self.nccl_id) != 128:
                 raise Error("nccl_id must be 128 bytes")
@@ -415,6 +417,14 @@ def two_phase_solve(lp: StandardFormLP, cfg: Optional[SolverConfig] = None) -> S
 
 def device_count() -> int:
     return L.load().lpsg_device_count()
+
+
+def shard_range(n: int, world: int, rank: int):
+    """[lo, hi) of n items owned by shard `rank` of `world` (rows of B^-1 or
+    pricing columns; include/lpsg.h lpsg_shard_range)."""
+    lo, hi = C.c_int(), C.c_int()
+    _check(L.load().lpsg_shard_range(int(n), int(world), int(rank), C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
 
 
 def nccl_unique_id() -> bytes:
