@@ -134,6 +134,7 @@ struct Dev {
     const CUtensorMap* tm_T;   // 2D TMA descriptor of T, box {h rows, C columns}
     const CUtensorMap* tm_nb;  // 2D TMA descriptors of A_nb, box {wbx slots, price_rows(wbx) rows}
     int price_nwc, price_S, price_smem, price_threads;
+    int dbg;               // experiment knobs (cfg.reserved[2]); 0 in production
     size_t price_stage_bytes;
 };
 
@@ -142,10 +143,13 @@ struct Dev {
 struct PriceGeom {
     int w, nb, wbx, R;
 };
+// Rows per pricing stage: ~48 KB of A_nb per box, a multiple of 16 rows (the
+// consumer runs 8-row groups in pairs) so full stages have no row tail and the
+// per-stage barrier / pipeline-restart cost is amortised over many rows.
 __host__ __device__ inline int price_rows(int wbx) {
-    int R = (24 * 1024) / (8 * wbx);
-    R = R < 2 ? 2 : (R > 256 ? 256 : R);
-    return R & ~1;
+    int R = (48 * 1024) / (8 * wbx);
+    R &= ~15;
+    return R < 16 ? 16 : (R > 256 ? 256 : R);
 }
 __host__ __device__ inline PriceGeom price_geom(int n_scan, int G) {
     int w = (n_scan + G - 1) / G;

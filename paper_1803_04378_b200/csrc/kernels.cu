@@ -78,7 +78,7 @@ __device__ __forceinline__ void price_decide(const Dev& d, Ctl* c, bool budget_h
     } else {
         c->q = j == INT_MAX ? -1 : j;
         c->d = j == INT_MAX ? 0.0 : z;
-        if (j == INT_MAX || z <= d.opt_tol) c->status = ST_OPTIMAL;
+        if (j == INT_MAX || (z <= d.opt_tol && !d.dbg)) c->status = ST_OPTIMAL;
     }
 }
 
@@ -241,6 +241,33 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// 8 rows of a slot pair (col, row pitch in double2) and the matching 8 W values.
+__device__ __forceinline__ void lds_group(const double2* col, int pitch, const double* ws, double2 (&a)[8],
+                                          double2 (&w)[4]) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(a[u].x), "=d"(a[u].y) : "r"(su32(col + u * pitch)));
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(w[u].x), "=d"(w[u].y) : "r"(su32(ws + 2 * u)));
+}
+
+// Scheduling fence: a volatile no-op that "writes" the accumulators, so the
+// chains after it cannot be hoisted above the volatile loads before it.
+__device__ __forceinline__ void pin(double& a, double& b) { asm volatile("" : "+d"(a), "+d"(b)); }
+
+// two sequential chains (slot 2t, slot 2t+1) over 8 rows, in row order
+__device__ __forceinline__ void chain_group(double& acc0, double& acc1, const double2 (&a)[8],
+                                            const double2 (&w)[4]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        acc0 = dadd(acc0, dmul(w[u].x, a[2 * u].x));
+        acc1 = dadd(acc1, dmul(w[u].x, a[2 * u].y));
+        acc0 = dadd(acc0, dmul(w[u].y, a[2 * u + 1].x));
+        acc1 = dadd(acc1, dmul(w[u].y, a[2 * u + 1].y));
+    }
+}
+
 // ---------------------------------------------------------------- price ---
 // solver.cpp:79-129 (+ the loop-top budget check, solver.cpp:281).
 // One CTA per SM; CTA b owns the contiguous slot range [b*w, b*w + w) of the
@@ -250,7 +277,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // 1D bulk copy of the matching W segment; consumer thread t accumulates
 // z_t = sum_i W_i * a_i,t strictly in ascending i. The grid-wide
 // (max z, min j) reduction is finished by the last CTA.
-__global__ void __launch_bounds__(512) k_price(Dev d) {
+__global__ void __launch_bounds__(384) k_price(Dev d) {
     extern __shared__ __align__(1024) unsigned char smem[];
     Ctl* c = d.ctl;
     if (c->status != ST_RUNNING) return;
@@ -292,19 +319,27 @@ __global__ void __launch_bounds__(512) k_price(Dev d) {
                     const int i0 = k * R;
                     unsigned char* sb = smem + (size_t)st * stage_stride;
                     double* ws = reinterpret_cast<double*>(sb) + (size_t)R * w;
-                    mbar_expect_tx(&full[st], (uint32_t)(R * w * 8 + R * 8));
-                    for (int q = 0; q < g.nb; ++q)
-                        tma_load_2d(sb + (size_t)q * g.wbx * R * 8, map, s0 + q * g.wbx, i0, &full[st]);
-                    bulk_g2s(ws, d.top + i0, (uint32_t)R * 8u, &full[st]);
+                    if (d.dbg & 2) {  // experiment: no loads (compute-only rate)
+                        mbar_arrive(&full[st]);
+                    } else {
+                        mbar_expect_tx(&full[st], (uint32_t)(R * w * 8 + R * 8));
+                        for (int q = 0; q < g.nb; ++q)
+                            tma_load_2d(sb + (size_t)q * g.wbx * R * 8, map, s0 + q * g.wbx, i0, &full[st]);
+                        bulk_g2s(ws, d.top + i0, (uint32_t)R * 8u, &full[st]);
+                    }
                     if (++st == S) { st = 0; ph ^= 1; }
                 }
             }
         } else if (warp < nwc) {
+            // consumer thread t owns the adjacent slot pair (2t, 2t+1): one
+            // LDS.128 per row feeds two independent sequential chains
             const int t = threadIdx.x;
-            // box q holds slots [q*wbx, (q+1)*wbx) as R rows of wbx doubles
-            const int q = t / g.wbx, tq = t - q * g.wbx;
+            const int s2 = 2 * t;
+            // box q holds slots [q*wbx, (q+1)*wbx) as R rows of wbx doubles (wbx % 8 == 0,
+            // so a pair never straddles two boxes)
+            const int q = s2 / g.wbx, tq = s2 - q * g.wbx;
             const int wbx = g.wbx;
-            double acc = 0.0;
+            double acc0 = 0.0, acc1 = 0.0;
             int st = 0;
             uint32_t ph = 0;
             for (int k = 0; k < nst; ++k) {
@@ -312,33 +347,43 @@ __global__ void __launch_bounds__(512) k_price(Dev d) {
                 const int nr = min(R, m - k * R);
                 const double* sb = reinterpret_cast<const double*>(smem + (size_t)st * stage_stride);
                 const double* ws = sb + (size_t)R * w;
-                if (t < ns) {
-                    const double* col = sb + q * wbx * R + tq;
-                    int rr = 0;
-                    // loads of a group are issued before its (sequential) chain
-                    for (; rr + 8 <= nr; rr += 8) {
-                        double av[8], wv[8];
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) av[u] = col[(rr + u) * wbx];
-#pragma unroll
-                        for (int u = 0; u < 8; u += 2) {
-                            const double2 w2 = *reinterpret_cast<const double2*>(ws + rr + u);
-                            wv[u] = w2.x;
-                            wv[u + 1] = w2.y;
-                        }
-#pragma unroll
-                        for (int u = 0; u < 8; ++u) acc = dadd(acc, dmul(wv[u], av[u]));
+                if (s2 < ns && !(d.dbg & 1)) {  // dbg bit 0: no math (memory-only rate)
+                    const double2* col = reinterpret_cast<const double2*>(sb + q * wbx * R + tq);
+                    const int pitch = wbx / 2;  // row pitch in double2
+                    const int ng = nr >> 3;
+                    // software pipeline: group g+1's shared loads are issued
+                    // (volatile, in order) before group g's two chains run
+                    double2 a0[8], w0[4], a1[8], w1[4];
+                    if (ng > 0) lds_group(col, pitch, ws, a0, w0);
+                    int gi = 0;
+                    for (; gi + 2 <= ng; gi += 2) {
+                        lds_group(col + (gi + 1) * 8 * pitch, pitch, ws + (gi + 1) * 8, a1, w1);
+                        pin(acc0, acc1);  // keeps group g's chain behind group g+1's loads
+                        chain_group(acc0, acc1, a0, w0);
+                        if (gi + 2 < ng) lds_group(col + (gi + 2) * 8 * pitch, pitch, ws + (gi + 2) * 8, a0, w0);
+                        pin(acc0, acc1);
+                        chain_group(acc0, acc1, a1, w1);
                     }
-                    for (; rr < nr; ++rr) acc = dadd(acc, dmul(ws[rr], col[rr * wbx]));
+                    if (gi < ng) chain_group(acc0, acc1, a0, w0);
+                    for (int rr = ng * 8; rr < nr; ++rr) {
+                        const double2 a2 = col[rr * pitch];
+                        acc0 = dadd(acc0, dmul(ws[rr], a2.x));
+                        acc1 = dadd(acc1, dmul(ws[rr], a2.y));
+                    }
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[st]);
                 if (++st == S) { st = 0; ph ^= 1; }
             }
-            if (t < ns) {
-                const int j = d.slot2col[s0 + t];
-                bz = dsub(acc, cost[j]);
-                bj = j;
+            if (s2 < ns) {
+                const int j0 = d.slot2col[s0 + s2];
+                bz = dsub(acc0, cost[j0]);
+                bj = j0;
+                if (s2 + 1 < ns) {
+                    const int j1 = d.slot2col[s0 + s2 + 1];
+                    const double z1 = dsub(acc1, cost[j1]);
+                    if (better(z1, j1, bz, bj)) { bz = z1; bj = j1; }
+                }
             }
         }
     }
@@ -1235,7 +1280,7 @@ void configure_kernels(Dev& d) {
     const PriceGeom gm = price_geom(ncols_local, G);
     d.pivot_grid = std::max(1, std::min(2 * G, (d.m + 1 + 255) / 256));
     d.price_grid = G;
-    d.price_nwc = (gm.w + 31) / 32;
+    d.price_nwc = (gm.w + 63) / 64;  // consumer threads own slot pairs
     d.price_threads = (d.price_nwc + 1) * 32;
     d.price_stage_bytes = 0;
     for (int n = 1; n <= ncols_local; n = (n < 64 ? n + 1 : n + n / 64)) {

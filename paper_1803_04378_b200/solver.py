@@ -97,6 +97,7 @@ class SolverConfig:
     rank: int = 0
     nccl_id: bytes = b""
     nccl_single: bool = False  # run the NCCL exchange path even for world_size 1 (testing)
+    experiment: int = 0        # kernel experiment knobs (results are NOT valid); 0 = production
 
     def _c(self) -> L.Config:
         c = L.Config()
@@ -108,6 +109,7 @@ class SolverConfig:
         c.reserved[0] = int(self.debug_flags)
         c.world_size, c.rank = int(self.world_size), int(self.rank)
         c.reserved[1] = 1 if self.nccl_single else 0
+        c.reserved[2] = int(self.experiment)
         if self.nccl_id:
             if len(self.nccl_id) != 128:
                 raise Error("nccl_id must be 128 bytes")
