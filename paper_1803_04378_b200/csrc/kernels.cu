@@ -446,6 +446,7 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
         ny1[u] = (ok[u] && i + 1 < mloc && i + 1 != r) ? -d.Y[i + 1] : 0.0;
     }
     const size_t ldT = (size_t)d.ldT;
+    const bool nomath = (d.dbg & 4) != 0;  // experiment: stores without the update math
     double2* const gbase = reinterpret_cast<double2*>(d.T + i0) + lane;  // + col * ldT/2
     const int ncols = m + 1;
     int st = 0;
@@ -466,6 +467,10 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
                 for (int u = 0; u < NIT; ++u) {
                     if (ok[u]) {
                         double2 tv = tcol[32 * u];
+                        if (nomath) {
+                            gcol[32 * u] = tv;
+                            continue;
+                        }
                         const double p0 = dmul(ny0[u], xj);
                         const double p1 = dmul(ny1[u], xj);
                         const double s0v = dadd(tv.x, p0);
@@ -540,10 +545,14 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                 unsigned char* sb = smem + (size_t)st * stage_stride;
                 double* xs = reinterpret_cast<double*>(sb) + tile_el;
                 double* as = xs + C;
-                mbar_expect_tx(&full[st], (uint32_t)(tile_el * 8) + (up ? seg : 0u) + (ft ? seg : 0u));
-                tma_load_2d(sb, d.tm_T, i0, j0, &full[st]);
-                if (up) bulk_g2s(xs, d.xrow + j0, seg, &full[st]);
-                if (ft) bulk_g2s(as, a + j0, seg, &full[st]);
+                if (d.dbg & 8) {  // experiment: no loads (compute-only rate)
+                    mbar_arrive(&full[st]);
+                } else {
+                    mbar_expect_tx(&full[st], (uint32_t)(tile_el * 8) + (up ? seg : 0u) + (ft ? seg : 0u));
+                    tma_load_2d(sb, d.tm_T, i0, j0, &full[st]);
+                    if (up) bulk_g2s(xs, d.xrow + j0, seg, &full[st]);
+                    if (ft) bulk_g2s(as, a + j0, seg, &full[st]);
+                }
                 if (++st == S) { st = 0; ph ^= 1; }
             }
         }
@@ -569,7 +578,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         uint32_t ph = 0;
         for (int k = 0; k < nst; ++k) {
             mbar_wait(&upd[st], ph);
-            if (ft && valid) {
+            if (ft && valid && !(d.dbg & 4)) {  // dbg bit 2: no FTRAN math
                 const int j0 = k * C, nf = min(C, m - j0);
                 const double* tile = reinterpret_cast<const double*>(smem + (size_t)st * stage_stride);
                 if (m - j0 < C) f_bbar = tile[(m - j0) * h + t];  // updated b_bar_i (column m)
@@ -595,6 +604,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
             if (lane == 0) mbar_arrive(&empty[st]);
             if (++st == S) { st = 0; ph ^= 1; }
         }
+        if ((d.dbg & 12) && ft) acc = 1.0 + 1e-6 * i;  // experiments: keep pivoting on a valid column
         if (valid) {
             if (ft) {
                 d.Y[i] = acc;
