@@ -187,6 +187,8 @@ def dist_ctx():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if os.environ.get("LPSG_BENCH_SAME_DEVICE"):
+        local = 0  # testing the multi-process path on a one-GPU box (time-sliced, not a bench number)
     if world > 1:
         import torch.distributed as dist
         if not dist.is_initialized():
@@ -219,10 +221,32 @@ def barrier(world: int) -> None:
         dist.barrier()
 
 
+_PEER = None
+
+
+def peer_heap(world: int, rank: int, local: int):
+    """The P2P transport's symmetric heap, connected once per process: every
+    rank all-gathers the 64-byte CUDA IPC handles over gloo."""
+    global _PEER
+    if _PEER is None:
+        import paper_1803_04378_b200 as P
+        import torch.distributed as dist
+        h = P.PeerHeap(rank, world, device=local)
+        handles = [None] * world
+        dist.all_gather_object(handles, h.handle)
+        h.connect(handles)
+        dist.barrier()
+        _PEER = h
+    return _PEER
+
+
 def solver_config(P, args, world, rank, local, **kw):
     extra = {}
     if world > 1:
-        extra = dict(world_size=world, rank=rank, nccl_id=share_nccl_id(world, rank))
+        if args.transport == "p2p":
+            extra = dict(peer=peer_heap(world, rank, local))
+        else:
+            extra = dict(world_size=world, rank=rank, nccl_id=share_nccl_id(world, rank))
     return P.SolverConfig(device=local if world > 1 else 0, batch=args.batch,
                           debug_flags=args.debug_flags, **extra, **kw)
 
@@ -304,11 +328,13 @@ def run_ours(args, cfg):
         calls = (x1["calls"] - x0["calls"]) / max(1, done)
         nbytes = (x1["bytes"] - x0["bytes"]) / max(1, done)
         ex = kern.get("exchange")
-        exchange = {"transport": "NCCL (NVLink/NVSwitch)", "collectives_per_pivot": round(calls, 2),
+        exchange = {"transport": ("P2P: device-initiated NVLink stores + sequence flags (CUDA IPC heaps)"
+                                  if args.transport == "p2p" else "NCCL (NVLink/NVSwitch)"),
+                    "collectives_per_pivot": round(calls, 2),
                     "payload_bytes_per_pivot_per_rank": round(nbytes, 1),
                     "us_per_pivot": round(1e3 * ex["ms_total"] / max(1, done_p), 2) if ex else None,
-                    "note": "per pivot: pivot-row int64 allreduce (m+3 words), (z, j) all-gather, "
-                            "ratio-message all-gather"}
+                    "note": "per pivot: pivot-row broadcast from its owner (m+3 words), (z, j) "
+                            "all-gather, ratio-message all-gather"}
 
     # ---- end to end through the public API with host buffers: lpsg_create
     # uploads A from pinned host memory, solve() runs to optimality (or the
@@ -348,7 +374,8 @@ def run_ours(args, cfg):
                    "pivots_timed": [W, W + done],
                    "l2": "working set > L2 (A 8*m*n_total B, B^-1 8*m^2 B); no flush needed",
                    "parallelism": "single GPU" if world == 1 else
-                   f"{world} shards: rows of B^-1 and pricing columns split, NCCL exchanges"},
+                   f"{world} shards: rows of B^-1 and pricing columns split, "
+                   f"{'P2P (NVLink stores + flags)' if args.transport == 'p2p' else 'NCCL'} exchanges"},
         "roofline": roofline,
         "e2e": e2e,
         "time_to_optimal": tto,
@@ -381,6 +408,8 @@ def main():
                     help="pivot budget of the end-to-end solve (0 = to optimality)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--batch", type=int, default=0, help="pivots per host check (0 = auto)")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 exchanges: device-initiated NVLink stores + flags (p2p) or NCCL")
     ap.add_argument("--debug-flags", type=int, default=0)
     ap.add_argument("--no-profile", action="store_true",
                     help="no per-kernel CUDA events in the timed region (roofline omitted)")
@@ -388,8 +417,17 @@ def main():
     cfg = CONFIGS[args.config]
     if args.impl == "reference":
         run_reference_arm(args, cfg)
-    else:
+        return
+    try:
         run_ours(args, cfg)
+    except Exception as e:  # noqa: BLE001
+        if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.transport == "p2p":
+            # every rank fails the same exchange (it times out on all of them)
+            print(f"bench: p2p transport failed ({e}); retrying with NCCL", file=sys.stderr, flush=True)
+            args.transport = "nccl"
+            run_ours(args, cfg)
+        else:
+            raise
 
 
 if __name__ == "__main__":

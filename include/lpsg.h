@@ -79,6 +79,10 @@ typedef struct {
     int world_size;
     int rank;
     unsigned char nccl_id[128];
+    /* Alternative transport: a connected P2P heap (lpsg_peer_create/connect).
+     * When set, the shards exchange through device-initiated NVLink stores and
+     * flags instead of NCCL (world_size/rank come from the heap). */
+    struct lpsg_peer* peer;
 } lpsg_config;
 
 /* lps::SolveReport (solver.hpp:47-57); x is fetched with lpsg_get_x. */
@@ -138,12 +142,25 @@ int lpsg_get_trace(lpsg_solver* s, lpsg_trace* out, long cap, long* len);
  * distributes it, e.g. over torch.distributed / MPI). */
 int lpsg_nccl_unique_id(unsigned char out[128]);
 /* One process, `shards` host threads: the sharded solver with in-process
- * device-to-device exchanges. spread_devices = 0 puts every shard on
- * cfg->device (parity testing on one GPU); 1 puts shard g on device
- * (cfg->device + g) % device_count. Report, x (may be NULL) and trace (may be
+ * exchanges. flags & LPSG_SHARD_SPREAD puts shard g on device
+ * (cfg->device + g) % device_count (else all on cfg->device: parity testing on
+ * one GPU); flags & LPSG_SHARD_P2P uses the device-initiated P2P transport
+ * (else CUDA-event ordered copies with host barriers). Report, x (may be NULL) and trace (may be
  * NULL) are shard 0's; all shards reach the same decisions. */
-int lpsg_solve_sharded(const lpsg_problem* lp, const lpsg_config* cfg, int shards, int spread_devices,
+int lpsg_solve_sharded(const lpsg_problem* lp, const lpsg_config* cfg, int shards, int flags,
                        lpsg_report* report, double* x, lpsg_trace* trace, long cap, long* len);
+enum { LPSG_SHARD_SPREAD = 1, LPSG_SHARD_P2P = 2 };
+/* Device-initiated P2P transport: every rank allocates a
+ * symmetric heap on its GPU (heap_bytes 0 = default 96 MiB) and gets its
+ * 64-byte CUDA IPC handle; the caller all-gathers the handles (rank order) and
+ * connects. Pass the heap in lpsg_config.peer; destroy after the solver. */
+typedef struct lpsg_peer lpsg_peer;
+int lpsg_peer_create(int rank, int world, int device, size_t heap_bytes, lpsg_peer** out,
+                     unsigned char handle[64]);
+int lpsg_peer_connect(lpsg_peer* p, const unsigned char* handles /* world x 64 bytes */);
+void lpsg_peer_destroy(lpsg_peer* p);
+/* The transport a handle uses: "single", "nccl", "p2p" or "local-events". */
+const char* lpsg_transport(lpsg_solver* s);
 /* Shard partition used by every sharded solve: shard `rank` of `world` owns the
  * contiguous range [*lo, *hi) of n items (rows of T: n = m; pricing columns:
  * n = n_total), lo = floor(n*rank/world). Pure host arithmetic. */

@@ -7,13 +7,13 @@ kernels behind the C ABI in include/lpsg.h.
 """
 from .solver import (  # noqa: F401
     Anticycle, ColKind, CudaError, DegenerateSpec, Error, Form, GenSpec, IterationView,
-    PivotTooSmall, SimplexSolver, SolveReport, SolverConfig, SolveStatus, SparsityClass,
+    PeerHeap, PivotTooSmall, SimplexSolver, SolveReport, SolverConfig, SolveStatus, SparsityClass,
     StandardFormLP, TRACE_DTYPE, device_count, generate, nccl_unique_id, shard_range, solve_sharded,
     two_phase_solve)
 
 __all__ = [
     "Anticycle", "ColKind", "CudaError", "DegenerateSpec", "Error", "Form", "GenSpec",
-    "IterationView", "PivotTooSmall", "SimplexSolver", "SolveReport", "SolverConfig",
+    "IterationView", "PeerHeap", "PivotTooSmall", "SimplexSolver", "SolveReport", "SolverConfig",
     "SolveStatus", "SparsityClass", "StandardFormLP", "TRACE_DTYPE", "device_count",
     "generate", "nccl_unique_id", "shard_range", "solve_sharded", "two_phase_solve",
 ]

@@ -25,7 +25,8 @@ class Config(C.Structure):
                 ("ratio_tie_tol", C.c_double), ("max_iter", C.c_long), ("anticycle", C.c_int),
                 ("kernel", C.c_int), ("workers", C.c_int), ("device", C.c_int),
                 ("batch", C.c_int), ("use_graphs", C.c_int), ("reserved", C.c_int * 6),
-                ("world_size", C.c_int), ("rank", C.c_int), ("nccl_id", C.c_ubyte * 128)]
+                ("world_size", C.c_int), ("rank", C.c_int), ("nccl_id", C.c_ubyte * 128),
+                ("peer", C.c_void_p)]
 
 
 class Report(C.Structure):
@@ -87,6 +88,11 @@ SIGNATURES = [
                                      C.POINTER(Report), _PD, C.POINTER(Trace), C.c_long,
                                      C.POINTER(C.c_long)]),
     ("lpsg_shard_range", C.c_int, [C.c_int, C.c_int, C.c_int, _PI, _PI]),
+    ("lpsg_peer_create", C.c_int, [C.c_int, C.c_int, C.c_int, C.c_size_t, C.POINTER(_P),
+                                   C.POINTER(C.c_ubyte)]),
+    ("lpsg_peer_connect", C.c_int, [_P, C.POINTER(C.c_ubyte)]),
+    ("lpsg_peer_destroy", None, [_P]),
+    ("lpsg_transport", C.c_char_p, [_P]),
     ("lpsg_comm_stats", C.c_int, [_P, C.POINTER(C.c_longlong), _PD]),
     ("lpsg_shard_info", C.c_int, [_P, _PI, _PI, _PI, _PI, _PI, _PI]),
     ("lpsg_host_free", None, [C.c_void_p]),

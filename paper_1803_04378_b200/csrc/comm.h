@@ -42,7 +42,51 @@ public:
     virtual void sum_i64(long long* buf, size_t n, cudaStream_t st) = 0;
     virtual void min_i32(int* buf, size_t n, cudaStream_t st) = 0;
     virtual void bcast(void* buf, size_t bytes, int root, cudaStream_t st) = 0;
+    // Broadcast from the rank whose *is_owner (device int) is non-zero; the
+    // owner is known on the device only. Default: the int64 bit-pattern sum
+    // (non-owners must have zero-filled buf).
+    virtual void owner_bcast(void* buf, size_t bytes, const int* is_owner, cudaStream_t st) {
+        (void)is_owner;
+        sum_i64(static_cast<long long*>(buf), bytes / 8, st);
+    }
+    // Device memory that collectives may write remotely (owner_bcast targets).
+    // Every rank must make the same sequence of calls (symmetric heaps).
+    virtual void* sym_alloc(size_t bytes);
+    virtual void sym_free(void* p);
+    virtual const char* transport() const = 0;
+    // Host-side barrier of shards that share a process (no-op across processes).
+    virtual void host_barrier() {}
+    // Throws CommError when the transport recorded a failure (called after syncs).
+    virtual void check() {}
 };
+
+struct LocalHub;
+
+// ---- device-initiated peer transport (NVLink / NVSwitch P2P stores + flags) ----
+// Every rank owns a symmetric heap (same size, same allocation sequence); each
+// collective is one or a few kernels that store straight into the peers'
+// heaps and raise a per-source sequence flag there, then spin on the local
+// flags. No host synchronisation, no NCCL kernel. Peers are mapped with CUDA
+// IPC (multi-process) or shared directly (shards of one process).
+struct PeerHeap {
+    int rank = 0, size = 1, device = 0;
+    size_t bytes = 0;
+    char* base = nullptr;                // this rank's heap
+    std::vector<char*> peers;            // every rank's heap as seen from this device
+    std::vector<bool> opened;            // peers[g] came from cudaIpcOpenMemHandle
+    LocalHub* hub = nullptr;             // in-process shards: their host barrier
+    unsigned long long seq = 0;          // last exchange sequence (persists across solvers on this heap)
+    ~PeerHeap();
+};
+constexpr size_t kPeerHeapDefault = (size_t)96 << 20;
+// allocate this rank's heap; `handle` (64 bytes) is its cudaIpcMemHandle
+std::unique_ptr<PeerHeap> peer_heap_create(int rank, int size, int device, size_t bytes,
+                                           unsigned char handle[64]);
+// map the other ranks' heaps from their handles (size x 64 bytes, rank order)
+void peer_heap_connect(PeerHeap* h, const unsigned char* handles);
+// in-process shards: adopt each other's heap pointers directly
+void peer_heap_connect_local(PeerHeap* h, const std::vector<char*>& bases);
+std::unique_ptr<Comm> make_peer_comm(PeerHeap* heap);
 
 // NCCL unique id (128 bytes) for rank 0 to hand to the others.
 bool nccl_unique_id(unsigned char out[128], std::string* err);

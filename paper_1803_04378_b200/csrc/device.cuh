@@ -36,7 +36,7 @@ enum CtlStatus : int {
 
 // Sharded solves (world > 1): fixed-size messages exchanged by
 // all-gather after the local pricing and ratio passes.
-constexpr int kRatioMsgCap = 6;
+constexpr int kRatioMsgCap = 30;
 struct PriceMsg {
     double z;
     int j;
@@ -82,7 +82,7 @@ struct Ctl {
     int found;         // drive-out scan result
     double found_red;
     int no_ratio;      // FTRAN without the fused ratio test (drive-out, step API)
-    int pad;
+    int x_owner;       // sharded: this shard owns the current pivot row (k_pivot_row)
 };
 
 struct Dev {
@@ -92,7 +92,8 @@ struct Dev {
     int sharded;           // 1: a communicator is attached (even with world == 1)
     int row0, mloc;        // this shard's rows of T = [B^-1 | b_bar] and of Y
     int col0, col1;        // this shard's pricing columns (original index range)
-    double* xbuf;          // world > 1: pivot row exchange, m+3 slots summed as int64 bits
+    double* xbuf;          // sharded: pivot row exchange (m+3 slots), in the transport's symmetric heap
+    int xbuf_zero;         // transport sums int64 bit patterns: non-owners zero-fill xbuf
     PriceMsg* pmsg;        // world > 1: [0] local result, [1..world] gathered
     RatioMsg* rmsg;        // world > 1: [0] local result, [1..world] gathered
     double* cand_ratio;    // ratios of the candidates in cand (same order)

@@ -902,14 +902,22 @@ __global__ void __launch_bounds__(1024) k_ratio(Dev d) {
 // the owner's doubles bit for bit; k_pivot then runs on every shard from xbuf.
 __global__ void __launch_bounds__(256) k_pivot_row(Dev d) {
     Ctl* c = d.ctl;
-    if (c->status != ST_RUNNING) return;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c->status != ST_RUNNING) {
+        if (gtid == 0) c->x_owner = 0;
+        return;
+    }
     const int m = d.m;
     const int li = c->r - d.row0;
-    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const int gstride = gridDim.x * blockDim.x;
     long long* xb = reinterpret_cast<long long*>(d.xbuf);
-    if (li < 0 || li >= d.mloc) {
-        for (int j = gtid; j <= m + 2; j += gstride) xb[j] = 0;
+    const bool own = li >= 0 && li < d.mloc;
+    if (gtid == 0) c->x_owner = own ? 1 : 0;
+    if (!own) {
+        // summing transports need zeros from non-owners; a P2P owner writes our
+        // xbuf remotely, so we must not touch it
+        if (d.xbuf_zero)
+            for (int j = gtid; j <= m + 2; j += gstride) xb[j] = 0;
         return;
     }
     const double yr = d.Y[li];
@@ -1307,6 +1315,20 @@ void configure_kernels(Dev& d) {
     d.price_smem = (int)(d.price_S * d.price_stage_bytes + 2 * d.price_S * 8);
     cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, d.upd_smem);
     cudaFuncSetAttribute(k_price, cudaFuncAttributeMaxDynamicSharedMemorySize, d.price_smem);
+    // One shared-memory carveout for every kernel: SMs never reconfigure the
+    // L1/shared split between the streaming kernels and the small ones, and a
+    // shard's spin-waiting exchange kernel can share an SM with another shard's
+    // streaming CTA when shards share a GPU (a different carveout would make the
+    // streaming kernel wait for the spinner to exit: deadlock).
+    const void* all[] = {(const void*)k_init_tableau, (const void*)k_transpose, (const void*)k_build_nb,
+                         (const void*)k_rebuild_top, (const void*)k_price, (const void*)k_price_final,
+                         (const void*)k_update, (const void*)k_ratio_final, (const void*)k_ratio,
+                         (const void*)k_pivot_row, (const void*)k_pivot, (const void*)k_gather_row,
+                         (const void*)k_drive_scan, (const void*)k_drive_red, (const void*)k_la_x,
+                         (const void*)k_la_wp, (const void*)k_la_price, (const void*)k_la_price_local,
+                         (const void*)k_la_decide, (const void*)k_la_theta, (const void*)k_la_theta_local,
+                         (const void*)k_la_score, (const void*)k_sum_i64, (const void*)k_min_i32};
+    for (const void* f : all) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
 namespace {

@@ -18,6 +18,8 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <stdexcept>
@@ -55,6 +57,16 @@ template <class T>
 T* dalloc(size_t n) {
     void* p = nullptr;
     CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+    return static_cast<T*>(p);
+}
+
+// Stream-ordered temporaries: cudaMalloc/cudaFree may synchronise the whole
+// device, which would deadlock against another shard's spin-waiting exchange
+// kernel when shards share a GPU.
+template <class T>
+T* talloc(size_t n, cudaStream_t st) {
+    void* p = nullptr;
+    CK(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), st));
     return static_cast<T*>(p);
 }
 
@@ -142,6 +154,7 @@ private:
     bool unfused_ratio_ = false;  // debug knob (cfg.reserved[0] & 1): standalone ratio kernel
     Comm* comm_ = nullptr;
     bool sharded_ = false;        // comm_ attached: the exchange path runs even for one rank
+    bool dbg_trace_ = getenv("LPSG_TRACE_COMM") != nullptr;
     int world_ = 1, rank_ = 0;
     double* chain_ = nullptr;     // world > 1: rebuild_top_row partial sums (m+1)
 
@@ -351,7 +364,8 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     d_.Y = dalloc<double>(d_.mloc);
     d_.xrow = dalloc<double>(m + 4);
     if (sharded_) {
-        d_.xbuf = dalloc<double>(m + 4);
+        d_.xbuf = static_cast<double*>(comm_->sym_alloc(sizeof(double) * (m + 4)));
+        d_.xbuf_zero = std::strcmp(comm_->transport(), "p2p") != 0;
         d_.pmsg = dalloc<PriceMsg>(world_ + 1);
         d_.rmsg = dalloc<RatioMsg>(world_ + 1);
         chain_ = dalloc<double>(m + 1);
@@ -440,12 +454,22 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     hctl_->upd_r = -1;
     hctl_->found = INT_MAX;
     push();
+    // shards sharing a process finish their (device-synchronising) setup before
+    // any of them starts spinning in an exchange
+    if (comm_) {
+        CK(cudaStreamSynchronize(st_));
+        comm_->host_barrier();
+    }
     rebuild_top_row();
     last_objective_ = objective_value();
 }
 
 Solver::~Solver() {
     if (st_) cudaStreamSynchronize(st_);
+    if (sharded_ && d_.xbuf) {
+        comm_->sym_free(d_.xbuf);
+        if (d_.xrow == d_.xbuf) d_.xrow = nullptr;
+    }
     void* bufs[] = {d_.T, d_.top, d_.Y, d_.xrow, (void*)d_.A_cm, d_.A_nb, d_.slot2col, d_.col2slot,
                     d_.basic, d_.frozen, cost_buf_, d_.ctl, d_.cand, d_.pz, d_.pj, d_.log, scratch_, tmaps_,
                     d_.rc_theta, d_.rc_cnt, d_.rc_row, d_.rc_ratio, d_.cand_ratio, d_.pmsg, d_.rmsg,
@@ -474,6 +498,7 @@ void Solver::pull(bool with_log) {
     }
     CK(cudaStreamSynchronize(st_));
     CK(cudaGetLastError());
+    if (comm_) comm_->check();
 }
 
 double Solver::objective_value() {
@@ -544,7 +569,7 @@ void Solver::seq_pivot() {
         return;
     }
     L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot_row(d_, st_); });
-    L(K_COMM, 0.0, [&] { comm_->sum_i64(reinterpret_cast<long long*>(d_.xbuf), (size_t)m_ + 3, st_); });
+    L(K_COMM, 0.0, [&] { comm_->owner_bcast(d_.xbuf, sizeof(double) * ((size_t)m_ + 3), &d_.ctl->x_owner, st_); });
     L(K_PIVOT, 0.0, [&] { launch_pivot(d_, st_); });
 }
 
@@ -592,8 +617,8 @@ std::vector<int> Solver::gather_overflow_candidates() {
     CK(cudaMemcpy(msgs.data(), d_.rmsg + 1, sizeof(RatioMsg) * G, cudaMemcpyDeviceToHost));
     int maxn = 1;
     for (auto& mm : msgs) maxn = std::max(maxn, mm.any ? mm.n : 0);
-    int* rows_d = dalloc<int>((size_t)G * maxn);
-    double* rat_d = dalloc<double>((size_t)G * maxn);
+    int* rows_d = talloc<int>((size_t)G * maxn, st_);
+    double* rat_d = talloc<double>((size_t)G * maxn, st_);
     comm_->allgather(d_.cand, rows_d, sizeof(int) * maxn, st_);
     comm_->allgather(d_.cand_ratio, rat_d, sizeof(double) * maxn, st_);
     std::vector<int> rows((size_t)G * maxn);
@@ -601,8 +626,8 @@ std::vector<int> Solver::gather_overflow_candidates() {
     CK(cudaMemcpyAsync(rows.data(), rows_d, sizeof(int) * rows.size(), cudaMemcpyDeviceToHost, st_));
     CK(cudaMemcpyAsync(rat.data(), rat_d, sizeof(double) * rat.size(), cudaMemcpyDeviceToHost, st_));
     CK(cudaStreamSynchronize(st_));
-    cudaFree(rows_d);
-    cudaFree(rat_d);
+    CK(cudaFreeAsync(rows_d, st_));
+    CK(cudaFreeAsync(rat_d, st_));
     const double th = hctl_->theta;
     const double window = th + cfg_.ratio_tie_tol * std::max(1.0, std::fabs(th));
     std::vector<int> cand;
@@ -630,6 +655,9 @@ int Solver::run_phase() {
         enqueue_pivots(batch_);
         pull(true);
         if (prof_) flush_profile();
+        if (dbg_trace_)
+            fprintf(stderr, "[solver r%d] status %d log %d q %d r %d ncand %d iter %lld\n", rank_, hctl_->status,
+                    hctl_->log_len, hctl_->q, hctl_->r, hctl_->ncand, (long long)hctl_->total_iter);
         drain_log();
         const int st = hctl_->status;
         if (st == ST_RUNNING) {
@@ -699,21 +727,21 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     la.q = entering;
     la.nblk = (int)std::min<long long>(64, std::max<long long>((hctl_->n_scan + 255) / 256, (d_.mloc + 127) / 128));
     la.nblk = std::max(la.nblk, 1);
-    int* rows_d = dalloc<int>(kb);
+    int* rows_d = talloc<int>(kb, st_);
     la.rows = rows_d;
-    la.X = dalloc<double>((size_t)kb * ldx);
-    la.Wp = dalloc<double>((size_t)kb * ldx);
-    la.bz = dalloc<double>(kb);
-    la.bj = dalloc<int>(kb);
-    la.theta = dalloc<double>(kb);
-    la.score = dalloc<double>(kb);
-    la.part_z = dalloc<double>((size_t)kb * la.nblk);
-    la.part_j = dalloc<int>((size_t)kb * la.nblk);
-    la.part_t = dalloc<double>((size_t)kb * la.nblk);
-    la.pm = dalloc<PriceMsg>((size_t)kb);
-    la.pm_all = sharded_ ? dalloc<PriceMsg>((size_t)kb * G) : nullptr;
-    la.tl = dalloc<double>(kb);
-    la.tl_all = sharded_ ? dalloc<double>((size_t)kb * G) : nullptr;
+    la.X = talloc<double>((size_t)kb * ldx, st_);
+    la.Wp = talloc<double>((size_t)kb * ldx, st_);
+    la.bz = talloc<double>(kb, st_);
+    la.bj = talloc<int>(kb, st_);
+    la.theta = talloc<double>(kb, st_);
+    la.score = talloc<double>(kb, st_);
+    la.part_z = talloc<double>((size_t)kb * la.nblk, st_);
+    la.part_j = talloc<int>((size_t)kb * la.nblk, st_);
+    la.part_t = talloc<double>((size_t)kb * la.nblk, st_);
+    la.pm = talloc<PriceMsg>((size_t)kb, st_);
+    la.pm_all = sharded_ ? talloc<PriceMsg>((size_t)kb * G, st_) : nullptr;
+    la.tl = talloc<double>(kb, st_);
+    la.tl_all = sharded_ ? talloc<double>((size_t)kb * G, st_) : nullptr;
     CK(cudaMemsetAsync(la.X, 0, sizeof(double) * (size_t)kb * ldx, st_));
     for (int k0 = 0; k0 < K; k0 += kb) {
         la.K = std::min(kb, K - k0);
@@ -733,7 +761,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     void* bufs[] = {rows_d, la.X, la.Wp, la.bz, la.bj, la.theta, la.score, la.part_z, la.part_j, la.part_t,
                     la.pm, la.pm_all, la.tl, la.tl_all};
     for (void* p : bufs)
-        if (p) cudaFree(p);
+        if (p) CK(cudaFreeAsync(p, st_));
 }
 
 // drive_out_artificials (solver.cpp:295-316)
@@ -864,13 +892,13 @@ void Solver::get_x(double* x, int n) {
     } else {
         // every shard's b_bar rows, padded to the largest shard, in rank order
         const int pad = m_ / world_ + 1;
-        double* tmp = dalloc<double>((size_t)pad * (world_ + 1));
+        double* tmp = talloc<double>((size_t)pad * (world_ + 1), st_);
         CK(cudaMemcpyAsync(tmp, bcol, sizeof(double) * d_.mloc, cudaMemcpyDeviceToDevice, st_));
         comm_->allgather(tmp, tmp + pad, sizeof(double) * pad, st_);
         std::vector<double> all((size_t)pad * world_);
         CK(cudaMemcpyAsync(all.data(), tmp + pad, sizeof(double) * all.size(), cudaMemcpyDeviceToHost, st_));
         CK(cudaStreamSynchronize(st_));
-        cudaFree(tmp);
+        CK(cudaFreeAsync(tmp, st_));
         for (int g = 0; g < world_; ++g) {
             int r0 = 0, r1 = 0;
             lpsg_shard_range(m_, world_, g, &r0, &r1);
@@ -991,6 +1019,10 @@ struct lpsg_solver {
     std::unique_ptr<lpsg::Comm> comm;
 };
 
+struct lpsg_peer {
+    std::unique_ptr<lpsg::PeerHeap> heap;
+};
+
 namespace {
 template <class F>
 int guard(F&& f) {
@@ -1049,7 +1081,12 @@ int lpsg_create(const lpsg_problem* lp, const lpsg_config* cfg, lpsg_solver** ou
     return guard([&] {
         auto* h = new lpsg_solver{nullptr, nullptr};
         try {
-            if (c.world_size > 1 || (c.reserved[1] & 1)) {
+            if (c.peer) {
+                if (!c.peer->heap) throw lpsg::CommError("lpsg_create: peer heap not created");
+                if (c.peer->heap->device != c.device)
+                    throw lpsg::CommError("lpsg_create: peer heap lives on another device");
+                h->comm = lpsg::make_peer_comm(c.peer->heap.get());
+            } else if (c.world_size > 1 || (c.reserved[1] & 1)) {
                 h->comm = lpsg::make_nccl_comm(c.nccl_id, c.rank, std::max(1, c.world_size), c.device);
                 if (!h->comm) throw lpsg::CommError("NCCL communicator");
             }
@@ -1090,8 +1127,36 @@ int lpsg_nccl_unique_id(unsigned char out[128]) {
     return LPSG_OK;
 }
 
-int lpsg_solve_sharded(const lpsg_problem* lp, const lpsg_config* cfg, int shards, int spread, lpsg_report* rep,
+int lpsg_peer_create(int rank, int world, int device, size_t heap_bytes, lpsg_peer** out, unsigned char handle[64]) {
+    if (!out || world < 1 || world > 32 || rank < 0 || rank >= world) return bad("lpsg_peer_create: bad argument");
+    return guard([&] {
+        auto* p = new lpsg_peer;
+        try {
+            p->heap = lpsg::peer_heap_create(rank, world, device, heap_bytes, handle);
+        } catch (...) {
+            delete p;
+            throw;
+        }
+        *out = p;
+    });
+}
+
+int lpsg_peer_connect(lpsg_peer* p, const unsigned char* handles) {
+    if (!p || !handles) return bad("lpsg_peer_connect: null argument");
+    return guard([&] { lpsg::peer_heap_connect(p->heap.get(), handles); });
+}
+
+void lpsg_peer_destroy(lpsg_peer* p) { delete p; }
+
+const char* lpsg_transport(lpsg_solver* s) {
+    if (!s) return "";
+    return s->comm ? s->comm->transport() : "single";
+}
+
+int lpsg_solve_sharded(const lpsg_problem* lp, const lpsg_config* cfg, int shards, int flags, lpsg_report* rep,
                        double* x, lpsg_trace* trace, long cap, long* len) {
+    const bool spread = (flags & LPSG_SHARD_SPREAD) != 0;
+    const bool p2p = (flags & LPSG_SHARD_P2P) != 0;
     if (!lp || !rep || shards < 1 || shards > 32) return bad("lpsg_solve_sharded: bad argument");
     lpsg_config c;
     if (cfg) c = *cfg;
@@ -1102,6 +1167,7 @@ int lpsg_solve_sharded(const lpsg_problem* lp, const lpsg_config* cfg, int shard
         return LPSG_CUDA_ERROR;
     }
     lpsg::LocalHub hub(shards);
+    std::vector<char*> bases(shards, nullptr);
     std::vector<int> rc(shards, LPSG_OK);
     std::vector<std::string> msg(shards);
     std::vector<std::thread> th;
@@ -1109,10 +1175,32 @@ int lpsg_solve_sharded(const lpsg_problem* lp, const lpsg_config* cfg, int shard
         th.emplace_back([&, g] {
             lpsg_config cg = c;
             cg.world_size = 1;  // the in-process comm below, not NCCL
+            cg.peer = nullptr;
             cg.device = spread ? (c.device + g) % ndev : c.device;
+            std::unique_ptr<lpsg::PeerHeap> heap;
+            bool heap_ok = true;
+            if (p2p) {
+                // every shard allocates its heap, then all adopt each other's pointers
+                try {
+                    heap = lpsg::peer_heap_create(g, shards, cg.device, 0, nullptr);
+                    bases[g] = heap->base;
+                } catch (...) {
+                    heap_ok = false;
+                }
+                hub.barrier();
+                for (char* b : bases) heap_ok = heap_ok && b != nullptr;
+            }
             rc[g] = guard([&] {
                 CK_SET_DEVICE(cg.device);
-                std::unique_ptr<lpsg::Comm> comm = lpsg::make_local_comm(&hub, g);
+                if (!heap_ok) throw lpsg::CommError("peer heap allocation failed on some shard");
+                std::unique_ptr<lpsg::Comm> comm;
+                if (p2p) {
+                    heap->hub = &hub;
+                    lpsg::peer_heap_connect_local(heap.get(), bases);
+                    comm = lpsg::make_peer_comm(heap.get());
+                } else {
+                    comm = lpsg::make_local_comm(&hub, g);
+                }
                 lpsg::Solver s(*lp, cg, comm.get());
                 s.keep_trace = g == 0 && trace != nullptr;
                 lpsg_report r{};
@@ -1128,6 +1216,8 @@ int lpsg_solve_sharded(const lpsg_problem* lp, const lpsg_config* cfg, int shard
                 }
             });
             msg[g] = lpsg::g_err;
+            // the other shards may be blocked in an exchange with this one: say so now
+            if (rc[g] != LPSG_OK) fprintf(stderr, "lpsg: shard %d failed: %s\n", g, msg[g].c_str());
         });
     }
     for (auto& t : th) t.join();

@@ -97,6 +97,7 @@ class SolverConfig:
     rank: int = 0
     nccl_id: bytes = b""
     nccl_single: bool = False  # run the NCCL exchange path even for world_size 1 (testing)
+    peer: Optional["PeerHeap"] = None  # P2P transport (NVLink stores + flags) instead of NCCL
     experiment: int = 0        # kernel experiment knobs (results are NOT valid); 0 = production
 
     def _c(self) -> L.Config:
@@ -109,6 +110,7 @@ class SolverConfig:
         c.reserved[0] = int(self.debug_flags)
         c.world_size, c.rank = int(self.world_size), int(self.rank)
         c.reserved[1] = 1 if self.nccl_single else 0
+        c.peer = self.peer.ptr if self.peer is not None else None
         c.reserved[2] = int(self.experiment)
         if self.nccl_id:
             if len(self.nccl_id) != 128:
@@ -341,6 +343,9 @@ class SimplexSolver:
         _check(self.lib.lpsg_shard_info(self._h, *[C.byref(x) for x in v]))
         return dict(zip(("world", "rank", "row0", "rows", "col0", "col1"), (x.value for x in v)))
 
+    def transport(self) -> str:
+        return self.lib.lpsg_transport(self._h).decode()
+
     def counters(self) -> dict:
         a, b, c = C.c_long(), C.c_longlong(), C.c_longlong()
         _check(self.lib.lpsg_counters(self._h, C.byref(a), C.byref(b), C.byref(c)))
@@ -436,8 +441,40 @@ def nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
+class PeerHeap:
+    """Symmetric device heap of the P2P transport (include/lpsg.h lpsg_peer_*).
+
+    Every rank: ``h = PeerHeap(rank, world, device)``; all-gather ``h.handle``
+    (64 bytes) in rank order; ``h.connect(handles)``; pass ``SolverConfig(peer=h)``.
+    Keep it alive until the solver is closed."""
+
+    def __init__(self, rank: int, world: int, device: int = 0, heap_bytes: int = 0):
+        self.lib = L.load()
+        self.ptr = C.c_void_p()
+        buf = (C.c_ubyte * 64)()
+        _check(self.lib.lpsg_peer_create(int(rank), int(world), int(device), int(heap_bytes),
+                                         C.byref(self.ptr), buf))
+        self.handle = bytes(buf)
+
+    def connect(self, handles) -> None:
+        blob = b"".join(handles)
+        arr = (C.c_ubyte * len(blob)).from_buffer_copy(blob)
+        _check(self.lib.lpsg_peer_connect(self.ptr, arr))
+
+    def close(self) -> None:
+        if self.ptr:
+            self.lib.lpsg_peer_destroy(self.ptr)
+            self.ptr = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def solve_sharded(lp: StandardFormLP, cfg: Optional[SolverConfig] = None, shards: int = 2,
-                  spread_devices: bool = False, trace: bool = False):
+                  spread_devices: bool = False, trace: bool = False, p2p: bool = False):
     """The sharded solver in one process: `shards` host threads with in-process
     device-to-device exchanges (all on cfg.device, or spread over the visible
     GPUs). Returns (SolveReport, trace or None) of shard 0."""
@@ -449,7 +486,8 @@ def solve_sharded(lp: StandardFormLP, cfg: Optional[SolverConfig] = None, shards
     tr = np.zeros(cap, TRACE_DTYPE)
     n = C.c_long()
     prob = lp._c()
-    _check(lib.lpsg_solve_sharded(C.byref(prob), C.byref(cfg._c()), int(shards), int(spread_devices),
+    flags = (1 if spread_devices else 0) | (2 if p2p else 0)
+    _check(lib.lpsg_solve_sharded(C.byref(prob), C.byref(cfg._c()), int(shards), flags,
                                   C.byref(rep), x.ctypes.data_as(C.POINTER(C.c_double)),
                                   tr.ctypes.data_as(C.POINTER(L.Trace)) if trace else None, cap,
                                   C.byref(n)))

@@ -65,6 +65,31 @@ def test_sharded_golden_parity(name, shards):
     _check(rep, tr, g, (name, shards))
 
 
+P2P_NAMES = ["gen_256x512_f2_s1", "gen_256x512_f0_s1", "gen_1000x2000_f0_s1_max_iter400",
+             "gen_2000x4000_f0_s1_max_iter200", "netlib_scsd1", "netlib_sctap1", "netlib_boeing2",
+             "beale_3x7", "infeasible_2x2", "unbounded_1x3", "gen_128x256_f2_s5_anticyclenone"]
+
+
+@pytest.mark.parametrize("shards", [2, 3])
+@pytest.mark.parametrize("name", P2P_NAMES)
+def test_sharded_p2p_golden_parity(name, shards):
+    """The device-initiated P2P transport (peer stores + sequence flags, no host
+    synchronisation per exchange), shards sharing one B200. Limited to 2-3
+    shards: on a SHARED GPU a shard's spin-waiting exchange kernel competes for
+    SMs with the other shards' streaming kernels; with one shard per GPU (the
+    real deployment) it never does. A wait that cannot complete times out
+    (LPSG_P2P_TIMEOUT_S) instead of hanging."""
+    P = _P()
+    g = Golden(name)
+    if shards > g.m:
+        pytest.skip("fewer rows than shards")
+    lp = _golden_lp(g)
+    cfg = P.SolverConfig(max_iter=g.max_iter, pivot_tol=g.pivot_tol,
+                         anticycle=P.Anticycle(g.anticycle))
+    rep, tr = P.solve_sharded(lp, cfg, shards=shards, trace=True, p2p=True)
+    _check(rep, tr, g, (name, shards, "p2p"))
+
+
 @pytest.mark.parametrize("shards", [4, 8])
 @pytest.mark.parametrize("name", ["gen_256x512_f2_s1", "gen_128x256_f2_s5", "netlib_scsd1",
                                   "gen_256x512_f1_s1", "beale_3x7"])
@@ -90,9 +115,10 @@ def test_sharded_matches_single_gpu_prefix_c3():
         s.keep_trace(True)
         rep1 = s.solve()
         tr1 = s.trace()
-    rep4, tr4 = P.solve_sharded(lp, cfg, shards=4, trace=True)
-    assert len(tr1) == len(tr4) == 60
-    for f in ("row", "leaving", "entering"):
-        assert np.array_equal(tr1[f], tr4[f]), f
-    assert np.array_equal(_bits(tr1["objective"]), _bits(tr4["objective"]))
-    assert np.array_equal(_bits(rep1.x), _bits(rep4.x))
+    for shards, p2p in ((4, False), (2, True)):
+        rep4, tr4 = P.solve_sharded(lp, cfg, shards=shards, trace=True, p2p=p2p)
+        assert len(tr1) == len(tr4) == 60
+        for f in ("row", "leaving", "entering"):
+            assert np.array_equal(tr1[f], tr4[f]), (f, p2p)
+        assert np.array_equal(_bits(tr1["objective"]), _bits(tr4["objective"]))
+        assert np.array_equal(_bits(rep1.x), _bits(rep4.x))
