@@ -317,7 +317,7 @@ def run_ours(args, cfg):
                     "kernels": kern, "instrumented_pivots": prof_range,
                     "note": "per-kernel CUDA events on the solver stream over a second window of "
                             "K pivots (rank 0); the headline value is the un-instrumented window"}
-        t = _ncu_traffic(NCU_NAMES.get(dom, dom))
+        t = _ncu_traffic(NCU_NAMES.get(dom, dom)) if args.config == "c3" else None  # captures are of C3
         if t is not None and world == 1:
             traffic = t[0]
             roofline["traffic_source"] = f"profiles/{t[1]} (ncu --set full, one launch, DRAM read+write bytes)"

@@ -13,6 +13,7 @@
 #include <cfloat>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 
 #include <vector>
 
@@ -1287,10 +1288,13 @@ void configure_kernels(Dev& d) {
     d.upd_h = h;
     d.update_grid = (d.mloc + h - 1) / h;
     d.upd_C = h <= 64 ? 32 : h <= 160 ? 16 : 8;
+    if (const char* e = getenv("LPSG_UPD_COLS")) d.upd_C = std::max(2, atoi(e)) & ~1;  // tuning experiments
     d.upd_U = 8;
     const size_t tile_el = (size_t)d.upd_C * h;
     const size_t stage = ((tile_el + 2 * (size_t)d.upd_C) * 8 + 1023) / 1024 * 1024;
-    d.upd_S = (int)std::max<size_t>(2, std::min<size_t>(8, (size_t)(192 * 1024) / stage));
+    size_t s_cap = 8;
+    if (const char* e = getenv("LPSG_UPD_STAGES")) s_cap = (size_t)std::max(2, atoi(e));  // tuning experiments
+    d.upd_S = (int)std::max<size_t>(2, std::min<size_t>(s_cap, (size_t)(200 * 1024) / stage));
     d.upd_smem = (int)(d.upd_S * stage + 3 * d.upd_S * 8);
     d.upd_threads = (d.upd_U + (h + 31) / 32 + 1) * 32;
     // pricing: one CTA per SM over contiguous slot ranges of this shard's columns

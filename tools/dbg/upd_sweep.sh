@@ -1,0 +1,8 @@
+for cfg in "6 64" "3 64" "4 96" "3 128" "2 192" "5 80"; do
+  set -- $cfg
+  r=$(LPSG_UPD_STAGES=$1 LPSG_UPD_COLS=$2 timeout 120 python bench.py --steps 200 --warmup 20 --no-cpu-baseline --e2e-max-iter 10 | python -c "
+import json,sys
+l=json.loads(sys.stdin.read().strip().splitlines()[-1]); k=l['roofline']['kernels']
+print(round(l['value'],1), k['update_ftran']['us_per_launch'], k['price']['us_per_launch'])")
+  echo "S=$1 C=$2: $r"
+done
