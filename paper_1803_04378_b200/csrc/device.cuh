@@ -83,6 +83,7 @@ struct Ctl {
     double found_red;
     int no_ratio;      // FTRAN without the fused ratio test (drive-out, step API)
     int x_owner;       // sharded: this shard owns the current pivot row (k_pivot_row)
+    unsigned long long work[4];  // launches that did their work: price, update, pivot (profiling)
 };
 
 struct Dev {

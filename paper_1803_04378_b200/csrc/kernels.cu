@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
         warp_argmax(z, j);
         if (threadIdx.x == 0) {
             c->ticket_price = 0;
+            if (!budget_hit) c->work[0] += 1;  // a real pricing pass (profile byte accounting)
             if (d.sharded) {
                 d.pmsg[0] = PriceMsg{z, j, 0};  // merged across shards by k_price_final
             } else {
@@ -662,6 +663,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         c->ticket_update = 0;
         if (up) c->pending = 0;
         if (ft) d.top[m + 1] = c->d;
+        if (up) c->work[1] += 1;  // credited as an update pass (an FTRAN-only pass is not)
     }
     if (!do_ratio) return;
     // ---- fused ratio test, global part: the last CTA, one thread per producing
@@ -991,6 +993,7 @@ __global__ void __launch_bounds__(256) k_pivot(Dev d) {
     if (!last_block(&c->ticket_misc)) return;
     if (threadIdx.x == 0) {
         c->ticket_misc = 0;
+        c->work[2] += 1;
         // the d slot (T[0][m+1]) is every CTA's multiplier source: update it
         // only after all of them have read it
         {

@@ -175,6 +175,7 @@ public:
 
 private:
     bool prof_ = false;
+    unsigned long long work_seen_[4] = {0, 0, 0, 0};
     std::vector<cudaEvent_t> ev_pool_;
     struct EvRec {
         int kind;
@@ -221,14 +222,24 @@ void Solver::L(int kind, double bytes, F&& f) {
     ev_chain_ = b;
 }
 
+// Algorithmic bytes are credited per launch that did its work (ctl.work
+// counters), not per launch: the kernels enqueued behind a stop (budget,
+// optimality, a tie) exit at once and move nothing.
 void Solver::flush_profile() {
     std::vector<cudaEvent_t> seen;
+    const int widx[K_NUM] = {-1, 2, 0, 1, -1, -1};
+    for (int k = 0; k < K_NUM; ++k) {
+        if (widx[k] < 0) continue;
+        const unsigned long long w = hctl_->work[widx[k]];
+        kstat[k].bytes += (double)(w - work_seen_[widx[k]]) * bytes_of(k);
+        work_seen_[widx[k]] = w;
+    }
     for (auto& r : ev_used_) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, r.a, r.b));
         kstat[r.kind].launches += 1;
         kstat[r.kind].ms += ms;
-        kstat[r.kind].bytes += r.bytes;
+        if (r.kind != K_PRICE && r.kind != K_UPDATE && r.kind != K_PIVOT) kstat[r.kind].bytes += r.bytes;
         seen.push_back(r.a);
         seen.push_back(r.b);
     }
@@ -255,6 +266,7 @@ double Solver::bytes_of(int kind) const {
 void Solver::set_profile(bool on) {
     prof_ = on;
     for (auto& k : kstat) k = KStat{};
+    for (int k = 0; k < 4; ++k) work_seen_[k] = hctl_->work[k];
 }
 
 void Solver::set_max_iter(long long v) {
