@@ -137,6 +137,7 @@ struct Dev {
     const CUtensorMap* tm_nb;  // 2D TMA descriptors of A_nb, box {wbx slots, price_rows(wbx) rows}
     int price_nwc, price_S, price_smem, price_threads;
     int dbg;               // experiment knobs (cfg.reserved[2]); 0 in production
+    int pdl;               // launch the pivot chain with programmatic dependent launch
     size_t price_stage_bytes;
 };
 

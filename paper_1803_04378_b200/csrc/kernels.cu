@@ -101,6 +101,13 @@ __device__ double block_min(double v) {
     return v;
 }
 
+// Programmatic dependent launch (PDL): the pivot-chain kernels are launched
+// with programmatic stream serialization, so kernel t+1's CTAs are dispatched
+// while kernel t drains; griddepcontrol.wait then blocks until kernel t has
+// completed and its writes are visible. Both are no-ops without PDL.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Returns true in exactly one thread of the last CTA to arrive (threadfence
 // reduction pattern); all CTAs must call it.
 __device__ bool last_block(unsigned int* ticket) {
@@ -280,6 +287,8 @@ __device__ __forceinline__ void chain_group(double& acc0, double& acc1, const do
 // (max z, min j) reduction is finished by the last CTA.
 __global__ void __launch_bounds__(384) k_price(Dev d) {
     extern __shared__ __align__(1024) unsigned char smem[];
+    pdl_wait();
+    pdl_trigger();
     Ctl* c = d.ctl;
     if (c->status != ST_RUNNING) return;
     const bool budget_hit = c->total_iter >= c->budget;
@@ -505,6 +514,8 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
 //     sequential chain in ascending j, reading the updated tile.
 __global__ void __launch_bounds__(512) k_update(Dev d) {
     extern __shared__ __align__(1024) unsigned char smem[];
+    pdl_wait();
+    pdl_trigger();
     Ctl* c = d.ctl;
     const int status = c->status;
     const bool up = c->pending != 0;
@@ -833,6 +844,8 @@ __global__ void k_ratio_final(Dev d) {
 // block compaction. One candidate (or anticycle = none) resolves on device;
 // two or more under tabu hand over to the host (ST_TIE).
 __global__ void __launch_bounds__(1024) k_ratio(Dev d) {
+    pdl_wait();
+    pdl_trigger();
     Ctl* c = d.ctl;
     if (c->status != ST_RUNNING || c->pending) return;
     const int m = d.m;
@@ -937,6 +950,8 @@ __global__ void __launch_bounds__(256) k_pivot_row(Dev d) {
 }
 
 __global__ void __launch_bounds__(256) k_pivot(Dev d) {
+    pdl_wait();
+    pdl_trigger();
     Ctl* c = d.ctl;
     if (c->status != ST_RUNNING) return;
     const int m = d.m;
@@ -1273,12 +1288,34 @@ void launch_price_final(const Dev& d, cudaStream_t st) { k_price_final<<<1, 32, 
 
 void launch_ratio_final(const Dev& d, cudaStream_t st) { k_ratio_final<<<1, 32, 0, st>>>(d); }
 
+namespace {
+// Launch with programmatic stream serialization when d.pdl (single-GPU pivot chain).
+template <class K>
+void launch_chain(const Dev& d, K kernel, unsigned grid, unsigned block, size_t smem, cudaStream_t st) {
+    if (!d.pdl) {
+        kernel<<<grid, block, smem, st>>>(d);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, d);
+}
+}  // namespace
+
 void launch_price(const Dev& d, cudaStream_t st) {
-    k_price<<<d.price_grid, d.price_threads, d.price_smem, st>>>(d);
+    launch_chain(d, k_price, d.price_grid, d.price_threads, d.price_smem, st);
 }
 
 void launch_update(const Dev& d, cudaStream_t st) {
-    k_update<<<d.update_grid, d.upd_threads, d.upd_smem, st>>>(d);
+    launch_chain(d, k_update, d.update_grid, d.upd_threads, d.upd_smem, st);
 }
 
 // Launch geometry of the streaming kernels and their TMA
@@ -1394,9 +1431,9 @@ bool create_tensor_maps(Dev& d, CUtensorMap** dev_maps, int* count) {
     return true;
 }
 
-void launch_ratio(const Dev& d, cudaStream_t st) { k_ratio<<<1, 1024, 0, st>>>(d); }
+void launch_ratio(const Dev& d, cudaStream_t st) { launch_chain(d, k_ratio, 1, 1024, 0, st); }
 
-void launch_pivot(const Dev& d, cudaStream_t st) { k_pivot<<<d.pivot_grid, 256, 0, st>>>(d); }
+void launch_pivot(const Dev& d, cudaStream_t st) { launch_chain(d, k_pivot, d.pivot_grid, 256, 0, st); }
 
 void launch_pivot_row(const Dev& d, cudaStream_t st) { k_pivot_row<<<d.pivot_grid, 256, 0, st>>>(d); }
 
