@@ -187,7 +187,8 @@ struct LookaheadDev {
     PriceMsg* pm_all; // world x K
     double* tl;       // K local theta'
     double* tl_all;   // world x K
-    int nblk;         // partial blocks per candidate
+    int nblk;         // pricing partials per candidate (64-slot tiles + 1 leaving column)
+    int nblk_t;       // theta' partials per candidate (64-row tiles)
     int q;            // entering column
     double d;         // entering reduced cost
 };

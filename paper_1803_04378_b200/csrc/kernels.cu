@@ -1162,6 +1162,201 @@ __global__ void __launch_bounds__(256) k_la_price(Dev d, LookaheadDev la) {
     }
 }
 
+// ---- register-tiled batched lookahead (a SIMT "GEMM" with sequential sums) --
+// The K candidates share every A_nb / T element they read: a CTA computes a
+// 64 x 64 tile of outputs (4 x 4 per thread, 16 independent chains hide the
+// DADD latency) and stages 16-deep chunks of both operands in shared memory,
+// so A_nb and T are read once per 64 candidates instead of once per candidate.
+// Each output is still one chain in ascending reduction index, bit for bit the
+// reference's dot (solver.cpp:190-200, 203-210).
+constexpr int kLT = 64;  // tile edge
+constexpr int kLC = 16;  // reduction chunk
+
+// z_k(s) = dot(W'_k, a_s) - c_j over this shard's slots (j = slot2col[s] != q):
+// the best (z, j) of the tile's 64 slots per candidate -> part_z/part_j[k][bx].
+__global__ void __launch_bounds__(256) k_la_gemm_price(Dev d, LookaheadDev la) {
+    __shared__ double Ws[kLC][kLT + 1];  // [i][k]
+    __shared__ double As[kLC][kLT];      // [i][s]
+    const int n_scan = d.ctl->n_scan;
+    const double* cost = phase_cost(d, d.ctl->phase);
+    const int s0 = blockIdx.x * kLT, k0 = blockIdx.y * kLT;
+    const int t = threadIdx.x, tk = t >> 4, ts = t & 15;
+    const int m = d.m;
+    double acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+    for (int i0 = 0; i0 < m; i0 += kLC) {
+        for (int e = t; e < kLC * kLT; e += 256) {
+            const int ii = e % kLC, kk = e / kLC;
+            const int k = k0 + kk, i = i0 + ii;
+            Ws[ii][kk] = (k < la.K && i < m) ? la.Wp[(size_t)k * la.ldx + i] : 0.0;
+            const int ss = e % kLT, ia = e / kLT;
+            const int sl = s0 + ss, i2 = i0 + ia;
+            As[ia][ss] = (sl < n_scan && i2 < m) ? d.A_nb[(size_t)i2 * d.ld_nb + sl] : 0.0;
+        }
+        __syncthreads();
+        const int lim = min(kLC, m - i0);
+        for (int ii = 0; ii < lim; ++ii) {
+            double w[4], a[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                w[u] = Ws[ii][tk + 16 * u];
+                a[u] = As[ii][ts + 16 * u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) acc[u][v] = dadd(acc[u][v], dmul(w[u], a[v]));
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        double bz = -kInf;
+        int bj = INT_MAX;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const int sl = s0 + ts + 16 * v;
+            if (sl < n_scan) {
+                const int j = d.slot2col[sl];
+                if (j != la.q) {
+                    const double z = dsub(acc[u][v], cost[j]);
+                    if (better(z, j, bz, bj)) { bz = z; bj = j; }
+                }
+            }
+        }
+        for (int o = 8; o > 0; o >>= 1) {  // the 16 lanes sharing candidate tk + 16u
+            const double oz = __shfl_xor_sync(0xffffffffu, bz, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (better(oz, oj, bz, bj)) { bz = oz; bj = oj; }
+        }
+        const int k = k0 + tk + 16 * u;
+        if (ts == 0 && k < la.K) {
+            la.part_z[(size_t)k * la.nblk + blockIdx.x] = bz;
+            la.part_j[(size_t)k * la.nblk + blockIdx.x] = bj;
+        }
+    }
+}
+
+// The leaving variable of candidate k re-enters the nonbasic set
+// (solver.cpp:186-188): priced by the shard owning its column, into the last
+// partial slot (index nblk - 1).
+__global__ void k_la_leave(Dev d, LookaheadDev la) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= la.K) return;
+    double bz = -kInf;
+    int bj = INT_MAX;
+    const int p = d.basic[la.rows[k]];
+    if (p < d.n_total && p != la.q && p >= d.col0 && p < d.col1) {
+        const double* cost = phase_cost(d, d.ctl->phase);
+        const double* __restrict__ w = la.Wp + (size_t)k * la.ldx;
+        const double* __restrict__ a = d.A_cm + (size_t)p * d.ld_cm;
+        double acc = 0.0;
+        for (int i = 0; i < d.m; ++i) acc = dadd(acc, dmul(w[i], a[i]));
+        bz = dsub(acc, cost[p]);
+        bj = p;
+    }
+    la.part_z[(size_t)k * la.nblk + la.nblk - 1] = bz;
+    la.part_j[(size_t)k * la.nblk + la.nblk - 1] = bj;
+}
+
+// y'_ik = sum_j t_ij(k) a_{b_k}[j] for this shard's rows, t = X_kj on the
+// candidate's own row, T_ij where y_i == 0, else T_ij - y_i X_kj (solver.cpp:
+// 177-184, 203-210); theta'_k partial (min ratio) per 64-row tile -> part_t[k][bx].
+__global__ void __launch_bounds__(256) k_la_gemm_theta(Dev d, LookaheadDev la) {
+    __shared__ double Ts[kLC][kLT];      // [j][i]
+    __shared__ double Xs[kLC][kLT + 1];  // [j][k]
+    __shared__ double Bs[kLC][kLT + 1];  // [j][k]  a_{b_k}[j]
+    __shared__ int s_bj[kLT], s_rk[kLT];
+    const int m = d.m;
+    const int i0 = blockIdx.x * kLT, k0 = blockIdx.y * kLT;
+    const int t = threadIdx.x, ti = t & 15, tk = t >> 4;
+    if (t < kLT) {
+        const int k = k0 + t;
+        s_bj[t] = k < la.K ? la.bj[k] : -1;
+        s_rk[t] = k < la.K ? la.rows[k] : -1;
+    }
+    __syncthreads();
+    bool any = false;
+    for (int kk = 0; kk < kLT; ++kk) any |= s_bj[kk] >= 0;
+    if (!any) {  // no candidate of this tile has an entering column: score 0
+        if (ti == 0)
+            for (int v = 0; v < 4; ++v) {
+                const int k = k0 + tk + 16 * v;
+                if (k < la.K) la.part_t[(size_t)k * la.nblk_t + blockIdx.x] = kInf;
+            }
+        return;
+    }
+    double yv[4];
+    bool rowok[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int li = i0 + ti + 16 * u;
+        rowok[u] = li < d.mloc;
+        yv[u] = rowok[u] ? d.Y[li] : 0.0;
+    }
+    double acc[4][4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+    for (int j0 = 0; j0 < m; j0 += kLC) {
+        for (int e = t; e < kLC * kLT; e += 256) {
+            const int ii = e % kLT, jj = e / kLT;
+            const int li = i0 + ii, j = j0 + jj;
+            Ts[jj][ii] = (li < d.mloc && j < m) ? d.T[(size_t)j * d.ldT + li] : 0.0;
+            const int jx = e % kLC, kk = e / kLC;
+            const int k = k0 + kk, j2 = j0 + jx;
+            const bool okk = k < la.K && j2 < m;
+            Xs[jx][kk] = okk ? la.X[(size_t)k * la.ldx + j2] : 0.0;
+            Bs[jx][kk] = (okk && s_bj[kk] >= 0) ? d.A_cm[(size_t)s_bj[kk] * d.ld_cm + j2] : 0.0;
+        }
+        __syncthreads();
+        const int lim = min(kLC, m - j0);
+        for (int jj = 0; jj < lim; ++jj) {
+            double tv[4], xv[4], bv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                tv[u] = Ts[jj][ti + 16 * u];
+                xv[u] = Xs[jj][tk + 16 * u];
+                bv[u] = Bs[jj][tk + 16 * u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    const int li = i0 + ti + 16 * u;
+                    const bool own = d.row0 + li == s_rk[tk + 16 * v];
+                    const double tij = own ? xv[v] : (yv[u] == 0.0 ? tv[u] : dsub(tv[u], dmul(yv[u], xv[v])));
+                    acc[u][v] = dadd(acc[u][v], dmul(tij, bv[v]));
+                }
+        }
+        __syncthreads();
+    }
+    const double* bcol = d.T + (size_t)m * d.ldT;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        const int kk = tk + 16 * v, k = k0 + kk;
+        double th = kInf;
+        if (k < la.K && s_bj[kk] >= 0) {
+            const double xm = la.X[(size_t)k * la.ldx + m];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int li = i0 + ti + 16 * u;
+                if (!rowok[u] || d.frozen[d.row0 + li]) continue;
+                if (acc[u][v] <= d.pivot_tol) continue;
+                const bool own = d.row0 + li == s_rk[kk];
+                const double bb = own ? xm : (yv[u] == 0.0 ? bcol[li] : dsub(bcol[li], dmul(yv[u], xm)));
+                th = min_keep(th, ddiv(bb, acc[u][v]));
+            }
+        }
+        for (int o = 8; o > 0; o >>= 1) th = min_keep(th, __shfl_xor_sync(0xffffffffu, th, o));
+        if (ti == 0 && k < la.K) la.part_t[(size_t)k * la.nblk_t + blockIdx.x] = th;
+    }
+}
+
 __global__ void k_la_price_local(Dev d, LookaheadDev la) {
     const int k = blockIdx.x;
     if (threadIdx.x >= 32) return;
@@ -1230,7 +1425,7 @@ __global__ void k_la_theta_local(Dev d, LookaheadDev la) {
     if (k >= la.K) return;
     double t = kInf;
     if (la.bj[k] >= 0)
-        for (int b = 0; b < la.nblk; ++b) t = min_keep(t, la.part_t[(size_t)k * la.nblk + b]);
+        for (int b = 0; b < la.nblk_t; ++b) t = min_keep(t, la.part_t[(size_t)k * la.nblk_t + b]);
     la.tl[k] = t;
 }
 
@@ -1370,6 +1565,7 @@ void configure_kernels(Dev& d) {
                          (const void*)k_pivot_row, (const void*)k_pivot, (const void*)k_gather_row,
                          (const void*)k_drive_scan, (const void*)k_drive_red, (const void*)k_la_x,
                          (const void*)k_la_wp, (const void*)k_la_price, (const void*)k_la_price_local,
+                         (const void*)k_la_gemm_price, (const void*)k_la_gemm_theta, (const void*)k_la_leave,
                          (const void*)k_la_decide, (const void*)k_la_theta, (const void*)k_la_theta_local,
                          (const void*)k_la_score, (const void*)k_sum_i64, (const void*)k_min_i32};
     for (const void* f : all) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1453,7 +1649,9 @@ void launch_la_x(const Dev& d, LookaheadDev& la, cudaStream_t st) {
 
 void launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     k_la_wp<<<dim3((d.m + 255) / 256, la.K), 256, 0, st>>>(d, la);
-    k_la_price<<<dim3(la.nblk, la.K), 256, 0, st>>>(d, la);
+    // la.nblk = slot tiles + 1 (the last partial holds the leaving column)
+    if (la.nblk > 1) k_la_gemm_price<<<dim3(la.nblk - 1, (la.K + kLT - 1) / kLT), 256, 0, st>>>(d, la);
+    k_la_leave<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);
     k_la_price_local<<<la.K, 32, 0, st>>>(d, la);
 }
 
@@ -1462,7 +1660,7 @@ void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int 
 }
 
 void launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st) {
-    k_la_theta<<<dim3(la.nblk, la.K), 128, 0, st>>>(d, la);
+    k_la_gemm_theta<<<dim3(la.nblk_t, (la.K + kLT - 1) / kLT), 256, 0, st>>>(d, la);
     k_la_theta_local<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);
 }
 

@@ -738,8 +738,8 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     LookaheadDev la{};
     la.ldx = ldx;
     la.q = entering;
-    la.nblk = (int)std::min<long long>(64, std::max<long long>((hctl_->n_scan + 255) / 256, (d_.mloc + 127) / 128));
-    la.nblk = std::max(la.nblk, 1);
+    la.nblk = (hctl_->n_scan + 63) / 64 + 1;  // 64-slot tiles + the leaving column
+    la.nblk_t = std::max(1, (d_.mloc + 63) / 64);
     int* rows_d = talloc<int>(kb, st_);
     la.rows = rows_d;
     la.X = talloc<double>((size_t)kb * ldx, st_);
@@ -750,7 +750,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     la.score = talloc<double>(kb, st_);
     la.part_z = talloc<double>((size_t)kb * la.nblk, st_);
     la.part_j = talloc<int>((size_t)kb * la.nblk, st_);
-    la.part_t = talloc<double>((size_t)kb * la.nblk, st_);
+    la.part_t = talloc<double>((size_t)kb * la.nblk_t, st_);
     la.pm = talloc<PriceMsg>((size_t)kb, st_);
     la.pm_all = sharded_ ? talloc<PriceMsg>((size_t)kb * G, st_) : nullptr;
     la.tl = talloc<double>(kb, st_);
