@@ -1126,42 +1126,6 @@ __global__ void k_la_wp(Dev d, LookaheadDev la) {
     }
 }
 
-__global__ void __launch_bounds__(256) k_la_price(Dev d, LookaheadDev la) {
-    const int k = blockIdx.y;
-    const int n_scan = d.ctl->n_scan;
-    const double* cost = phase_cost(d, d.ctl->phase);
-    const double* __restrict__ w = la.Wp + (size_t)k * la.ldx;
-    const int m = d.m;
-    double bz = -kInf;
-    int bj = INT_MAX;
-    for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < n_scan; s += gridDim.x * blockDim.x) {
-        const int j = d.slot2col[s];
-        if (j == la.q) continue;
-        const double* __restrict__ a = d.A_nb + s;
-        double acc = 0.0;
-        for (int i = 0; i < m; ++i) acc = dadd(acc, dmul(w[i], a[(size_t)i * d.ld_nb]));
-        const double z = dsub(acc, cost[j]);
-        if (better(z, j, bz, bj)) { bz = z; bj = j; }
-    }
-    // the leaving variable becomes nonbasic (solver.cpp:186-188); priced by the
-    // shard that owns its column
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        const int p = d.basic[la.rows[k]];
-        if (p < d.n_total && p != la.q && p >= d.col0 && p < d.col1) {
-            const double* __restrict__ a = d.A_cm + (size_t)p * d.ld_cm;
-            double acc = 0.0;
-            for (int i = 0; i < m; ++i) acc = dadd(acc, dmul(w[i], a[i]));
-            const double z = dsub(acc, cost[p]);
-            if (better(z, p, bz, bj)) { bz = z; bj = p; }
-        }
-    }
-    block_argmax(bz, bj);
-    if (threadIdx.x == 0) {
-        la.part_z[(size_t)k * la.nblk + blockIdx.x] = bz;
-        la.part_j[(size_t)k * la.nblk + blockIdx.x] = bj;
-    }
-}
-
 // ---- register-tiled batched lookahead (a SIMT "GEMM" with sequential sums) --
 // The K candidates share every A_nb / T element they read: a CTA computes a
 // 64 x 64 tile of outputs (4 x 4 per thread, 16 independent chains hide the
@@ -1386,40 +1350,6 @@ __global__ void k_la_decide(Dev d, LookaheadDev la, const PriceMsg* __restrict__
     la.bj[k] = (j == INT_MAX || z <= d.opt_tol) ? -1 : j;
 }
 
-__global__ void __launch_bounds__(128) k_la_theta(Dev d, LookaheadDev la) {
-    const int k = blockIdx.y;
-    const int bj = la.bj[k];
-    if (bj < 0) return;
-    const int m = d.m;
-    const int rk = la.rows[k];
-    const double* __restrict__ X = la.X + (size_t)k * la.ldx;
-    const double* __restrict__ a = d.A_cm + (size_t)bj * d.ld_cm;
-    double theta = kInf;
-    for (int li = blockIdx.x * blockDim.x + threadIdx.x; li < d.mloc; li += gridDim.x * blockDim.x) {
-        const int i = d.row0 + li;
-        if (d.frozen[i]) continue;
-        const double yi = d.Y[li];
-        const double* __restrict__ col = d.T + li;
-        double acc = 0.0;
-        double bb;
-        if (i == rk) {
-            for (int j = 0; j < m; ++j) acc = dadd(acc, dmul(X[j], a[j]));
-            bb = X[m];
-        } else if (yi == 0.0) {
-            for (int j = 0; j < m; ++j) acc = dadd(acc, dmul(col[(size_t)j * d.ldT], a[j]));
-            bb = col[(size_t)m * d.ldT];
-        } else {
-            for (int j = 0; j < m; ++j)
-                acc = dadd(acc, dmul(dsub(col[(size_t)j * d.ldT], dmul(yi, X[j])), a[j]));
-            bb = dsub(col[(size_t)m * d.ldT], dmul(yi, X[m]));
-        }
-        if (acc <= d.pivot_tol) continue;
-        theta = min_keep(theta, ddiv(bb, acc));
-    }
-    theta = block_min(theta);
-    if (threadIdx.x == 0) la.part_t[(size_t)k * la.nblk + blockIdx.x] = theta;
-}
-
 __global__ void k_la_theta_local(Dev d, LookaheadDev la) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= la.K) return;
@@ -1564,9 +1494,9 @@ void configure_kernels(Dev& d) {
                          (const void*)k_update, (const void*)k_ratio_final, (const void*)k_ratio,
                          (const void*)k_pivot_row, (const void*)k_pivot, (const void*)k_gather_row,
                          (const void*)k_drive_scan, (const void*)k_drive_red, (const void*)k_la_x,
-                         (const void*)k_la_wp, (const void*)k_la_price, (const void*)k_la_price_local,
+                         (const void*)k_la_wp, (const void*)k_la_price_local,
                          (const void*)k_la_gemm_price, (const void*)k_la_gemm_theta, (const void*)k_la_leave,
-                         (const void*)k_la_decide, (const void*)k_la_theta, (const void*)k_la_theta_local,
+                         (const void*)k_la_decide, (const void*)k_la_theta_local,
                          (const void*)k_la_score, (const void*)k_sum_i64, (const void*)k_min_i32};
     for (const void* f : all) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
