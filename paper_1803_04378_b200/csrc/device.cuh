@@ -138,6 +138,7 @@ struct Dev {
     int price_nwc, price_S, price_smem, price_threads;
     int dbg;               // experiment knobs (cfg.reserved[2]); 0 in production
     int pdl;               // launch the pivot chain with programmatic dependent launch
+    int upd_tma_store;     // k_update writes tiles back with TMA stores (else per-warp STG)
     size_t price_stage_bytes;
 };
 

@@ -245,6 +245,19 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         "l"(map), "r"(x), "r"(y), "r"(su32(b))
         : "memory");
 }
+// TMA tile store (shared -> global) in a bulk async-group.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(x),
+        "r"(y), "r"(su32(src))
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -458,6 +471,7 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
     }
     const size_t ldT = (size_t)d.ldT;
     const bool nomath = (d.dbg & 4) != 0;  // experiment: stores without the update math
+    const bool tstore = d.upd_tma_store != 0;  // the tile goes back by TMA store (producer warp)
     double2* const gbase = reinterpret_cast<double2*>(d.T + i0) + lane;  // + col * ldT/2
     const int ncols = m + 1;
     int st = 0;
@@ -479,7 +493,7 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
                     if (ok[u]) {
                         double2 tv = tcol[32 * u];
                         if (nomath) {
-                            gcol[32 * u] = tv;
+                            if (!tstore) gcol[32 * u] = tv;
                             continue;
                         }
                         const double p0 = dmul(ny0[u], xj);
@@ -489,7 +503,7 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
                         tv.x = (p0 != 0.0) ? s0v : tv.x;
                         tv.y = (p1 != 0.0) ? s1v : tv.y;
                         tcol[32 * u] = tv;
-                        gcol[32 * u] = tv;
+                        if (!tstore) gcol[32 * u] = tv;
                     }
                 }
             }
@@ -538,7 +552,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         for (int k = 0; k < S; ++k) {
             mbar_init(&full[k], 1);
             mbar_init(&upd[k], U);
-            mbar_init(&empty[k], F);
+            mbar_init(&empty[k], F + (up && d.upd_tma_store ? 1 : 0));
         }
         mbar_fence_init();
     }
@@ -568,6 +582,19 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                 }
                 if (++st == S) { st = 0; ph ^= 1; }
             }
+        } else if (lane == 1 && up && d.upd_tma_store) {
+            // ---- storer: each updated tile goes back to HBM with one TMA store;
+            // the stage is released once the store has read shared memory
+            int st = 0;
+            uint32_t ph = 0;
+            for (int k = 0; k < nst; ++k) {
+                mbar_wait(&upd[st], ph);
+                tma_store_2d(d.tm_T, i0, k * C, smem + (size_t)st * stage_stride);
+                bulk_wait_read_all();
+                mbar_arrive(&empty[st]);
+                if (++st == S) { st = 0; ph ^= 1; }
+            }
+            bulk_wait_all();
         }
     } else if (warp < U) {
         // ---- update warps: warp-per-column, lane-per-row-pair (double2), rows

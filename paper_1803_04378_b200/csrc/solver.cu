@@ -365,6 +365,7 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     d_.anticycle = cfg_.anticycle;
     d_.dbg = cfg_.reserved[2];
     d_.pdl = (!comm && getenv("LPSG_NO_PDL") == nullptr) ? 1 : 0;
+    d_.upd_tma_store = getenv("LPSG_UPD_STG") == nullptr ? 1 : 0;
     configure_kernels(d_);
     CK(cudaGetLastError());
     d_.ldT = round_up(std::max<long long>(d_.mloc + 1, (long long)d_.update_grid * d_.upd_h), 32);
