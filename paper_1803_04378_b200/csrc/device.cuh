@@ -142,26 +142,28 @@ struct Dev {
     size_t price_stage_bytes;
 };
 
-// Pricing geometry for n_scan active slots over G CTAs: each CTA owns w slots
-// (multiple of 8) loaded as nb TMA boxes of wbx <= 256 slots x R rows.
+// Pricing geometry for n_scan active slots over G CTAs. The slots are dealt
+// out in units of 8 so every CTA gets floor or ceil(units / G) of them (CTA b
+// owns [s0, s0 + own)). The CTA loads nb TMA boxes of wbx <= 256 slots x R rows.
 struct PriceGeom {
-    int w, nb, wbx, R;
+    int w, nb, wbx, R, s0, own;
 };
-// Rows per pricing stage: ~48 KB of A_nb per box, a multiple of 16 rows (the
-// consumer runs 8-row groups in pairs) so full stages have no row tail and the
-// per-stage barrier / pipeline-restart cost is amortised over many rows.
 __host__ __device__ inline int price_rows(int wbx) {
     int R = (48 * 1024) / (8 * wbx);
     R &= ~15;
     return R < 16 ? 16 : (R > 256 ? 256 : R);
 }
-__host__ __device__ inline PriceGeom price_geom(int n_scan, int G) {
-    int w = (n_scan + G - 1) / G;
-    if (w < 8) w = 8;
+__host__ __device__ inline PriceGeom price_geom(int n_scan, int G, int b = 0) {
+    const int units = (n_scan + 7) / 8;
+    const int q = units / G, rem = units % G;
+    const int wu = q + (b < rem ? 1 : 0);
+    PriceGeom g;
+    g.own = 8 * wu;
+    g.s0 = 8 * (b * q + (b < rem ? b : rem));
+    int w = g.own < 8 ? 8 : g.own;
     const int nb = (w + 255) / 256;
     int wbx = (w + nb - 1) / nb;
     wbx = (wbx + 7) & ~7;
-    PriceGeom g;
     g.nb = nb;
     g.wbx = wbx;
     g.w = nb * wbx;

@@ -309,9 +309,9 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
     const double* cost = phase_cost(d, c->phase);
     const int m = d.m;
     const int G = gridDim.x;
-    const PriceGeom g = price_geom(n_scan, G);
-    const int s0 = blockIdx.x * g.w;
-    const int ns = max(0, min(g.w, n_scan - s0));
+    const PriceGeom g = price_geom(n_scan, G, blockIdx.x);
+    const int s0 = g.s0;
+    const int ns = max(0, min(g.own, n_scan - s0));
     const int nwc = d.price_nwc;
     const int S = d.price_S;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -1,4 +1,4 @@
-for cfg in "6 64" "3 64" "4 96" "3 128" "2 192" "5 80"; do
+for cfg in "8 32" "4 64" "6 48" "12 24" "3 96"; do
   set -- $cfg
   r=$(LPSG_UPD_STAGES=$1 LPSG_UPD_COLS=$2 timeout 120 python bench.py --steps 200 --warmup 20 --no-cpu-baseline --e2e-max-iter 10 | python -c "
 import json,sys
