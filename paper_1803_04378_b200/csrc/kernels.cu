@@ -1165,7 +1165,7 @@ constexpr int kLC = 16;  // reduction chunk
 
 // z_k(s) = dot(W'_k, a_s) - c_j over this shard's slots (j = slot2col[s] != q):
 // the best (z, j) of the tile's 64 slots per candidate -> part_z/part_j[k][bx].
-__global__ void __launch_bounds__(256) k_la_gemm_price(Dev d, LookaheadDev la) {
+__global__ void __launch_bounds__(256, 2) k_la_gemm_price(Dev d, LookaheadDev la) {
     __shared__ double Ws[kLC][kLT + 1];  // [i][k]
     __shared__ double As[kLC][kLT];      // [i][s]
     const int n_scan = d.ctl->n_scan;
@@ -1178,16 +1178,30 @@ __global__ void __launch_bounds__(256) k_la_gemm_price(Dev d, LookaheadDev la) {
     for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-    for (int i0 = 0; i0 < m; i0 += kLC) {
-        for (int e = t; e < kLC * kLT; e += 256) {
+    // chunk c+1 is fetched into registers while chunk c is consumed
+    double rw[4], ra[4];
+    auto fetch = [&](int i0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = t + 256 * q;
             const int ii = e % kLC, kk = e / kLC;
             const int k = k0 + kk, i = i0 + ii;
-            Ws[ii][kk] = (k < la.K && i < m) ? la.Wp[(size_t)k * la.ldx + i] : 0.0;
+            rw[q] = (k < la.K && i < m) ? la.Wp[(size_t)k * la.ldx + i] : 0.0;
             const int ss = e % kLT, ia = e / kLT;
             const int sl = s0 + ss, i2 = i0 + ia;
-            As[ia][ss] = (sl < n_scan && i2 < m) ? d.A_nb[(size_t)i2 * d.ld_nb + sl] : 0.0;
+            ra[q] = (sl < n_scan && i2 < m) ? d.A_nb[(size_t)i2 * d.ld_nb + sl] : 0.0;
+        }
+    };
+    fetch(0);
+    for (int i0 = 0; i0 < m; i0 += kLC) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = t + 256 * q;
+            Ws[e % kLC][e / kLC] = rw[q];
+            As[e / kLT][e % kLT] = ra[q];
         }
         __syncthreads();
+        if (i0 + kLC < m) fetch(i0 + kLC);
         const int lim = min(kLC, m - i0);
         for (int ii = 0; ii < lim; ++ii) {
             double w[4], a[4];
@@ -1256,7 +1270,7 @@ __global__ void k_la_leave(Dev d, LookaheadDev la) {
 // y'_ik = sum_j t_ij(k) a_{b_k}[j] for this shard's rows, t = X_kj on the
 // candidate's own row, T_ij where y_i == 0, else T_ij - y_i X_kj (solver.cpp:
 // 177-184, 203-210); theta'_k partial (min ratio) per 64-row tile -> part_t[k][bx].
-__global__ void __launch_bounds__(256) k_la_gemm_theta(Dev d, LookaheadDev la) {
+__global__ void __launch_bounds__(256, 2) k_la_gemm_theta(Dev d, LookaheadDev la) {
     __shared__ double Ts[kLC][kLT];      // [j][i]
     __shared__ double Xs[kLC][kLT + 1];  // [j][k]
     __shared__ double Bs[kLC][kLT + 1];  // [j][k]  a_{b_k}[j]
@@ -1293,18 +1307,43 @@ __global__ void __launch_bounds__(256) k_la_gemm_theta(Dev d, LookaheadDev la) {
     for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-    for (int j0 = 0; j0 < m; j0 += kLC) {
-        for (int e = t; e < kLC * kLT; e += 256) {
+    // per-chain row kind, fixed for the whole reduction: the candidate's own row
+    // takes X, rows with y_i == 0 keep T, the others T - y_i X
+    unsigned own_mask = 0, zero_mask = 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int li = i0 + ti + 16 * u;
+        if (yv[u] == 0.0) zero_mask |= 1u << u;
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+            if (d.row0 + li == s_rk[tk + 16 * v]) own_mask |= 1u << (4 * u + v);
+    }
+    double rt[4], rx[4], rb[4];
+    auto fetch = [&](int j0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = t + 256 * q;
             const int ii = e % kLT, jj = e / kLT;
             const int li = i0 + ii, j = j0 + jj;
-            Ts[jj][ii] = (li < d.mloc && j < m) ? d.T[(size_t)j * d.ldT + li] : 0.0;
+            rt[q] = (li < d.mloc && j < m) ? d.T[(size_t)j * d.ldT + li] : 0.0;
             const int jx = e % kLC, kk = e / kLC;
             const int k = k0 + kk, j2 = j0 + jx;
             const bool okk = k < la.K && j2 < m;
-            Xs[jx][kk] = okk ? la.X[(size_t)k * la.ldx + j2] : 0.0;
-            Bs[jx][kk] = (okk && s_bj[kk] >= 0) ? d.A_cm[(size_t)s_bj[kk] * d.ld_cm + j2] : 0.0;
+            rx[q] = okk ? la.X[(size_t)k * la.ldx + j2] : 0.0;
+            rb[q] = (okk && s_bj[kk] >= 0) ? d.A_cm[(size_t)s_bj[kk] * d.ld_cm + j2] : 0.0;
+        }
+    };
+    fetch(0);
+    for (int j0 = 0; j0 < m; j0 += kLC) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int e = t + 256 * q;
+            Ts[e / kLT][e % kLT] = rt[q];
+            Xs[e % kLC][e / kLC] = rx[q];
+            Bs[e % kLC][e / kLC] = rb[q];
         }
         __syncthreads();
+        if (j0 + kLC < m) fetch(j0 + kLC);
         const int lim = min(kLC, m - j0);
         for (int jj = 0; jj < lim; ++jj) {
             double tv[4], xv[4], bv[4];
@@ -1318,9 +1357,9 @@ __global__ void __launch_bounds__(256) k_la_gemm_theta(Dev d, LookaheadDev la) {
             for (int u = 0; u < 4; ++u)
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
-                    const int li = i0 + ti + 16 * u;
-                    const bool own = d.row0 + li == s_rk[tk + 16 * v];
-                    const double tij = own ? xv[v] : (yv[u] == 0.0 ? tv[u] : dsub(tv[u], dmul(yv[u], xv[v])));
+                    const double sub = dsub(tv[u], dmul(yv[u], xv[v]));
+                    const double tij = (own_mask >> (4 * u + v)) & 1u ? xv[v]
+                                       : ((zero_mask >> u) & 1u ? tv[u] : sub);
                     acc[u][v] = dadd(acc[u][v], dmul(tij, bv[v]));
                 }
         }
