@@ -189,6 +189,7 @@ struct LookaheadDev {
     PriceMsg* pm;     // K local (z, j) per candidate; world > 1: gathered into pm_all
     PriceMsg* pm_all; // world x K
     double* tl;       // K local theta'
+    double* own_t;    // K theta' ratio of each candidate's own pivot row (k_la_own)
     double* tl_all;   // world x K
     int nblk;         // pricing partials per candidate (64-slot tiles + 1 leaving column)
     int nblk_t;       // theta' partials per candidate (64-row tiles)

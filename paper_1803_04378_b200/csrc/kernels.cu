@@ -1248,6 +1248,25 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_price(Dev d, LookaheadDev la
 // The leaving variable of candidate k re-enters the nonbasic set
 // (solver.cpp:186-188): priced by the shard owning its column, into the last
 // partial slot (index nblk - 1).
+// One thread's sequential dot (ascending index) with 16 loads in flight ahead
+// of the chain: one-thread-per-output dots are otherwise load-latency bound.
+__device__ __forceinline__ double seq_dot(const double* __restrict__ x, const double* __restrict__ y, int n) {
+    double acc = 0.0;
+    int i = 0;
+    for (; i + 16 <= n; i += 16) {
+        double xv[16], yv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            xv[u] = __ldg(x + i + u);
+            yv[u] = __ldg(y + i + u);
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc = dadd(acc, dmul(xv[u], yv[u]));
+    }
+    for (; i < n; ++i) acc = dadd(acc, dmul(x[i], y[i]));
+    return acc;
+}
+
 __global__ void k_la_leave(Dev d, LookaheadDev la) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= la.K) return;
@@ -1256,15 +1275,29 @@ __global__ void k_la_leave(Dev d, LookaheadDev la) {
     const int p = d.basic[la.rows[k]];
     if (p < d.n_total && p != la.q && p >= d.col0 && p < d.col1) {
         const double* cost = phase_cost(d, d.ctl->phase);
-        const double* __restrict__ w = la.Wp + (size_t)k * la.ldx;
-        const double* __restrict__ a = d.A_cm + (size_t)p * d.ld_cm;
-        double acc = 0.0;
-        for (int i = 0; i < d.m; ++i) acc = dadd(acc, dmul(w[i], a[i]));
+        const double acc = seq_dot(la.Wp + (size_t)k * la.ldx, d.A_cm + (size_t)p * d.ld_cm, d.m);
         bz = dsub(acc, cost[p]);
         bj = p;
     }
     la.part_z[(size_t)k * la.nblk + la.nblk - 1] = bz;
     la.part_j[(size_t)k * la.nblk + la.nblk - 1] = bj;
+}
+
+// The candidate's own pivot row r_k becomes X_k (solver.cpp:176): its y' is
+// dot(X_k, a_{b_k}) and its b_bar' is X_k[m]. The tiled kernel skips that row;
+// this one computes its ratio (thread per candidate) into own_t[k].
+__global__ void k_la_own(Dev d, LookaheadDev la) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= la.K) return;
+    double th = kInf;
+    const int rk = la.rows[k];
+    const int bj = la.bj[k];
+    if (bj >= 0 && rk >= d.row0 && rk < d.row0 + d.mloc && !d.frozen[rk]) {
+        const double* __restrict__ X = la.X + (size_t)k * la.ldx;
+        const double acc = seq_dot(X, d.A_cm + (size_t)bj * d.ld_cm, d.m);
+        if (!(acc <= d.pivot_tol)) th = ddiv(X[d.m], acc);
+    }
+    la.own_t[k] = th;
 }
 
 // y'_ik = sum_j t_ij(k) a_{b_k}[j] for this shard's rows, t = X_kj on the
@@ -1307,17 +1340,14 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_theta(Dev d, LookaheadDev la
     for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-    // per-chain row kind, fixed for the whole reduction: the candidate's own row
-    // takes X, rows with y_i == 0 keep T, the others T - y_i X
-    unsigned own_mask = 0, zero_mask = 0;
+    // Chains use T_ij - y_i X_kj; rows with y_i == 0 keep T_ij exactly as the
+    // reference does (solver.cpp:177-184: T - 0*X would flip a -0 entry of a
+    // former pivot row). The row kind is fixed per thread row, so it costs one
+    // select per element. The candidate's own row (t = X_kj) is skipped here and
+    // handled by k_la_own.
+    bool zrow[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const int li = i0 + ti + 16 * u;
-        if (yv[u] == 0.0) zero_mask |= 1u << u;
-#pragma unroll
-        for (int v = 0; v < 4; ++v)
-            if (d.row0 + li == s_rk[tk + 16 * v]) own_mask |= 1u << (4 * u + v);
-    }
+    for (int u = 0; u < 4; ++u) zrow[u] = yv[u] == 0.0;
     double rt[4], rx[4], rb[4];
     auto fetch = [&](int j0) {
 #pragma unroll
@@ -1358,9 +1388,7 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_theta(Dev d, LookaheadDev la
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
                     const double sub = dsub(tv[u], dmul(yv[u], xv[v]));
-                    const double tij = (own_mask >> (4 * u + v)) & 1u ? xv[v]
-                                       : ((zero_mask >> u) & 1u ? tv[u] : sub);
-                    acc[u][v] = dadd(acc[u][v], dmul(tij, bv[v]));
+                    acc[u][v] = dadd(acc[u][v], dmul(zrow[u] ? tv[u] : sub, bv[v]));
                 }
         }
         __syncthreads();
@@ -1375,10 +1403,9 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_theta(Dev d, LookaheadDev la
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int li = i0 + ti + 16 * u;
-                if (!rowok[u] || d.frozen[d.row0 + li]) continue;
+                if (!rowok[u] || d.frozen[d.row0 + li] || d.row0 + li == s_rk[kk]) continue;
                 if (acc[u][v] <= d.pivot_tol) continue;
-                const bool own = d.row0 + li == s_rk[kk];
-                const double bb = own ? xm : (yv[u] == 0.0 ? bcol[li] : dsub(bcol[li], dmul(yv[u], xm)));
+                const double bb = zrow[u] ? bcol[li] : dsub(bcol[li], dmul(yv[u], xm));
                 th = min_keep(th, ddiv(bb, acc[u][v]));
             }
         }
@@ -1420,8 +1447,10 @@ __global__ void k_la_theta_local(Dev d, LookaheadDev la) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= la.K) return;
     double t = kInf;
-    if (la.bj[k] >= 0)
+    if (la.bj[k] >= 0) {
         for (int b = 0; b < la.nblk_t; ++b) t = min_keep(t, la.part_t[(size_t)k * la.nblk_t + b]);
+        t = min_keep(t, la.own_t[k]);
+    }
     la.tl[k] = t;
 }
 
@@ -1564,6 +1593,7 @@ void configure_kernels(Dev& d) {
                          (const void*)k_drive_scan, (const void*)k_drive_red, (const void*)k_la_x,
                          (const void*)k_la_wp, (const void*)k_la_price_local,
                          (const void*)k_la_gemm_price, (const void*)k_la_gemm_theta, (const void*)k_la_leave,
+                         (const void*)k_la_own,
                          (const void*)k_la_decide, (const void*)k_la_theta_local,
                          (const void*)k_la_score, (const void*)k_sum_i64, (const void*)k_min_i32};
     for (const void* f : all) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
@@ -1659,6 +1689,7 @@ void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int 
 
 void launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     k_la_gemm_theta<<<dim3(la.nblk_t, (la.K + kLT - 1) / kLT), 256, 0, st>>>(d, la);
+    k_la_own<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);
     k_la_theta_local<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);
 }
 

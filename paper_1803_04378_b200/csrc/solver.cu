@@ -297,6 +297,17 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
         throw Error(LPSG_INVALID_ARGUMENT, "lpsg_create: more shards than rows (or than 32)");
     CK(cudaSetDevice(cfg.device));
     CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    {
+        // stream-ordered temporaries (lookahead batches, exchanges) come from the
+        // device pool; keep freed blocks cached instead of returning them to the
+        // driver at every synchronisation
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, cfg.device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        cudaGetLastError();
+    }
     const int m = m_, n = n_total_;
 
     // ---- start basis (solver.cpp:27-39): first row i (ascending) with A[i][j] == 1.0
@@ -755,6 +766,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     la.pm = talloc<PriceMsg>((size_t)kb, st_);
     la.pm_all = sharded_ ? talloc<PriceMsg>((size_t)kb * G, st_) : nullptr;
     la.tl = talloc<double>(kb, st_);
+    la.own_t = talloc<double>(kb, st_);
     la.tl_all = sharded_ ? talloc<double>((size_t)kb * G, st_) : nullptr;
     CK(cudaMemsetAsync(la.X, 0, sizeof(double) * (size_t)kb * ldx, st_));
     for (int k0 = 0; k0 < K; k0 += kb) {
@@ -773,7 +785,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
         CK(cudaStreamSynchronize(st_));
     }
     void* bufs[] = {rows_d, la.X, la.Wp, la.bz, la.bj, la.theta, la.score, la.part_z, la.part_j, la.part_t,
-                    la.pm, la.pm_all, la.tl, la.tl_all};
+                    la.pm, la.pm_all, la.tl, la.tl_all, la.own_t};
     for (void* p : bufs)
         if (p) CK(cudaFreeAsync(p, st_));
 }
