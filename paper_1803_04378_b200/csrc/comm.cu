@@ -2,6 +2,8 @@
 #include "comm.h"
 
 #include <dlfcn.h>
+#include <execinfo.h>
+#include <signal.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -23,8 +25,20 @@ namespace {
 // other shard's kernels queued behind it (deadlock), so ask for the maximum
 // number of queues before the CUDA context exists (the caller's own setting
 // wins; the runtime reads it at context creation).
+void segv_trace(int sig) {
+    void* frames[64];
+    const int n = backtrace(frames, 64);
+    fprintf(stderr, "lpsg: signal %d, native backtrace:\n", sig);
+    backtrace_symbols_fd(frames, n, 2);
+    signal(sig, SIG_DFL);
+    raise(sig);
+}
+
 struct ConnectionsDefault {
-    ConnectionsDefault() { setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0); }
+    ConnectionsDefault() {
+        setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
+        if (getenv("LPSG_SEGV_TRACE")) signal(SIGSEGV, segv_trace);  // diagnostics
+    }
 } g_connections_default;
 
 void cuda_ok(cudaError_t e, const char* what) {
@@ -388,11 +402,15 @@ public:
     void host_barrier() override {
         if (h_->hub) h_->hub->barrier();
     }
-    void check() override {
+    // Shards sharing one GPU in one process keep to one batch in flight: their
+    // spin-waiting exchange kernels compete for the same SMs.
+    bool allows_pipelining() const override { return h_->hub == nullptr; }
+    void check(cudaStream_t st) override {
         unsigned long long e = 0;
-        cuda_ok(cudaMemcpy(&e, reinterpret_cast<unsigned long long*>(h_->base) + kErrorWord, 8,
-                           cudaMemcpyDeviceToHost),
-                "cudaMemcpy");
+        cuda_ok(cudaMemcpyAsync(&e, reinterpret_cast<unsigned long long*>(h_->base) + kErrorWord, 8,
+                                cudaMemcpyDeviceToHost, st),
+                "cudaMemcpyAsync");
+        cuda_ok(cudaStreamSynchronize(st), "cudaStreamSynchronize");
         if (e) throw CommError("p2p exchange timed out waiting for a peer (LPSG_P2P_TIMEOUT_S)");
     }
 

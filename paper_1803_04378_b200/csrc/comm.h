@@ -56,8 +56,13 @@ public:
     virtual const char* transport() const = 0;
     // Host-side barrier of shards that share a process (no-op across processes).
     virtual void host_barrier() {}
-    // Throws CommError when the transport recorded a failure (called after syncs).
-    virtual void check() {}
+    // Throws CommError when the transport recorded a failure (called after syncs;
+    // stream-ordered: a legacy-stream copy here can stall behind another shard's
+    // spin-waiting kernel on a shared GPU).
+    virtual void check(cudaStream_t st) { (void)st; }
+    // Whether the solver may keep a second pivot batch in flight while it
+    // drains the first (pipelined host loop).
+    virtual bool allows_pipelining() const { return true; }
 };
 
 struct LocalHub;

@@ -139,6 +139,7 @@ struct Dev {
     int dbg;               // experiment knobs (cfg.reserved[2]); 0 in production
     int pdl;               // launch the pivot chain with programmatic dependent launch
     int upd_tma_store;     // k_update writes tiles back with TMA stores (else per-warp STG)
+    int l2_hint;           // streaming TMA traffic carries an L2 evict-first hint
     size_t price_stage_bytes;
 };
 

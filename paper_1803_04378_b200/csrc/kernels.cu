@@ -245,6 +245,30 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         "l"(map), "r"(x), "r"(y), "r"(su32(b))
         : "memory");
 }
+// Streaming variants with an L2 eviction-priority hint: A_nb and T are read
+// (and T written) once per pivot and exceed L2, so their lines should not
+// displace anything worth keeping.
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int x, int y, uint64_t* b,
+                                                 uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], "
+        "[%1, {%2, %3}], [%4], %5;" ::"r"(su32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(su32(b)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, int x, int y, const void* src, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::"l"(map),
+        "r"(x), "r"(y), "r"(su32(src)), "l"(pol)
+        : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
 // TMA tile store (shared -> global) in a bulk async-group.
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
     asm volatile(
@@ -335,6 +359,7 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
         const CUtensorMap* map = d.tm_nb + (g.wbx / 8 - 1);
         if (warp == nwc) {
             if (lane == 0) {
+                const uint64_t pol = l2_evict_first();
                 int st = 0;
                 uint32_t ph = 0;
                 for (int k = 0; k < nst; ++k) {
@@ -347,7 +372,10 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
                     } else {
                         mbar_expect_tx(&full[st], (uint32_t)(R * w * 8 + R * 8));
                         for (int q = 0; q < g.nb; ++q)
-                            tma_load_2d(sb + (size_t)q * g.wbx * R * 8, map, s0 + q * g.wbx, i0, &full[st]);
+                            if (d.l2_hint)
+                                tma_load_2d_hint(sb + (size_t)q * g.wbx * R * 8, map, s0 + q * g.wbx, i0, &full[st], pol);
+                            else
+                                tma_load_2d(sb + (size_t)q * g.wbx * R * 8, map, s0 + q * g.wbx, i0, &full[st]);
                         bulk_g2s(ws, d.top + i0, (uint32_t)R * 8u, &full[st]);
                     }
                     if (++st == S) { st = 0; ph ^= 1; }
@@ -563,6 +591,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
     if (warp == U + F) {
         // ---- producer
         if (lane == 0) {
+            const uint64_t pol = l2_evict_first();
             int st = 0;
             uint32_t ph = 0;
             for (int k = 0; k < nst; ++k) {
@@ -576,7 +605,8 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                     mbar_arrive(&full[st]);
                 } else {
                     mbar_expect_tx(&full[st], (uint32_t)(tile_el * 8) + (up ? seg : 0u) + (ft ? seg : 0u));
-                    tma_load_2d(sb, d.tm_T, i0, j0, &full[st]);
+                    if (d.l2_hint) tma_load_2d_hint(sb, d.tm_T, i0, j0, &full[st], pol);
+                    else tma_load_2d(sb, d.tm_T, i0, j0, &full[st]);
                     if (up) bulk_g2s(xs, d.xrow + j0, seg, &full[st]);
                     if (ft) bulk_g2s(as, a + j0, seg, &full[st]);
                 }
@@ -589,7 +619,8 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
             uint32_t ph = 0;
             for (int k = 0; k < nst; ++k) {
                 mbar_wait(&upd[st], ph);
-                tma_store_2d(d.tm_T, i0, k * C, smem + (size_t)st * stage_stride);
+                if (d.l2_hint) tma_store_2d_hint(d.tm_T, i0, k * C, smem + (size_t)st * stage_stride, l2_evict_first());
+                else tma_store_2d(d.tm_T, i0, k * C, smem + (size_t)st * stage_stride);
                 bulk_wait_read_all();
                 mbar_arrive(&empty[st]);
                 if (++st == S) { st = 0; ph ^= 1; }
@@ -1059,8 +1090,8 @@ __global__ void __launch_bounds__(256) k_pivot(Dev d) {
         c->n_scan = ns;
         d.basic[r] = q;
         c->total_iter += 1;
-        const int li = c->log_len;
-        if (li < d.log_cap) {
+        const int li = c->log_len;  // monotonic; the log is a ring the host drains
+        {
             LogEntry e;
             e.iteration = c->total_iter;
             e.phase = c->phase;
@@ -1068,7 +1099,7 @@ __global__ void __launch_bounds__(256) k_pivot(Dev d) {
             e.leaving = p_leave;
             e.entering = q;
             e.objective = ((volatile double*)d.top)[m];
-            d.log[li] = e;
+            d.log[li % d.log_cap] = e;
         }
         c->log_len = li + 1;
         c->pending = 1;

@@ -64,9 +64,9 @@ T* dalloc(size_t n) {
 // device, which would deadlock against another shard's spin-waiting exchange
 // kernel when shards share a GPU.
 template <class T>
-T* talloc(size_t n, cudaStream_t st) {
+T* talloc(size_t n, cudaStream_t st, cudaMemPool_t pool) {
     void* p = nullptr;
-    CK(cudaMallocAsync(&p, std::max<size_t>(n, 1) * sizeof(T), st));
+    CK(cudaMallocFromPoolAsync(&p, std::max<size_t>(n, 1) * sizeof(T), pool, st));
     return static_cast<T*>(p);
 }
 
@@ -116,6 +116,7 @@ private:
     void pull(bool with_log);
     void push();
     void drain_log();
+    void snapshot();
     void note_pivot(const LogEntry& e);
     void enqueue_pivots(int n);
     void seq_pivot();
@@ -125,6 +126,7 @@ private:
     std::vector<int> gather_overflow_candidates();
     void single_gpu_only(const char* what) const;
     int owner_of_row(int i) const;
+    void temp_alloc_fence();
     double objective_value();
 
     lpsg_config cfg_;
@@ -144,7 +146,10 @@ private:
     cudaStream_t st_ = nullptr;
     Dev d_{};
     Ctl* hctl_ = nullptr;       // pinned mirror of the control block
-    LogEntry* hlog_ = nullptr;  // pinned mirror of the pivot log
+    LogEntry* hlog_ = nullptr;  // pinned mirror of the pivot log (a ring of log_cap entries)
+    long long log_seen_ = 0;    // log entries already drained
+    cudaEvent_t ev_snap_ = nullptr;
+    cudaMemPool_t pool_ = nullptr;  // stream-ordered temporaries
     int* hone_ = nullptr;       // pinned constant 1 (stream-ordered flag writes)
     double* scratch_ = nullptr;
     double* cost_buf_ = nullptr;
@@ -298,15 +303,18 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     CK(cudaSetDevice(cfg.device));
     CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
     {
-        // stream-ordered temporaries (lookahead batches, exchanges) come from the
-        // device pool; keep freed blocks cached instead of returning them to the
-        // driver at every synchronisation
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, cfg.device) == cudaSuccess) {
-            uint64_t keep = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-        cudaGetLastError();
+        // Stream-ordered temporaries (lookahead batches, overflow gathers) come
+        // from this solver's own pool, which keeps freed blocks cached. Its own
+        // pool, not the device default: shards of one process must not reuse each
+        // other's freed blocks, which would order one shard's stream behind
+        // another's (a deadlock against spin-waiting exchange kernels).
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = cfg.device;
+        CK(cudaMemPoolCreate(&pool_, &props));
+        uint64_t keep = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &keep));
     }
     const int m = m_, n = n_total_;
 
@@ -377,12 +385,13 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     d_.dbg = cfg_.reserved[2];
     d_.pdl = (!comm && getenv("LPSG_NO_PDL") == nullptr) ? 1 : 0;
     d_.upd_tma_store = getenv("LPSG_UPD_STG") == nullptr ? 1 : 0;
+    d_.l2_hint = getenv("LPSG_NO_L2_HINT") == nullptr ? 1 : 0;
     configure_kernels(d_);
     CK(cudaGetLastError());
     d_.ldT = round_up(std::max<long long>(d_.mloc + 1, (long long)d_.update_grid * d_.upd_h), 32);
     unfused_ratio_ = !sharded_ && (cfg_.reserved[0] & 1) != 0;
     batch_ = cfg_.batch > 0 ? cfg_.batch : (m <= 1024 ? 64 : m <= 4096 ? 16 : 4);
-    d_.log_cap = batch_ + 8;
+    d_.log_cap = 2 * batch_ + 8;  // ring: the drained batch + the one in flight
 
     d_.T = dalloc<double>((size_t)(m + 1) * d_.ldT + 64);
     d_.top = dalloc<double>(m + 520);  // + padding: TMA-side W segments may run past m+2
@@ -421,6 +430,7 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     CK(cudaMallocHost(&hctl_, sizeof(Ctl)));
     CK(cudaMallocHost(&hlog_, sizeof(LogEntry) * d_.log_cap));
     CK(cudaMallocHost(&hone_, sizeof(int)));
+    CK(cudaEventCreateWithFlags(&ev_snap_, cudaEventDisableTiming));
     *hone_ = 1;
 
     // ---- upload A once (row-major), derive the column-major copy and the
@@ -504,6 +514,8 @@ Solver::~Solver() {
     if (hctl_) cudaFreeHost(hctl_);
     if (hlog_) cudaFreeHost(hlog_);
     if (hone_) cudaFreeHost(hone_);
+    if (ev_snap_) cudaEventDestroy(ev_snap_);
+    if (pool_) cudaMemPoolDestroy(pool_);
     if (st_) cudaStreamDestroy(st_);
 }
 
@@ -523,7 +535,7 @@ void Solver::pull(bool with_log) {
     }
     CK(cudaStreamSynchronize(st_));
     CK(cudaGetLastError());
-    if (comm_) comm_->check();
+    if (comm_) comm_->check(st_);
 }
 
 double Solver::objective_value() {
@@ -548,6 +560,16 @@ void Solver::rebuild_top_row() {
     }
     CK(cudaMemcpyAsync(d_.top, chain_, sizeof(double) * (m_ + 1), cudaMemcpyDeviceToDevice, st_));
     CK(cudaMemsetAsync(d_.top + m_ + 1, 0, sizeof(double), st_));
+}
+
+// Shards sharing a GPU: growing a memory pool may wait for the whole device,
+// including another shard's spin-waiting exchange kernel, which in turn waits
+// for this shard. Before stream-ordered allocations on a sharded path, every
+// shard drains its stream and meets the others (a no-op across processes).
+void Solver::temp_alloc_fence() {
+    if (!comm_) return;
+    CK(cudaStreamSynchronize(st_));
+    comm_->host_barrier();
 }
 
 int Solver::owner_of_row(int i) const {
@@ -578,11 +600,23 @@ void Solver::note_pivot(const LogEntry& e) {
     if (observer) observer(&t, observer_user);
 }
 
+// The device appends to a ring (log_len is monotonic); entries
+// [log_seen_, log_len) are new since the last drain.
 void Solver::drain_log() {
-    const int n = hctl_->log_len;
+    const long long n = (long long)hctl_->log_len - log_seen_;
     if (n > d_.log_cap) throw Error(LPSG_CUDA_ERROR, "pivot log overflow");
-    for (int k = 0; k < n; ++k) note_pivot(hlog_[k]);
-    hctl_->log_len = 0;
+    for (long long k = 0; k < n; ++k) note_pivot(hlog_[(log_seen_ + k) % d_.log_cap]);
+    log_seen_ = hctl_->log_len;
+}
+
+// Asynchronous snapshot of the control block and the log ring, ordered after
+// everything enqueued so far; ev_snap_ completes when it has landed.
+void Solver::snapshot() {
+    ev_chain_ = nullptr;
+    CK(cudaMemcpyAsync(hctl_, d_.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st_));
+    CK(cudaMemcpyAsync(hlog_, d_.log, sizeof(LogEntry) * d_.log_cap, cudaMemcpyDeviceToHost, st_));
+    d2h_bytes += sizeof(Ctl) + sizeof(LogEntry) * d_.log_cap;
+    CK(cudaEventRecord(ev_snap_, st_));
 }
 
 // One pivot's device work in the fused schedule; world > 1 adds the three
@@ -639,11 +673,13 @@ void Solver::resume_with_row(int r) {
 std::vector<int> Solver::gather_overflow_candidates() {
     const int G = world_;
     std::vector<RatioMsg> msgs(G);
-    CK(cudaMemcpy(msgs.data(), d_.rmsg + 1, sizeof(RatioMsg) * G, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpyAsync(msgs.data(), d_.rmsg + 1, sizeof(RatioMsg) * G, cudaMemcpyDeviceToHost, st_));
+    CK(cudaStreamSynchronize(st_));
     int maxn = 1;
     for (auto& mm : msgs) maxn = std::max(maxn, mm.any ? mm.n : 0);
-    int* rows_d = talloc<int>((size_t)G * maxn, st_);
-    double* rat_d = talloc<double>((size_t)G * maxn, st_);
+    temp_alloc_fence();
+    int* rows_d = talloc<int>((size_t)G * maxn, st_, pool_);
+    double* rat_d = talloc<double>((size_t)G * maxn, st_, pool_);
     comm_->allgather(d_.cand, rows_d, sizeof(int) * maxn, st_);
     comm_->allgather(d_.cand_ratio, rat_d, sizeof(double) * maxn, st_);
     std::vector<int> rows((size_t)G * maxn);
@@ -670,15 +706,32 @@ int Solver::run_phase() {
     hctl_->pending = 0;
     hctl_->no_ftran = 0;
     hctl_->no_ratio = unfused_ratio_ ? 1 : 0;
-    hctl_->log_len = 0;
     hctl_->phase = phase_;
     push();
     seq_price();   // price(W_t), first pivot of the phase
     seq_update();  // standalone FTRAN (pending == 0) + ratio test
     CK(cudaGetLastError());
+    // Pipelined batches: batch k+1 is enqueued before the host waits for batch
+    // k's snapshot, so the GPU never idles on the host round trip. Kernels of
+    // an in-flight batch no-op once the device status leaves RUNNING, so a
+    // stop (optimal, tie, budget) seen in snapshot k leaves the state exactly as
+    // batch k ended. Profiling windows stay synchronous (their events must be
+    // complete when read).
+    const bool pipelined = !prof_ && getenv("LPSG_NO_PIPELINE") == nullptr && (!comm_ || comm_->allows_pipelining());
+    bool enqueued = false;
     for (;;) {
-        enqueue_pivots(batch_);
-        pull(true);
+        if (!enqueued) enqueue_pivots(batch_);
+        enqueued = false;
+        if (pipelined) {
+            snapshot();
+            enqueue_pivots(batch_);
+            enqueued = true;
+            CK(cudaEventSynchronize(ev_snap_));
+            CK(cudaGetLastError());
+            if (comm_) comm_->check(st_);
+        } else {
+            pull(true);
+        }
         if (prof_) flush_profile();
         if (dbg_trace_)
             fprintf(stderr, "[solver r%d] status %d log %d q %d r %d ncand %d iter %lld\n", rank_, hctl_->status,
@@ -686,12 +739,14 @@ int Solver::run_phase() {
         drain_log();
         const int st = hctl_->status;
         if (st == ST_RUNNING) {
-            push();
+            if (!pipelined) push();
             continue;
         }
+        enqueued = false;  // an in-flight batch (if any) no-ops: the device stopped
         if (st == ST_TIE) {
             std::vector<int> cand(hctl_->ncand);
-            CK(cudaMemcpy(cand.data(), d_.cand, sizeof(int) * cand.size(), cudaMemcpyDeviceToHost));
+            CK(cudaMemcpyAsync(cand.data(), d_.cand, sizeof(int) * cand.size(), cudaMemcpyDeviceToHost, st_));
+            CK(cudaStreamSynchronize(st_));
             resume_with_row(select_leaving(cand, hctl_->q));
             continue;
         }
@@ -752,23 +807,25 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     la.q = entering;
     la.nblk = (hctl_->n_scan + 63) / 64 + 1;  // 64-slot tiles + the leaving column
     la.nblk_t = std::max(1, (d_.mloc + 63) / 64);
-    int* rows_d = talloc<int>(kb, st_);
+    int* rows_d = talloc<int>(kb, st_, pool_);
     la.rows = rows_d;
-    la.X = talloc<double>((size_t)kb * ldx, st_);
-    la.Wp = talloc<double>((size_t)kb * ldx, st_);
-    la.bz = talloc<double>(kb, st_);
-    la.bj = talloc<int>(kb, st_);
-    la.theta = talloc<double>(kb, st_);
-    la.score = talloc<double>(kb, st_);
-    la.part_z = talloc<double>((size_t)kb * la.nblk, st_);
-    la.part_j = talloc<int>((size_t)kb * la.nblk, st_);
-    la.part_t = talloc<double>((size_t)kb * la.nblk_t, st_);
-    la.pm = talloc<PriceMsg>((size_t)kb, st_);
-    la.pm_all = sharded_ ? talloc<PriceMsg>((size_t)kb * G, st_) : nullptr;
-    la.tl = talloc<double>(kb, st_);
-    la.own_t = talloc<double>(kb, st_);
-    la.tl_all = sharded_ ? talloc<double>((size_t)kb * G, st_) : nullptr;
+    la.X = talloc<double>((size_t)kb * ldx, st_, pool_);
+    la.Wp = talloc<double>((size_t)kb * ldx, st_, pool_);
+    la.bz = talloc<double>(kb, st_, pool_);
+    la.bj = talloc<int>(kb, st_, pool_);
+    la.theta = talloc<double>(kb, st_, pool_);
+    la.score = talloc<double>(kb, st_, pool_);
+    la.part_z = talloc<double>((size_t)kb * la.nblk, st_, pool_);
+    la.part_j = talloc<int>((size_t)kb * la.nblk, st_, pool_);
+    la.part_t = talloc<double>((size_t)kb * la.nblk_t, st_, pool_);
+    la.pm = talloc<PriceMsg>((size_t)kb, st_, pool_);
+    la.pm_all = sharded_ ? talloc<PriceMsg>((size_t)kb * G, st_, pool_) : nullptr;
+    la.tl = talloc<double>(kb, st_, pool_);
+    la.own_t = talloc<double>(kb, st_, pool_);
+    la.tl_all = sharded_ ? talloc<double>((size_t)kb * G, st_, pool_) : nullptr;
     CK(cudaMemsetAsync(la.X, 0, sizeof(double) * (size_t)kb * ldx, st_));
+    if (dbg_trace_) fprintf(stderr, "[solver r%d] lookahead K=%d\n", rank_, K);
+    temp_alloc_fence();
     for (int k0 = 0; k0 < K; k0 += kb) {
         la.K = std::min(kb, K - k0);
         CK(cudaMemcpyAsync(rows_d, rows.data() + k0, sizeof(int) * la.K, cudaMemcpyHostToDevice, st_));
@@ -809,7 +866,8 @@ void Solver::drive_out_artificials() {
         if (found < 0) {
             frozen_[i] = 1;
             const unsigned char one = 1;
-            CK(cudaMemcpy(d_.frozen + i, &one, 1, cudaMemcpyHostToDevice));
+            CK(cudaMemcpyAsync(d_.frozen + i, &one, 1, cudaMemcpyHostToDevice, st_));
+            CK(cudaStreamSynchronize(st_));
             continue;
         }
         // compute_direction(found, red) then pivot_update(i, found), unfused
@@ -820,7 +878,6 @@ void Solver::drive_out_artificials() {
         hctl_->pending = 0;
         hctl_->no_ftran = 0;
         hctl_->no_ratio = 1;
-        hctl_->log_len = 0;
         push();
         seq_update();  // FTRAN only
         seq_pivot();
@@ -918,7 +975,8 @@ void Solver::get_x(double* x, int n) {
     } else {
         // every shard's b_bar rows, padded to the largest shard, in rank order
         const int pad = m_ / world_ + 1;
-        double* tmp = talloc<double>((size_t)pad * (world_ + 1), st_);
+        temp_alloc_fence();
+        double* tmp = talloc<double>((size_t)pad * (world_ + 1), st_, pool_);
         CK(cudaMemcpyAsync(tmp, bcol, sizeof(double) * d_.mloc, cudaMemcpyDeviceToDevice, st_));
         comm_->allgather(tmp, tmp + pad, sizeof(double) * pad, st_);
         std::vector<double> all((size_t)pad * world_);
@@ -985,7 +1043,8 @@ void Solver::step_ratio(int* unbounded, double* theta, std::vector<int>& cand) {
     if (!*unbounded) {
         *theta = hctl_->theta;
         cand.resize(hctl_->ncand);
-        CK(cudaMemcpy(cand.data(), d_.cand, sizeof(int) * cand.size(), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpyAsync(cand.data(), d_.cand, sizeof(int) * cand.size(), cudaMemcpyDeviceToHost, st_));
+        CK(cudaStreamSynchronize(st_));
     }
     hctl_->status = ST_HOLD;
     push();
@@ -999,7 +1058,6 @@ void Solver::step_pivot(int r, int q) {
     hctl_->status = ST_RUNNING;
     hctl_->pending = 0;
     hctl_->no_ftran = 1;
-    hctl_->log_len = 0;
     push();
     launch_pivot(d_, st_);
     launch_update(d_, st_);
@@ -1012,8 +1070,11 @@ void Solver::step_pivot(int r, int q) {
         throw Error(LPSG_PIVOT_TOO_SMALL, "pivot element in row " + std::to_string(r) + " below pivot_tol");
     }
     // pivot_update itself does not count an iteration (run_phase does)
-    if (hctl_->log_len > 0) basic_[hlog_[0].row] = hlog_[0].entering;
-    hctl_->log_len = 0;
+    if (hctl_->log_len > log_seen_) {
+        const LogEntry& e = hlog_[(hctl_->log_len - 1) % d_.log_cap];
+        basic_[e.row] = e.entering;
+    }
+    log_seen_ = hctl_->log_len;
     hctl_->total_iter -= 1;
     hctl_->status = ST_HOLD;
     hctl_->no_ftran = 0;

@@ -28,6 +28,7 @@ CASES = {
     "c3_p200": (8000, 16000, 0, 1, {"max_iter": 200, "workers": 4}),
     "c4_p3": (4000, 8000, 2, 1, {"max_iter": 3, "workers": 1}),
     "c5_p10": (24000, 48000, 0, 1, {"max_iter": 10, "workers": 8}),
+    "c4_p20": (4000, 8000, 2, 1, {"max_iter": 20, "workers": 1}),
 }
 
 
