@@ -277,8 +277,9 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int 
         : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void bulk_wait_read_all() {
-    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
@@ -325,7 +326,6 @@ __device__ __forceinline__ void chain_group(double& acc0, double& acc1, const do
 __global__ void __launch_bounds__(384) k_price(Dev d) {
     extern __shared__ __align__(1024) unsigned char smem[];
     pdl_wait();
-    pdl_trigger();
     Ctl* c = d.ctl;
     if (c->status != ST_RUNNING) return;
     const bool budget_hit = c->total_iter >= c->budget;
@@ -438,6 +438,9 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
             }
         }
     }
+    // the next kernel's CTAs may launch now, during this kernel's tail only: early
+    // resident-but-waiting CTAs would crowd this kernel's latency-bound warps
+    pdl_trigger();
     block_argmax(bz, bj);
     if (threadIdx.x == 0) { d.pz[blockIdx.x] = bz; d.pj[blockIdx.x] = bj; }
     if (!last_block(&c->ticket_price)) return;
@@ -557,7 +560,6 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
 __global__ void __launch_bounds__(512) k_update(Dev d) {
     extern __shared__ __align__(1024) unsigned char smem[];
     pdl_wait();
-    pdl_trigger();
     Ctl* c = d.ctl;
     const int status = c->status;
     const bool up = c->pending != 0;
@@ -617,13 +619,26 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
             // the stage is released once the store has read shared memory
             int st = 0;
             uint32_t ph = 0;
+            // up to kStoreLag stores stay in flight; a stage is released once its
+            // store has read shared memory (wait_group.read), kStoreLag behind
+            constexpr int kStoreLag = 2;
+            const uint64_t spol = l2_evict_first();
+            int rel = 0;  // next stage index to release
             for (int k = 0; k < nst; ++k) {
                 mbar_wait(&upd[st], ph);
-                if (d.l2_hint) tma_store_2d_hint(d.tm_T, i0, k * C, smem + (size_t)st * stage_stride, l2_evict_first());
+                if (d.l2_hint) tma_store_2d_hint(d.tm_T, i0, k * C, smem + (size_t)st * stage_stride, spol);
                 else tma_store_2d(d.tm_T, i0, k * C, smem + (size_t)st * stage_stride);
-                bulk_wait_read_all();
-                mbar_arrive(&empty[st]);
                 if (++st == S) { st = 0; ph ^= 1; }
+                if (k >= kStoreLag) {
+                    bulk_wait_read<kStoreLag>();
+                    mbar_arrive(&empty[rel]);
+                    if (++rel == S) rel = 0;
+                }
+            }
+            bulk_wait_read<0>();
+            for (int k = nst > kStoreLag ? nst - kStoreLag : 0; k < nst; ++k) {
+                mbar_arrive(&empty[rel]);
+                if (++rel == S) rel = 0;
             }
             bulk_wait_all();
         }
@@ -692,6 +707,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
             }
         }
     }
+    pdl_trigger();  // tail only (see k_price)
     // ---- fused ratio test, CTA-local part (solver.cpp:138-162): theta_b over this
     // CTA's eligible rows and the rows within window(theta_b), in row order.
     // The global theta <= theta_b and window() is monotone, so the union of the
@@ -1587,7 +1603,8 @@ void configure_kernels(Dev& d) {
     const size_t stage = ((tile_el + 2 * (size_t)d.upd_C) * 8 + 1023) / 1024 * 1024;
     size_t s_cap = 8;
     if (const char* e = getenv("LPSG_UPD_STAGES")) s_cap = (size_t)std::max(2, atoi(e));  // tuning experiments
-    d.upd_S = (int)std::max<size_t>(2, std::min<size_t>(s_cap, (size_t)(200 * 1024) / stage));
+    // >= 3 stages: the storer keeps 2 TMA stores in flight behind the update warps
+    d.upd_S = (int)std::max<size_t>(3, std::min<size_t>(s_cap, (size_t)(200 * 1024) / stage));
     d.upd_smem = (int)(d.upd_S * stage + 3 * d.upd_S * 8);
     d.upd_threads = (d.upd_U + (h + 31) / 32 + 1) * 32;
     // pricing: one CTA per SM over contiguous slot ranges of this shard's columns

@@ -383,7 +383,10 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     d_.ratio_tie_tol = cfg_.ratio_tie_tol;
     d_.anticycle = cfg_.anticycle;
     d_.dbg = cfg_.reserved[2];
-    d_.pdl = (!comm && getenv("LPSG_NO_PDL") == nullptr) ? 1 : 0;
+    // PDL hides kernel-boundary latency; it pays up to m ~ 10^4 (C1 +21 %, C3
+    // +1.4 %) and was measured to cost ~17 % at m = 24000, where the boundaries
+    // are noise against 3 ms pivots
+    d_.pdl = (!comm && m <= 12000 && getenv("LPSG_NO_PDL") == nullptr) ? 1 : 0;
     d_.upd_tma_store = getenv("LPSG_UPD_STG") == nullptr ? 1 : 0;
     d_.l2_hint = getenv("LPSG_NO_L2_HINT") == nullptr ? 1 : 0;
     configure_kernels(d_);
