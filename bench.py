@@ -340,8 +340,9 @@ def run_ours(args, cfg):
                     "collectives_per_pivot": round(calls, 2),
                     "payload_bytes_per_pivot_per_rank": round(nbytes, 1),
                     "us_per_pivot": round(1e3 * ex["ms_total"] / max(1, done_p), 2) if ex else None,
-                    "note": "per pivot: pivot-row broadcast from its owner (m+3 words), (z, j) "
-                            "all-gather, ratio-message all-gather"}
+                    "note": "per pivot: pivot-row broadcast from its owner (m+3 words), the (z, j) "
+                            "and ratio-message exchanges (P2P: stored into the peers' mailboxes by the "
+                            "producing kernels' last CTA, no collective launch; NCCL: all-gathers)"}
 
     # ---- end to end through the public API with host buffers: lpsg_create
     # uploads A from pinned host memory, solve() runs to optimality (or the

@@ -15,6 +15,7 @@
 #include <stdexcept>
 
 #include "device.cuh"
+#include "peer.cuh"
 
 namespace lpsg {
 
@@ -221,30 +222,9 @@ private:
 //   [0, 4 KB)                 flags: u64 per source rank (last sequence it raised here)
 //   [4 KB, 4 KB + 2 MB_)      two mailboxes (by sequence parity)
 //   [4 KB + 2 MB_, bytes)     symmetric allocations (owner_bcast targets)
-constexpr size_t kFlagBytes = 4096;
-constexpr int kErrorWord = 480;  // u64 index inside the flag page: set on a wait timeout
-constexpr size_t kMailbox = (size_t)8 << 20;
 constexpr int kSmallThreads = 512;
 
 enum PeerOp : int { OP_GATHER = 0, OP_SUM_I64 = 1, OP_MIN_I32 = 2, OP_BCAST = 3, OP_OWNER = 4 };
-
-struct PeerArgs {
-    char* const* peers;  // device array: every rank's heap base
-    int rank, size;
-    unsigned long long seq;
-    size_t mbox;         // mailbox offset for this sequence's parity
-    int watchdog;        // debug: report timeouts
-    unsigned long long timeout_ns;
-};
-
-__device__ __forceinline__ void st_flag(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_flag(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 
 // copy `bytes` from src to dst with the threads [t0, t0 + nt) (16-byte lanes when aligned)
 __device__ __forceinline__ void peer_copy(char* dst, const char* src, size_t bytes, size_t t0, size_t nt) {
@@ -275,42 +255,6 @@ __device__ void peer_put(const PeerArgs& a, int op, const char* send, size_t byt
                 break;
         }
     }
-}
-
-__device__ void peer_signal(const PeerArgs& a) {
-    __threadfence_system();
-    if (threadIdx.x < (unsigned)a.size)
-        st_flag(reinterpret_cast<unsigned long long*>(a.peers[threadIdx.x]) + a.rank, a.seq);
-}
-
-__device__ __forceinline__ unsigned long long globaltimer_ns() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-
-// Spin until every source raised this sequence. A peer that never arrives
-// (crashed rank, mismatched call sequence) ends the wait after timeout_ns with
-// the error word set, so the host fails the solve instead of hanging the GPU.
-__device__ void peer_wait(const PeerArgs& a) {
-    if (threadIdx.x < (unsigned)a.size) {
-        unsigned long long* heap = reinterpret_cast<unsigned long long*>(a.peers[a.rank]);
-        const unsigned long long* f = heap + threadIdx.x;
-        const unsigned long long t0 = globaltimer_ns();
-        unsigned long long v;
-        unsigned spins = 0;
-        while ((v = ld_flag(f)) < a.seq) {
-            if ((++spins & 1023u) == 0 && globaltimer_ns() - t0 > a.timeout_ns) {
-                if (a.watchdog)
-                    printf("[p2p] rank %d timed out at seq %llu: flag[%d] = %llu\n", a.rank, a.seq,
-                           (int)threadIdx.x, v);
-                atomicExch(heap + kErrorWord, 1ull);
-                break;
-            }
-        }
-    }
-    __syncthreads();
-    __threadfence_system();
 }
 
 // Phase 3 (post): mailbox -> caller's buffer.
@@ -405,6 +349,12 @@ public:
     // Shards sharing one GPU in one process keep to one batch in flight: their
     // spin-waiting exchange kernels compete for the same SMs.
     bool allows_pipelining() const override { return h_->hub == nullptr; }
+    bool fused_slot(PeerArgs* out) override {
+        const unsigned long long seq = ++h_->seq;
+        *out = PeerArgs{peers_dev_, rank, size, seq, kFlagBytes + (seq & 1) * kMailbox, trace_ ? 1 : 0, timeout_ns_};
+        ++calls;
+        return true;
+    }
     void check(cudaStream_t st) override {
         unsigned long long e = 0;
         cuda_ok(cudaMemcpyAsync(&e, reinterpret_cast<unsigned long long*>(h_->base) + kErrorWord, 8,

@@ -23,6 +23,8 @@
 #include <string>
 #include <vector>
 
+#include "peer.cuh"
+
 namespace lpsg {
 
 struct CommError : std::runtime_error {
@@ -60,6 +62,13 @@ public:
     // stream-ordered: a legacy-stream copy here can stall behind another shard's
     // spin-waiting kernel on a shared GPU).
     virtual void check(cudaStream_t st) { (void)st; }
+    // Device-initiated transports: reserve the next exchange for a kernel that
+    // stores its payload straight into the peers' mailboxes (returns false if
+    // the transport cannot). Every rank must reserve in the same order.
+    virtual bool fused_slot(PeerArgs* out) {
+        (void)out;
+        return false;
+    }
     // Whether the solver may keep a second pivot batch in flight while it
     // drains the first (pipelined host loop).
     virtual bool allows_pipelining() const { return true; }

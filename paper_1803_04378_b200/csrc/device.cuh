@@ -20,6 +20,8 @@
 
 #include <cstdint>
 
+#include "peer.cuh"
+
 namespace lpsg {
 
 enum CtlStatus : int {
@@ -49,6 +51,8 @@ struct RatioMsg {
     int rows[kRatioMsgCap];
     double ratios[kRatioMsgCap];
 };
+static_assert(sizeof(RatioMsg) % 8 == 0, "RatioMsg is moved as 8-byte words");
+static_assert(sizeof(PriceMsg) == 16, "PriceMsg is moved as one 16-byte word");
 
 struct LogEntry {
     long long iteration;
@@ -97,6 +101,11 @@ struct Dev {
     int xbuf_zero;         // transport sums int64 bit patterns: non-owners zero-fill xbuf
     PriceMsg* pmsg;        // world > 1: [0] local result, [1..world] gathered
     RatioMsg* rmsg;        // world > 1: [0] local result, [1..world] gathered
+    // P2P transport, fused exchanges: the producing kernel's last CTA stores its
+    // message into every peer's mailbox and raises the flags; the consumer
+    // (k_price_final / k_ratio_final) waits and reads its own mailbox.
+    int fused;
+    PeerArgs px_price, px_ratio;
     double* cand_ratio;    // ratios of the candidates in cand (same order)
     long long ldT;
     long long ld_nb;

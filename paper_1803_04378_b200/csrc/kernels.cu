@@ -458,6 +458,16 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
             if (!budget_hit) c->work[0] += 1;  // a real pricing pass (profile byte accounting)
             if (d.sharded) {
                 d.pmsg[0] = PriceMsg{z, j, 0};  // merged across shards by k_price_final
+                if (d.fused) {
+                    // P2P: straight into every peer's mailbox slot [rank], then the flags
+                    const PeerArgs& a = d.px_price;
+                    for (int g = 0; g < a.size; ++g)
+                        *reinterpret_cast<PriceMsg*>(a.peers[g] + a.mbox + (size_t)a.rank * sizeof(PriceMsg)) =
+                            PriceMsg{z, j, 0};
+                    __threadfence_system();
+                    for (int g = 0; g < a.size; ++g)
+                        st_flag(reinterpret_cast<unsigned long long*>(a.peers[g]) + a.rank, a.seq);
+                }
             } else {
                 price_decide(d, c, budget_hit, z, j);
             }
@@ -470,10 +480,19 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
 __global__ void k_price_final(Dev d) {
     Ctl* c = d.ctl;
     if (c->status != ST_RUNNING) return;
+    if (d.fused) peer_wait(d.px_price);
     double z = -kInf;
     int j = INT_MAX;
     for (int g = threadIdx.x; g < d.world; g += 32) {
-        const PriceMsg mm = d.pmsg[1 + g];
+        PriceMsg mm;
+        if (d.fused) {
+            const PeerArgs& a = d.px_price;
+            const double2 v = __ldcg(reinterpret_cast<const double2*>(a.peers[a.rank] + a.mbox + (size_t)g * sizeof(PriceMsg)));
+            mm.z = v.x;
+            mm.j = (int)__double_as_longlong(v.y);
+        } else {
+            mm = d.pmsg[1 + g];
+        }
         if (better(mm.z, mm.j, z, j)) { z = mm.z; j = mm.j; }
     }
     warp_argmax(z, j);
@@ -544,6 +563,23 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
         if (lane == 0) mbar_arrive(&upd[st]);
         if (++st == S) { st = 0; ph ^= 1; }
     }
+}
+
+// P2P, fused: the last CTA of k_update copies this shard's RatioMsg (just
+// written to d.rmsg by its threads) into every peer's mailbox slot [rank] and
+// raises the flags. All threads of the CTA call it.
+__device__ __noinline__ void ratio_put(const Dev& d) {
+    __syncthreads();
+    const PeerArgs& a = d.px_ratio;
+    constexpr int kWords = sizeof(RatioMsg) / 8;
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(d.rmsg);
+    for (int g = 0; g < a.size; ++g) {
+        unsigned long long* dst =
+            reinterpret_cast<unsigned long long*>(a.peers[g] + a.mbox + (size_t)a.rank * sizeof(RatioMsg));
+        for (int w = threadIdx.x; w < kWords; w += blockDim.x) dst[w] = ((volatile const unsigned long long*)src)[w];
+    }
+    __syncthreads();
+    peer_signal(a);
 }
 
 // --------------------------------------------------------- update+FTRAN ---
@@ -774,6 +810,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                 c->status = ST_UNBOUNDED;
             }
         }
+        if (d.sharded && d.fused) ratio_put(d);
         return;
     }
     const double gth = s_th2;
@@ -847,6 +884,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                 mm->n = total;
             }
         }
+        if (d.fused) ratio_put(d);
         return;
     }
     if (threadIdx.x == 0) {
@@ -868,10 +906,22 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
 __global__ void k_ratio_final(Dev d) {
     Ctl* c = d.ctl;
     if (c->status != ST_RUNNING || c->no_ratio || c->no_ftran || c->q < 0) return;
+    if (d.fused) peer_wait(d.px_ratio);
     const int g = threadIdx.x;  // one lane per shard (world <= 32)
     const bool have = g < d.world;
     RatioMsg mm;
-    if (have) mm = d.rmsg[1 + g];
+    if (have) {
+        if (d.fused) {
+            const PeerArgs& a = d.px_ratio;
+            const unsigned long long* src =
+                reinterpret_cast<const unsigned long long*>(a.peers[a.rank] + a.mbox + (size_t)g * sizeof(RatioMsg));
+            unsigned long long* dst = reinterpret_cast<unsigned long long*>(&mm);
+            for (int w = 0; w < (int)(sizeof(RatioMsg) / 8); ++w) dst[w] = __ldcg(src + w);
+            d.rmsg[1 + g] = mm;  // the host's overflow path reads the gathered messages here
+        } else {
+            mm = d.rmsg[1 + g];
+        }
+    }
     const bool any_g = have && mm.any;
     double th = any_g ? mm.theta : kInf;
     for (int o = 16; o > 0; o >>= 1) th = min_keep(th, __shfl_xor_sync(0xffffffffu, th, o));

@@ -635,20 +635,29 @@ void Solver::seq_pivot() {
     L(K_PIVOT, 0.0, [&] { launch_pivot(d_, st_); });
 }
 
+// With a device-initiated transport the (z, j) and ratio messages are stored
+// into the peers' mailboxes by the producing kernel's last CTA (no collective
+// launch); the *_final kernels wait on the flags.
 void Solver::seq_price() {
+    d_.fused = 0;
+    if (sharded_ && comm_->fused_slot(&d_.px_price)) d_.fused = 1;
     L(K_PRICE, bytes_of(K_PRICE), [&] { launch_price(d_, st_); });
     if (sharded_) {
-        L(K_COMM, 0.0, [&] { comm_->allgather(d_.pmsg, d_.pmsg + 1, sizeof(PriceMsg), st_); });
+        if (!d_.fused) L(K_COMM, 0.0, [&] { comm_->allgather(d_.pmsg, d_.pmsg + 1, sizeof(PriceMsg), st_); });
         L(K_OTHER, 0.0, [&] { launch_price_final(d_, st_); });
     }
+    d_.fused = 0;
 }
 
 void Solver::seq_update() {
+    d_.fused = 0;
+    if (sharded_ && comm_->fused_slot(&d_.px_ratio)) d_.fused = 1;
     L(K_UPDATE, bytes_of(K_UPDATE), [&] { launch_update(d_, st_); });
     if (sharded_) {
-        L(K_COMM, 0.0, [&] { comm_->allgather(d_.rmsg, d_.rmsg + 1, sizeof(RatioMsg), st_); });
+        if (!d_.fused) L(K_COMM, 0.0, [&] { comm_->allgather(d_.rmsg, d_.rmsg + 1, sizeof(RatioMsg), st_); });
         L(K_OTHER, 0.0, [&] { launch_ratio_final(d_, st_); });
     }
+    d_.fused = 0;
 }
 
 void Solver::enqueue_pivots(int n) {
