@@ -1641,7 +1641,7 @@ void configure_kernels(Dev& d) {
     const int G = d.num_sms;
     // update + FTRAN: h rows per CTA (even, so the TMA box row is a 16-byte multiple)
     int h = (d.mloc + G - 1) / G;
-    h = std::min(256, std::max(2, (h + 1) & ~1));
+    h = std::min(224, std::max(2, (h + 1) & ~1));  // <= 224 rows: 8 update + 7 FTRAN + 1 producer warps = 512 threads
     d.upd_h = h;
     d.update_grid = (d.mloc + h - 1) / h;
     // columns per stage: short row blocks (small m) take wide stages so the
