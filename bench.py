@@ -335,11 +335,15 @@ def run_ours(args, cfg):
         calls = (x1["calls"] - x0["calls"]) / max(1, done)
         nbytes = (x1["bytes"] - x0["bytes"]) / max(1, done)
         ex = kern.get("exchange")
+        oth = kern.get("other")  # k_price_final / k_ratio_final: the flag waits + merges
         exchange = {"transport": ("P2P: device-initiated NVLink stores + sequence flags (CUDA IPC heaps)"
                                   if args.transport == "p2p" else "NCCL (NVLink/NVSwitch)"),
                     "collectives_per_pivot": round(calls, 2),
                     "payload_bytes_per_pivot_per_rank": round(nbytes, 1),
                     "us_per_pivot": round(1e3 * ex["ms_total"] / max(1, done_p), 2) if ex else None,
+                    "us_per_pivot_incl_merge_kernels": round(
+                        1e3 * ((ex["ms_total"] if ex else 0.0) + (oth["ms_total"] if oth else 0.0)) /
+                        max(1, done_p), 2),
                     "note": "per pivot: pivot-row broadcast from its owner (m+3 words), the (z, j) "
                             "and ratio-message exchanges (P2P: stored into the peers' mailboxes by the "
                             "producing kernels' last CTA, no collective launch; NCCL: all-gathers)"}
