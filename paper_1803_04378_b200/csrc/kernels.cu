@@ -568,7 +568,7 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
 // P2P, fused: the last CTA of k_update copies this shard's RatioMsg (just
 // written to d.rmsg by its threads) into every peer's mailbox slot [rank] and
 // raises the flags. All threads of the CTA call it.
-__device__ __noinline__ void ratio_put(const Dev& d) {
+__device__ __forceinline__ void ratio_put(const Dev& d) {
     __syncthreads();
     const PeerArgs& a = d.px_ratio;
     constexpr int kWords = sizeof(RatioMsg) / 8;

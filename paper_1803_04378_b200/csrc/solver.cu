@@ -731,12 +731,16 @@ int Solver::run_phase() {
     // complete when read).
     const bool pipelined = !prof_ && getenv("LPSG_NO_PIPELINE") == nullptr && (!comm_ || comm_->allows_pipelining());
     bool enqueued = false;
+    // Adaptive batch: a tie stops the device chain, and the rest of the batch (and
+    // the one in flight) then runs as no-op launches. Degenerate LPs tie on most
+    // pivots, so shrink the batch after a tie and grow it back after clean ones.
+    int cur = batch_;
     for (;;) {
-        if (!enqueued) enqueue_pivots(batch_);
+        if (!enqueued) enqueue_pivots(cur);
         enqueued = false;
         if (pipelined) {
             snapshot();
-            enqueue_pivots(batch_);
+            enqueue_pivots(cur);
             enqueued = true;
             CK(cudaEventSynchronize(ev_snap_));
             CK(cudaGetLastError());
@@ -751,9 +755,11 @@ int Solver::run_phase() {
         drain_log();
         const int st = hctl_->status;
         if (st == ST_RUNNING) {
+            cur = std::min(batch_, cur * 2);
             if (!pipelined) push();
             continue;
         }
+        if (st == ST_TIE || st == ST_OVERFLOW) cur = std::max(1, cur / 4);
         enqueued = false;  // an in-flight batch (if any) no-ops: the device stopped
         if (st == ST_TIE) {
             std::vector<int> cand(hctl_->ncand);
