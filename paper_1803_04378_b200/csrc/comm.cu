@@ -349,6 +349,11 @@ public:
     // Shards sharing one GPU in one process keep to one batch in flight: their
     // spin-waiting exchange kernels compete for the same SMs.
     bool allows_pipelining() const override { return h_->hub == nullptr; }
+    void wait_slot(const PeerArgs& a, cudaStream_t st) override {
+        k_peer_wait<<<1, 32, 0, st>>>(a);
+        cuda_ok(cudaGetLastError(), "k_peer_wait");
+    }
+    size_t sym_offset(const void* p) const override { return (size_t)(static_cast<const char*>(p) - h_->base); }
     bool fused_slot(PeerArgs* out) override {
         const unsigned long long seq = ++h_->seq;
         *out = PeerArgs{peers_dev_, rank, size, seq, kFlagBytes + (seq & 1) * kMailbox, trace_ ? 1 : 0, timeout_ns_};

@@ -69,6 +69,17 @@ public:
         (void)out;
         return false;
     }
+    // Completes a reserved exchange whose payload and flags the kernels stored:
+    // waits (stream-ordered, one CTA) until every rank raised the flag.
+    virtual void wait_slot(const PeerArgs& a, cudaStream_t st) {
+        (void)a;
+        (void)st;
+    }
+    // Offset of a sym_alloc'ed pointer in the symmetric heap (P2P), else 0.
+    virtual size_t sym_offset(const void* p) const {
+        (void)p;
+        return 0;
+    }
     // Whether the solver may keep a second pivot batch in flight while it
     // drains the first (pipelined host loop).
     virtual bool allows_pipelining() const { return true; }

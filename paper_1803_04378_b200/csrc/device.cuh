@@ -83,6 +83,7 @@ struct Ctl {
     unsigned int ticket_price;
     unsigned int ticket_update;
     unsigned int ticket_misc;
+    unsigned int ticket_x;     // k_pivot_row's last CTA (fused P2P signal)
     int found;         // drive-out scan result
     double found_red;
     int no_ratio;      // FTRAN without the fused ratio test (drive-out, step API)
@@ -106,6 +107,9 @@ struct Dev {
     // (k_price_final / k_ratio_final) waits and reads its own mailbox.
     int fused;
     PeerArgs px_price, px_ratio;
+    int fused_x;           // P2P: k_pivot_row stores the pivot row into the peers' xbuf
+    PeerArgs px_x;
+    size_t xbuf_off;       // xbuf's offset in the symmetric heap
     double* cand_ratio;    // ratios of the candidates in cand (same order)
     long long ldT;
     long long ld_nb;

@@ -1040,11 +1040,30 @@ __global__ void __launch_bounds__(1024) k_ratio(Dev d) {
 // world > 1: the owner of row r divides it in k_pivot_row and the shards sum
 // their xbuf as int64 bit patterns (the others contribute 0), which delivers
 // the owner's doubles bit for bit; k_pivot then runs on every shard from xbuf.
+// P2P, fused (d.fused_x): the owner's threads also store their x_j straight
+// into every peer's xbuf (same symmetric offset) and every shard's last CTA
+// raises its flag for px_x (always, even when the device has stopped, so the
+// wait that follows can never hang); k_peer_wait then completes the exchange.
+__device__ __forceinline__ void pivot_row_signal(const Dev& d) {
+    if (!d.fused_x) return;
+    __threadfence_system();
+    if (!last_block(&d.ctl->ticket_x)) return;
+    if (threadIdx.x == 0) d.ctl->ticket_x = 0;
+    peer_signal(d.px_x);
+}
+
+__device__ __forceinline__ void put_x(const Dev& d, int j, double v) {
+    const PeerArgs& a = d.px_x;
+    for (int g = 0; g < a.size; ++g)
+        if (g != a.rank) reinterpret_cast<double*>(a.peers[g] + d.xbuf_off)[j] = v;
+}
+
 __global__ void __launch_bounds__(256) k_pivot_row(Dev d) {
     Ctl* c = d.ctl;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     if (c->status != ST_RUNNING) {
         if (gtid == 0) c->x_owner = 0;
+        pivot_row_signal(d);
         return;
     }
     const int m = d.m;
@@ -1058,6 +1077,7 @@ __global__ void __launch_bounds__(256) k_pivot_row(Dev d) {
         // xbuf remotely, so we must not touch it
         if (d.xbuf_zero)
             for (int j = gtid; j <= m + 2; j += gstride) xb[j] = 0;
+        pivot_row_signal(d);
         return;
     }
     const double yr = d.Y[li];
@@ -1065,12 +1085,18 @@ __global__ void __launch_bounds__(256) k_pivot_row(Dev d) {
     for (int j = gtid; j <= m; j += gstride) {
         const double xj = ddiv(d.T[(size_t)j * d.ldT + li], yr);
         d.xbuf[j] = xj;
+        if (d.fused_x) put_x(d, j, xj);
         if (ok) d.T[(size_t)j * d.ldT + li] = xj;  // in place (solver.cpp:246-247)
     }
     if (gtid == 0) {
         d.xbuf[m + 1] = ddiv(yr, yr);
         d.xbuf[m + 2] = yr;
+        if (d.fused_x) {
+            put_x(d, m + 1, d.xbuf[m + 1]);
+            put_x(d, m + 2, yr);
+        }
     }
+    pivot_row_signal(d);
 }
 
 __global__ void __launch_bounds__(256) k_pivot(Dev d) {

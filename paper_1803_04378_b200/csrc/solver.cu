@@ -630,8 +630,18 @@ void Solver::seq_pivot() {
         L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot(d_, st_); });
         return;
     }
-    L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot_row(d_, st_); });
-    L(K_COMM, 0.0, [&] { comm_->owner_bcast(d_.xbuf, sizeof(double) * ((size_t)m_ + 3), &d_.ctl->x_owner, st_); });
+    d_.fused_x = 0;
+    if (comm_->fused_slot(&d_.px_x)) {
+        // P2P: the owner's k_pivot_row stores x into the peers' xbuf itself
+        d_.fused_x = 1;
+        d_.xbuf_off = comm_->sym_offset(d_.xbuf);
+        L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot_row(d_, st_); });
+        L(K_COMM, 0.0, [&] { comm_->wait_slot(d_.px_x, st_); });
+        d_.fused_x = 0;
+    } else {
+        L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot_row(d_, st_); });
+        L(K_COMM, 0.0, [&] { comm_->owner_bcast(d_.xbuf, sizeof(double) * ((size_t)m_ + 3), &d_.ctl->x_owner, st_); });
+    }
     L(K_PIVOT, 0.0, [&] { launch_pivot(d_, st_); });
 }
 
