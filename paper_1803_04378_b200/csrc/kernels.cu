@@ -1099,48 +1099,46 @@ __global__ void __launch_bounds__(256) k_pivot_row(Dev d) {
     pivot_row_signal(d);
 }
 
+// Latency-bound (one element per thread): every load the kernel needs is issued
+// up front in parallel, the CTA ticket is taken as soon as the loaded values are
+// in registers (so the last CTA may overwrite the d slot and the slot maps that
+// every CTA read), and the pivot-row / top-row / A_nb stores drain after it. The
+// logged objective is recomputed from T[m][r] by the bookkeeping thread with the
+// (the new T[0][m]) is written into the log entry by the thread that owns j = m,
+// so no CTA ever reads another CTA's store.
 __global__ void __launch_bounds__(256) k_pivot(Dev d) {
     pdl_wait();
     pdl_trigger();
     Ctl* c = d.ctl;
     if (c->status != ST_RUNNING) return;
     const int m = d.m;
-    const int r = c->r, q = c->q;
+    const int r = c->r, q = c->q, n_scan = c->n_scan;
     const bool sharded = d.sharded != 0;
+    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    const int gstride = gridDim.x * blockDim.x;
+    const size_t ldT = (size_t)d.ldT;
+    // independent loads, all in flight together
     const double yr = sharded ? d.xbuf[m + 2] : d.Y[r];
+    const double dk = d.top[m + 1];
+    const int p_leave = d.basic[r];
+    const int s_q = d.col2slot[q];
+    const int last_col = n_scan > 0 ? d.slot2col[n_scan - 1] : -1;
+    const bool one = gtid <= m && gtid + gstride > m;  // this thread owns at most one j
+    double tj = 0.0, topj = 0.0;
+    if (one) {
+        tj = sharded ? d.xbuf[gtid] : d.T[(size_t)gtid * ldT + r];
+        topj = d.top[gtid];
+    }
     if (fabs(yr) <= d.pivot_tol) {
         if (blockIdx.x == 0 && threadIdx.x == 0) c->status = ST_PIVOT_ERR;
         return;
     }
-    const double dk = d.top[m + 1];
     const double ndk = -dk;
-    const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    const int gstride = gridDim.x * blockDim.x;
-    for (int j = gtid; j <= m; j += gstride) {
-        double xj;
-        if (sharded) {
-            xj = d.xbuf[j];  // d.xrow == d.xbuf
-        } else {
-            xj = ddiv(d.T[(size_t)j * d.ldT + r], yr);
-            d.xrow[j] = xj;
-            d.T[(size_t)j * d.ldT + r] = xj;  // in place, like pr[j] /= y_rk (solver.cpp:246-247)
-        }
-        const double p = dmul(ndk, xj);
-        if (p != 0.0) d.top[j] = dadd(d.top[j], p);
-    }
-    double xl = 0.0;
-    if (gtid == 0) {
-        xl = sharded ? d.xbuf[m + 1] : ddiv(yr, yr);
-        if (!sharded) d.xrow[m + 1] = xl;
-    }
     // nonbasic slot maintenance for this shard's columns [col0, col1): the
     // leaving column takes the entering column's slot, or is appended when the
     // entering column lives on another shard; an entering column whose leaver
     // is not ours (artificial or another shard's) is removed by moving the
     // last slot into its place.
-    const int p_leave = d.basic[r];
-    const int s_q = d.col2slot[q];
-    const int n_scan = c->n_scan;
     const bool p_local = p_leave < d.n_total && p_leave >= d.col0 && p_leave < d.col1;
     const bool q_local = s_q >= 0;
     int dst = -1, src_col = -1;
@@ -1149,55 +1147,81 @@ __global__ void __launch_bounds__(256) k_pivot(Dev d) {
         src_col = p_leave;
     } else if (q_local && s_q != n_scan - 1) {
         dst = s_q;
-        src_col = d.slot2col[n_scan - 1];
+        src_col = last_col;
+    }
+    const double* __restrict__ src = d.A_cm + (size_t)(dst >= 0 ? src_col : 0) * d.ld_cm;
+    const bool one_i = dst >= 0 && gtid < m && gtid + gstride >= m;
+    const double ai = one_i ? src[gtid] : 0.0;
+    // every value read above is in registers once it has been used: take the
+    // ticket now; the stores below never feed another CTA's loads
+    const double xl = ddiv(yr, yr);
+    double xj = 0.0;
+    if (one) xj = sharded ? tj : ddiv(tj, yr);
+    const int li = c->log_len;  // monotonic; the log is a ring the host drains
+    LogEntry* const ent = d.log + li % d.log_cap;
+    const bool last = last_block(&c->ticket_misc);
+    if (one) {
+        if (!sharded) {
+            d.xrow[gtid] = xj;
+            d.T[(size_t)gtid * ldT + r] = xj;  // in place, like pr[j] /= y_rk (solver.cpp:246-247)
+        }
+        const double p = dmul(ndk, xj);
+        const double nt = (p != 0.0) ? dadd(topj, p) : topj;
+        if (p != 0.0) d.top[gtid] = nt;
+        if (gtid == m) ent->objective = nt;
+    } else {
+        for (int j = gtid; j <= m; j += gstride) {
+            const double x = sharded ? d.xbuf[j] : ddiv(d.T[(size_t)j * ldT + r], yr);
+            if (!sharded) {
+                d.xrow[j] = x;
+                d.T[(size_t)j * ldT + r] = x;
+            }
+            const double p = dmul(ndk, x);
+            const double t0 = d.top[j];
+            const double nt = (p != 0.0) ? dadd(t0, p) : t0;
+            if (p != 0.0) d.top[j] = nt;
+            if (j == m) ent->objective = nt;
+        }
     }
     if (dst >= 0) {
-        const double* __restrict__ src = d.A_cm + (size_t)src_col * d.ld_cm;
-        for (int i = gtid; i < m; i += gstride) d.A_nb[(size_t)i * d.ld_nb + dst] = src[i];
+        if (one_i) d.A_nb[(size_t)gtid * d.ld_nb + dst] = ai;
+        else
+            for (int i = gtid; i < m; i += gstride) d.A_nb[(size_t)i * d.ld_nb + dst] = src[i];
     }
-    if (!last_block(&c->ticket_misc)) return;
-    if (threadIdx.x == 0) {
-        c->ticket_misc = 0;
-        c->work[2] += 1;
-        // the d slot (T[0][m+1]) is every CTA's multiplier source: update it
-        // only after all of them have read it
-        {
-            const double x_l = sharded ? d.xbuf[m + 1] : ((volatile double*)d.xrow)[m + 1];
-            const double p = dmul(ndk, x_l);
-            if (p != 0.0) d.top[m + 1] = dadd(dk, p);
-        }
-        int ns = n_scan;
-        if (p_local) {
-            if (!q_local) ++ns;
-            d.slot2col[dst] = p_leave;
-            d.col2slot[p_leave] = dst;
-        } else if (q_local) {
-            if (dst >= 0) {
-                d.slot2col[dst] = src_col;
-                d.col2slot[src_col] = dst;
-            }
-            --ns;
-        }
-        if (q < d.n_total) d.col2slot[q] = -1;
-        c->n_scan = ns;
-        d.basic[r] = q;
-        c->total_iter += 1;
-        const int li = c->log_len;  // monotonic; the log is a ring the host drains
-        {
-            LogEntry e;
-            e.iteration = c->total_iter;
-            e.phase = c->phase;
-            e.row = r;
-            e.leaving = p_leave;
-            e.entering = q;
-            e.objective = ((volatile double*)d.top)[m];
-            d.log[li % d.log_cap] = e;
-        }
-        c->log_len = li + 1;
-        c->pending = 1;
-        c->upd_r = r;
-        c->upd_q = q;
+    if (gtid == 0 && !sharded) d.xrow[m + 1] = xl;
+    if (!last || threadIdx.x != 0) return;
+    c->ticket_misc = 0;
+    c->work[2] += 1;
+    {
+        // the d slot (T[0][m+1]) is every CTA's multiplier source
+        const double p = dmul(ndk, xl);
+        if (p != 0.0) d.top[m + 1] = dadd(dk, p);
     }
+    int ns = n_scan;
+    if (p_local) {
+        if (!q_local) ++ns;
+        d.slot2col[dst] = p_leave;
+        d.col2slot[p_leave] = dst;
+    } else if (q_local) {
+        if (dst >= 0) {
+            d.slot2col[dst] = src_col;
+            d.col2slot[src_col] = dst;
+        }
+        --ns;
+    }
+    if (q < d.n_total) d.col2slot[q] = -1;
+    c->n_scan = ns;
+    d.basic[r] = q;
+    c->total_iter += 1;
+    ent->iteration = c->total_iter;
+    ent->phase = c->phase;
+    ent->row = r;
+    ent->leaving = p_leave;
+    ent->entering = q;
+    c->log_len = li + 1;
+    c->pending = 1;
+    c->upd_r = r;
+    c->upd_q = q;
 }
 
 // --------------------------------------------------------- drive-out scan ---
