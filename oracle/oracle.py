@@ -177,6 +177,80 @@ class Ref(_Lib):
         return self._take(self.lib.ref_lp_generate(rows, cols, sparsity, seed, form),
                           f"{rows}_{cols}_f{form}_s{seed}")
 
+    # ---- MPS ingestion chain on in-memory text (ref_shim.cpp ref_mps_*) ----
+    def _mps_sigs(self):
+        L = self.lib
+        if getattr(self, "_mps_ready", False):
+            return L
+        L.ref_mps_load.restype = C.c_void_p
+        L.ref_mps_load.argtypes = [C.c_char_p]
+        L.ref_last_error_kind.restype = C.c_char_p
+        L.ref_mps_warnings.restype = C.c_char_p
+        L.ref_mps_warnings.argtypes = [C.c_void_p]
+        L.ref_mps_written.restype = C.c_char_p
+        L.ref_mps_written.argtypes = [C.c_void_p]
+        L.ref_mps_map.argtypes = [C.c_void_p, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                  C.POINTER(C.c_double), C.POINTER(C.c_uint8),
+                                  C.POINTER(C.c_int), C.POINTER(C.c_int)]
+        L.ref_mps_recover.restype = C.c_int
+        L.ref_mps_recover.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_double,
+                                      C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.ref_generated_mps.restype = C.c_char_p
+        L.ref_generated_mps.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int]
+        self._mps_ready = True
+        return L
+
+    def mps_load(self, text) -> dict:
+        """parse_mps + to_general_lp + canonicalize on `text`. Returns the
+        standard form, the CanonicalMap, the warnings and write_mps(doc), or
+        {"error_kind", "error"} when the reference throws."""
+        L = self._mps_sigs()
+        data = text.encode("latin-1") if isinstance(text, str) else bytes(text)
+        h = L.ref_mps_load(data)
+        if not h:
+            return {"error_kind": L.ref_last_error_kind().decode(), "error": self.last_error()}
+        m, n = C.c_int(), C.c_int()
+        L.ref_lp_dims(h, C.byref(m), C.byref(n))
+        m, n = m.value, n.value
+        oc, ns = C.c_int(), C.c_int()
+        L.ref_mps_map(h, C.byref(oc), C.byref(ns), None, None, None, None)
+        shift = np.zeros(oc.value); neg = np.zeros(m, np.uint8)
+        sp = np.zeros(max(ns.value, 1), np.int32); sn = np.zeros(max(ns.value, 1), np.int32)
+        L.ref_mps_map(h, C.byref(oc), C.byref(ns), _ptr(shift, C.c_double), _ptr(neg, C.c_uint8),
+                      _ptr(sp, C.c_int), _ptr(sn, C.c_int))
+        out = {"warnings": L.ref_mps_warnings(h).decode("latin-1"),
+               "written": L.ref_mps_written(h).decode("latin-1"),
+               "shift": shift, "negated_row": neg, "split_pos": sp[:ns.value],
+               "split_neg": sn[:ns.value], "_h": h}
+        A = np.zeros((m, n)); b = np.zeros(m); c = np.zeros(n)
+        ck = np.zeros(n, np.uint8)
+        sgn, const = C.c_double(), C.c_double()
+        L.ref_lp_copy(h, _ptr(A, C.c_double), _ptr(b, C.c_double), _ptr(c, C.c_double),
+                      _ptr(ck, C.c_uint8), C.byref(sgn), C.byref(const))
+        out["lp"] = LP(m, n, A, b, c, ck, sgn.value, const.value, "")
+        return out
+
+    def mps_recover(self, loaded: dict, x_std, z_std: float):
+        L = self._mps_sigs()
+        x_std = np.ascontiguousarray(x_std, np.float64)
+        x = np.zeros(len(loaded["shift"])); z = C.c_double()
+        if L.ref_mps_recover(loaded["_h"], _ptr(x_std, C.c_double), len(x_std), float(z_std),
+                             _ptr(x, C.c_double), C.byref(z)):
+            raise RuntimeError(L.ref_last_error_kind().decode() + ": " + self.last_error())
+        return x, z.value
+
+    def mps_free(self, loaded: dict) -> None:
+        if loaded.get("_h"):
+            self.lib.ref_lp_free(loaded.pop("_h"))
+
+    def generated_mps(self, rows: int, cols: int, seed: int = 1, form: int = 0,
+                      sparsity: int = 0) -> str:
+        L = self._mps_sigs()
+        t = L.ref_generated_mps(rows, cols, sparsity, seed, form)
+        if t is None:
+            raise RuntimeError(self.last_error())
+        return t.decode("latin-1")
+
     def from_mps(self, path: str) -> LP:
         return self._take(self.lib.ref_lp_from_mps(path.encode()),
                           os.path.splitext(os.path.basename(path))[0])

@@ -12,6 +12,10 @@
 //     (lp_model.cpp:43-163).
 //   * ref_lp_from_mps  — lps::parse_mps_file + to_general_lp + canonicalize
 //     (mps.cpp:216,227) for the Netlib fixtures.
+//   * ref_mps_*        — the MPS ingestion chain on in-memory text: parse_mps +
+//     to_general_lp (warnings kept) + canonicalize (+ CanonicalMap) +
+//     recover_solution, write_mps and to_mps_document (mps.cpp, lp_model.cpp),
+//     for the ingestion parity tests (tests/test_mps.py).
 //   * ref_solve        — lps::two_phase_solve (solver.cpp:394-397) with a
 //     per-pivot trace taken through SolverConfig::observer (solver.hpp:21-32,
 //     solver.cpp:264-275): the changed basis row is found by diffing `basic`.
@@ -19,6 +23,7 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <sstream>
 #include <string>
 #include <vector>
 
@@ -35,7 +40,24 @@ thread_local std::string g_err;
 struct RefLP {
     lps::StandardFormLP lp;
     lps::CanonicalMap map;
+    std::vector<std::string> warnings;  // parse + to_general_lp, in order
+    std::string written;                // write_mps(parse_mps(text))
 };
+
+// The most derived lps error type, for the error-behaviour parity tests.
+const char* error_kind(const std::exception& e) {
+#define LPS_KIND(T) \
+    if (dynamic_cast<const lps::T*>(&e)) return #T;
+    LPS_KIND(InconsistentBounds) LPS_KIND(EmptyProblem) LPS_KIND(LengthMismatch)
+    LPS_KIND(UnknownSection) LPS_KIND(UndeclaredRow) LPS_KIND(DuplicateRow)
+    LPS_KIND(MissingObjectiveRow) LPS_KIND(MalformedNumber) LPS_KIND(UnsupportedBoundKind)
+    LPS_KIND(Error)
+#undef LPS_KIND
+    return "std::exception";
+}
+
+thread_local std::string g_kind;
+thread_local std::string g_text;
 
 }  // namespace
 
@@ -98,6 +120,90 @@ void* ref_lp_from_mps(const char* path) {
         lps::GeneralLP g = lps::to_general_lp(lps::parse_mps_file(path));
         auto [lp, map] = lps::canonicalize(g);
         return new RefLP{std::move(lp), std::move(map)};
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
+// parse_mps(text) -> to_general_lp -> canonicalize; nullptr on error
+// (ref_last_error / ref_last_error_kind).
+void* ref_mps_load(const char* text) {
+    try {
+        auto* r = new RefLP{};
+        lps::MpsDocument doc = lps::parse_mps(std::string(text));
+        r->warnings = doc.warnings;
+        r->written = lps::write_mps(doc);
+        lps::GeneralLP g;
+        try {
+            g = lps::to_general_lp(doc, &r->warnings);
+            auto [lp, map] = lps::canonicalize(g);
+            r->lp = std::move(lp);
+            r->map = std::move(map);
+        } catch (...) {
+            delete r;
+            throw;
+        }
+        return r;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        g_kind = error_kind(e);
+        return nullptr;
+    }
+}
+
+const char* ref_last_error_kind() { return g_kind.c_str(); }
+
+// Warnings joined by '\n', then the written document, as NUL-free text.
+const char* ref_mps_warnings(void* h) {
+    g_text.clear();
+    for (const auto& w : static_cast<RefLP*>(h)->warnings) g_text += w + "\n";
+    return g_text.c_str();
+}
+
+const char* ref_mps_written(void* h) { return static_cast<RefLP*>(h)->written.c_str(); }
+
+// CanonicalMap: shift[orig_cols], negated_row[m] (0/1), split pairs (pos, neg).
+void ref_mps_map(void* h, int* orig_cols, int* n_split, double* shift, std::uint8_t* negated,
+                 int* split_pos, int* split_neg) {
+    const lps::CanonicalMap& mp = static_cast<RefLP*>(h)->map;
+    *orig_cols = mp.orig_cols;
+    *n_split = int(mp.split_pairs.size());
+    if (shift) std::memcpy(shift, mp.shift.data(), sizeof(double) * mp.shift.size());
+    if (negated)
+        for (std::size_t i = 0; i < mp.negated_row.size(); ++i) negated[i] = mp.negated_row[i] ? 1 : 0;
+    for (std::size_t k = 0; k < mp.split_pairs.size(); ++k) {
+        if (split_pos) split_pos[k] = mp.split_pairs[k].pos;
+        if (split_neg) split_neg[k] = mp.split_pairs[k].neg;
+    }
+}
+
+// recover_solution(map, x_std[n], z_std) -> x[orig_cols], *z; 1 on error.
+int ref_mps_recover(void* h, const double* x_std, int n, double z_std, double* x, double* z) {
+    try {
+        auto [xo, zo] = lps::recover_solution(static_cast<RefLP*>(h)->map,
+                                              std::vector<double>(x_std, x_std + n), z_std);
+        std::memcpy(x, xo.data(), sizeof(double) * xo.size());
+        *z = zo;
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        g_kind = error_kind(e);
+        return 1;
+    }
+}
+
+// write_mps(to_mps_document(generate(spec) with the input form)): the text
+// a generated instance is saved as.
+const char* ref_generated_mps(int rows, int cols, int sparsity, std::uint64_t seed, int form) {
+    try {
+        lps::GeneralLP g = lps::generate({rows, cols, static_cast<lps::SparsityClass>(sparsity), seed});
+        if (form >= 1) {
+            for (int i = 0; i < g.num_rows; ++i) g.row_kind[i] = lps::RowKind::le;
+            g.sense = lps::Sense::maximize;
+        }
+        g_text = lps::write_mps(lps::to_mps_document(g));
+        return g_text.c_str();
     } catch (const std::exception& e) {
         g_err = e.what();
         return nullptr;

@@ -135,24 +135,41 @@ def timed_solve(lp: StandardFormLP, cfg: Optional[SolverConfig] = None, runs: in
 
 def run_suite(instances: Sequence, cfg: Optional[SolverConfig] = None, runs: int = 1,
               reference: Optional[Callable[[StandardFormLP], float]] = None) -> List[BenchRow]:
-    """bench.cpp:155-215. `instances`: (label, StandardFormLP | GenSpec) pairs.
+    """bench.cpp:155-215. `instances`: (label, StandardFormLP | GenSpec | MPS path)
+    pairs; an MPS file goes through parse + to_general_lp + canonicalize
+    (mps.py) like the reference's suite loader (bench.cpp:160-166).
     `reference(lp)`, when given, returns the reference run's seconds (the
     reference harness uses a single-worker naive-kernel solve, 174-181)."""
     rows = []
     for label, inst in instances:
+        mp = None
         try:
-            lp = generate(inst) if isinstance(inst, GenSpec) else inst
-            rep, cnt = timed_solve(lp, cfg, runs)
-        except Exception as e:  # noqa: BLE001 - recorded as a row, like the reference
-            rows.append(BenchRow(label, "ParseError"))
-            _ = e
+            if isinstance(inst, GenSpec):
+                lp = generate(inst)
+            elif isinstance(inst, str):
+                from .mps import load_mps
+                lp, mp = load_mps(inst)
+            else:
+                lp = inst
+        except Exception:  # noqa: BLE001 - a ParseError row, like load_instance (bench.cpp:119-131)
+            rows.append(BenchRow(label, "ParseError", objective=float("nan")))
             continue
+        rep, cnt = timed_solve(lp, cfg, runs)
         it = rep.iterations
         rd, wr = _algorithmic_bytes(lp, it)
-        row = BenchRow(label, status_name(rep.status), rep.objective, rep.iterations_phase1,
+        obj = rep.objective
+        if rep.status in (SolveStatus.optimal, SolveStatus.iteration_limit):
+            # recover_solution's objective (bench.cpp:191-195); generated
+            # instances carry only the sign and constant of their map
+            if mp is not None:
+                from .lp_model import recover_solution
+                obj = recover_solution(mp, rep.x, rep.objective)[1]
+            else:
+                obj = lp.objective_sign * rep.objective + lp.objective_constant
+        row = BenchRow(label, status_name(rep.status), obj, rep.iterations_phase1,
                        rep.iterations_phase2, rep.total_seconds, rep.tpi_seconds, case_name(True),
                        rd, wr, int(cnt["h2d_bytes"]), int(cnt["d2h_bytes"]))
-        if reference is not None:
+        if reference is not None and rep.total_seconds > 0.0:
             row.reference_seconds = float(reference(lp))
             row.speedup = speedup(row.reference_seconds, row.total_seconds)
         rows.append(row)

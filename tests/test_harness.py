@@ -52,3 +52,20 @@ def test_run_suite_rows():
     assert rows[0].speedup == pytest.approx(1.0 / rows[0].total_seconds)
     assert math.isclose(rows[0].tpi_seconds, rows[0].total_seconds / 824)
     assert H.read_csv(H.write_csv(rows))[0].iterations_p2 == 824
+
+
+@pytest.mark.gpu
+def test_run_suite_mps_and_parse_error(tmp_path):
+    """MPS instances go through load_mps and report the recovered objective
+    (bench.cpp:191-195); an unreadable instance is a ParseError row with a NaN
+    objective (bench.cpp:160-168)."""
+    import os
+    import numpy as np
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "mps")
+    z = np.load(os.path.join(here, "production.npz"))
+    bad = tmp_path / "bad.mps"
+    bad.write_text("NAME X\nFOO\n")
+    rows = H.run_suite([("prod", os.path.join(here, "production.mps")), ("bad", str(bad))])
+    assert rows[0].status == "Optimal"
+    assert rows[0].objective == float(z["objective_recovered"])
+    assert rows[1].status == "ParseError" and math.isnan(rows[1].objective)
