@@ -232,11 +232,26 @@ def peer_heap(world: int, rank: int, local: int):
     if _PEER is None:
         import paper_1803_04378_b200 as P
         import torch.distributed as dist
-        h = P.PeerHeap(rank, world, device=local)
+        # every step is agreed by all ranks, so a failure on any rank raises on
+        # all of them together and they fall back to NCCL in step (main())
+        h, err = None, ""
+        try:
+            h = P.PeerHeap(rank, world, device=local)
+        except Exception as e:  # noqa: BLE001
+            err = f"rank {rank}: {e}"
         handles = [None] * world
-        dist.all_gather_object(handles, h.handle)
-        h.connect(handles)
-        dist.barrier()
+        dist.all_gather_object(handles, h.handle if h is not None else None)
+        if h is not None and all(x is not None for x in handles):
+            try:
+                h.connect(handles)
+            except Exception as e:  # noqa: BLE001
+                err = f"rank {rank}: {e}"
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        bad = [e for e in errs if e] or ([] if all(x is not None for x in handles)
+                                          else ["a rank has no peer heap"])
+        if bad:
+            raise RuntimeError("P2P heap unavailable: " + "; ".join(bad))
         _PEER = h
     return _PEER
 
