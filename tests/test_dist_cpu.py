@@ -66,3 +66,49 @@ def test_shard_range_rejects_bad_rank():
     import paper_1803_04378_b200 as P
     with pytest.raises(P.Error):
         P.shard_range(10, 2, 2)
+
+
+class _FakeHeap:
+    """PeerHeap stand-in: rank `bad` fails to create its heap (e.g. no CUDA IPC)."""
+    bad = 1
+
+    def __init__(self, rank, world, device=0):
+        if rank == _FakeHeap.bad:
+            raise RuntimeError("cudaMalloc(peer heap): out of memory")
+        self.handle = bytes([rank]) * (64 * world)
+
+    def connect(self, handles):
+        pass
+
+
+def _peer_worker(rank, world, port, out):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    import bench
+    import paper_1803_04378_b200 as P
+    P.PeerHeap = _FakeHeap
+    w, r, local = bench.dist_ctx()
+    try:
+        bench.peer_heap(w, r, local)
+        out[r] = "connected"
+    except RuntimeError as e:
+        out[r] = str(e)
+    # both ranks must still be in step: a collective after the failure completes
+    out[f"nid{r}"] = bench.share_nccl_id(w, r)
+    import torch.distributed as dist
+    dist.destroy_process_group()
+
+
+def test_p2p_setup_failure_is_agreed_by_all_ranks():
+    """bench.py's P2P heap setup: a failure on ONE rank raises on EVERY rank
+    (so all fall back to NCCL together instead of deadlocking in mismatched
+    collectives)."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_peer_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        assert out[r].startswith("P2P heap unavailable: rank 1: cudaMalloc"), out[r]
+    assert out["nid0"] == out["nid1"]
