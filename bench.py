@@ -311,19 +311,23 @@ def run_ours(args, cfg):
         if st["launches"] and st["ms"] > 0:
             kern[name] = dict(launches=st["launches"], ms_total=round(st["ms"], 4),
                               us_per_launch=round(1e3 * st["ms"] / st["launches"], 3),
-                              gbs=round(st["bytes"] / (st["ms"] / 1e3) / 1e9, 1) if st["bytes"] else None,
                               share=None)
+            if name.startswith("lookahead"):  # compute-bound: "bytes" are fp64 flops
+                kern[name]["tflops"] = round(st["bytes"] / (st["ms"] / 1e3) / 1e12, 3)
+            else:
+                kern[name]["gbs"] = (round(st["bytes"] / (st["ms"] / 1e3) / 1e9, 1)
+                                     if st["bytes"] else None)
     tot = sum(v["ms_total"] for v in kern.values()) or 1.0
     for v in kern.values():
         v["share"] = round(v["ms_total"] / tot, 4)
     roofline = None
     traffic = None
     if kern:
-        hbm = {k: v for k, v in kern.items() if v["gbs"]}
+        hbm = {k: v for k, v in kern.items() if v.get("gbs")}
         dom = max(hbm, key=lambda k: hbm[k]["ms_total"])
         ach = kern[dom]["gbs"]
         # algorithmic bytes of one pivot on this rank; the whole job moves world x that
-        pivot_bytes = sum(stats[k]["bytes"] for k in stats) / max(1, done_p)
+        pivot_bytes = sum(stats[k]["bytes"] for k in stats if not k.startswith("lookahead")) / max(1, done_p)
         job_gbs = pivot_bytes * world * value / 1e9
         roofline = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": peak, "unit": "GB/s",
                     "frac": round(ach / peak, 4), "traffic": None, "peak_source": peak_kind,
@@ -339,6 +343,28 @@ def run_ours(args, cfg):
                     "kernels": kern, "instrumented_pivots": prof_range,
                     "note": "per-kernel CUDA events on the solver stream over a second window of "
                             "K pivots (rank 0); the headline value is the un-instrumented window"}
+        la = {k: v for k, v in kern.items() if "tflops" in v}
+        la_ms = sum(v["ms_total"] for v in la.values())
+        if la and la_ms > sum(v["ms_total"] for v in hbm.values()):
+            # tie pivots dominate (C4): the batched lookahead GEMMs are fp64
+            # SIMT compute-bound (DMUL + DADD per multiply-add, no FMA, no tensor
+            # cores: either would change the bits), so the roofline is the fp64 pipe
+            ldom = max(la, key=lambda k: la[k]["ms_total"])
+            fpk = P.fp64_peak(device)
+            roofline = {"bound": "fp64", "kernel": ldom, "achieved": la[ldom]["tflops"],
+                        "peak": round(fpk, 2), "unit": "TFLOP/s",
+                        "frac": round(la[ldom]["tflops"] / fpk, 4), "traffic": None,
+                        "peak_source": "measured in this run: lpsg_fp64_peak (independent DMUL/DADD "
+                                       "chains on all SMs, 1 flop per instruction)",
+                        "lookahead_share_of_profiled_time": round(la_ms / tot, 4),
+                        "lookahead_tflops_all": round(sum(stats[k]["bytes"] for k in la) /
+                                                      (la_ms / 1e3) / 1e12, 3),
+                        "hbm_side": {"kernel": dom, "achieved_gbs": ach, "peak_gbs": peak,
+                                     "frac": round(ach / peak, 4)},
+                        "kernels": kern, "instrumented_pivots": prof_range,
+                        "note": "flops = 2 per multiply-add of the batched per-candidate dots "
+                                "(K x m x n_scan pricing + K x m x m theta); per-kernel CUDA events "
+                                "on the solver stream over a second window"}
         t = _ncu_traffic(NCU_NAMES.get(dom, dom)) if args.config == "c3" else None  # captures are of C3
         if t is not None and world == 1:
             traffic = t[0]

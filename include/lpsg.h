@@ -216,6 +216,11 @@ int lpsg_last_solve_device_ms(lpsg_solver* s, double* ms);
 int lpsg_counters(lpsg_solver* s, long* kernel_launches, long long* h2d_bytes,
                   long long* d2h_bytes);
 
+/* Measured fp64 SIMT throughput of this device (TFLOP/s), the roofline
+ * denominator of the compute-bound batched lookahead: independent DMUL and DADD
+ * chains (no FMA, like every lpsg dot) on all SMs, each instruction one flop. */
+int lpsg_fp64_peak(int device, double* tflops);
+
 /* Page-locked host buffers (cudaHostAlloc) so lpsg_create's upload of A runs at
  * full DMA bandwidth. Freed with lpsg_host_free. */
 int lpsg_host_alloc(size_t bytes, void** out);

@@ -8,7 +8,7 @@ kernels behind the C ABI in include/lpsg.h.
 from .solver import (  # noqa: F401
     Anticycle, ColKind, CudaError, DegenerateSpec, Error, Form, GenSpec, IterationView,
     PeerHeap, PivotTooSmall, SimplexSolver, SolveReport, SolverConfig, SolveStatus, SparsityClass,
-    StandardFormLP, TRACE_DTYPE, device_count, generate, nccl_unique_id, shard_range, solve_sharded,
+    StandardFormLP, TRACE_DTYPE, device_count, fp64_peak, generate, nccl_unique_id, shard_range, solve_sharded,
     two_phase_solve)
 from .lp_model import (  # noqa: F401
     CanonicalMap, EmptyProblem, GeneralLP, InconsistentBounds, LengthMismatch, RowKind, Sense,
@@ -22,7 +22,7 @@ __all__ = [
     "Anticycle", "ColKind", "CudaError", "DegenerateSpec", "Error", "Form", "GenSpec",
     "IterationView", "PeerHeap", "PivotTooSmall", "SimplexSolver", "SolveReport", "SolverConfig",
     "SolveStatus", "SparsityClass", "StandardFormLP", "TRACE_DTYPE", "device_count",
-    "generate", "nccl_unique_id", "shard_range", "solve_sharded", "two_phase_solve",
+    "fp64_peak", "generate", "nccl_unique_id", "shard_range", "solve_sharded", "two_phase_solve",
     # LP ingestion (lp_model.py, mps.py)
     "CanonicalMap", "EmptyProblem", "GeneralLP", "InconsistentBounds", "LengthMismatch",
     "RowKind", "Sense", "canonicalize", "recover_solution", "DuplicateRow", "MalformedNumber",

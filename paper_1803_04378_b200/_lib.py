@@ -83,6 +83,7 @@ SIGNATURES = [
     ("lpsg_counters", C.c_int, [_P, C.POINTER(C.c_long), C.POINTER(C.c_longlong),
                                 C.POINTER(C.c_longlong)]),
     ("lpsg_host_alloc", C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    ("lpsg_fp64_peak", C.c_int, [C.c_int, _PD]),
     ("lpsg_nccl_unique_id", C.c_int, [C.POINTER(C.c_ubyte)]),
     ("lpsg_solve_sharded", C.c_int, [C.POINTER(Problem), C.POINTER(Config), C.c_int, C.c_int,
                                      C.POINTER(Report), _PD, C.POINTER(Trace), C.c_long,

@@ -1866,11 +1866,26 @@ void launch_la_x(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     k_la_x<<<dim3((d.m + 1 + 255) / 256, la.K), 256, 0, st>>>(d, la);
 }
 
-void launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st) {
+// The per-candidate dot kernels use (K + 63) / 64 CTAs only, so they run on a
+// high-priority side stream next to the batched GEMM that fills the GPU,
+// instead of after it: they are independent of it until the merge kernel.
+static void fork_side(const LaSide* sd, cudaStream_t st) {
+    cudaEventRecord(sd->fork, st);
+    cudaStreamWaitEvent(sd->side, sd->fork, 0);
+}
+
+static void join_side(const LaSide* sd, cudaStream_t st) {
+    cudaEventRecord(sd->join, sd->side);
+    cudaStreamWaitEvent(st, sd->join, 0);
+}
+
+void launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st, const LaSide* sd) {
     k_la_wp<<<dim3((d.m + 255) / 256, la.K), 256, 0, st>>>(d, la);
+    if (sd) fork_side(sd, st);
     // la.nblk = slot tiles + 1 (the last partial holds the leaving column)
+    k_la_leave<<<(la.K + 63) / 64, 64, 0, sd ? sd->side : st>>>(d, la);  // 2 warps x 32 candidates
     if (la.nblk > 1) k_la_gemm_price<<<dim3(la.nblk - 1, (la.K + kLT - 1) / kLT), 256, 0, st>>>(d, la);
-    k_la_leave<<<(la.K + 63) / 64, 64, 0, st>>>(d, la);  // 2 warps x 32 candidates
+    if (sd) join_side(sd, st);
     k_la_price_local<<<la.K, 32, 0, st>>>(d, la);
 }
 
@@ -1878,14 +1893,66 @@ void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int 
     k_la_decide<<<(la.K + 127) / 128, 128, 0, st>>>(d, la, msgs, nsrc);
 }
 
-void launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st) {
+void launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st, const LaSide* sd) {
+    if (sd) fork_side(sd, st);
+    k_la_own<<<(la.K + 63) / 64, 64, 0, sd ? sd->side : st>>>(d, la);
     k_la_gemm_theta<<<dim3(la.nblk_t, (la.K + kLT - 1) / kLT), 256, 0, st>>>(d, la);
-    k_la_own<<<(la.K + 63) / 64, 64, 0, st>>>(d, la);
+    if (sd) join_side(sd, st);
     k_la_theta_local<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);
 }
 
 void launch_la_score(const Dev& d, LookaheadDev& la, const double* tl, int nsrc, cudaStream_t st) {
     k_la_score<<<(la.K + 127) / 128, 128, 0, st>>>(d, la, tl, nsrc);
+}
+
+// fp64 pipe probe: 8 independent DMUL chains and 8 DADD chains per thread
+// (no FMA contraction: --fmad=false and explicit __dmul_rn/__dadd_rn).
+__global__ void __launch_bounds__(256) k_fp64_probe(double* out, int iters, double a, double b) {
+    double m[8], s[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        m[u] = 1.0 + 1e-9 * (threadIdx.x + u);
+        s[u] = 1e-3 * (blockIdx.x + u);
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            m[u] = __dmul_rn(m[u], a);
+            s[u] = __dadd_rn(s[u], b);
+        }
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += m[u] + s[u];
+    if (acc == 12345.678) out[0] = acc;  // keeps the chains alive
+}
+
+double fp64_probe_tflops(cudaStream_t st) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    double* out = nullptr;
+    if (cudaMalloc(&out, sizeof(double)) != cudaSuccess) return 0.0;
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_fp64_probe<<<blocks, threads, 0, st>>>(out, iters, 0.9999999, 1e-12);  // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(e0, st);
+        k_fp64_probe<<<blocks, threads, 0, st>>>(out, iters, 0.9999999, 1e-12);
+        cudaEventRecord(e1, st);
+        cudaEventSynchronize(e1);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        best = std::min(best, ms);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    const double flops = 16.0 * iters * (double)blocks * threads;
+    return cudaGetLastError() == cudaSuccess && best > 0.f ? flops / (best * 1e-3) / 1e12 : 0.0;
 }
 
 void launch_sum_i64(const long long* in, int nsrc, size_t n, long long* out, cudaStream_t st) {

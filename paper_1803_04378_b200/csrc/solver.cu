@@ -144,6 +144,18 @@ private:
     long long n_scan_host_ = 0;
 
     cudaStream_t st_ = nullptr;
+    LaSide la_side_{};          // lookahead side stream (created on first use)
+    const LaSide* side() {
+        if (getenv("LPSG_LA_SERIAL")) return nullptr;  // A/B experiments
+        if (!la_side_.side) {
+            int lo = 0, hi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CK(cudaStreamCreateWithPriority(&la_side_.side, cudaStreamNonBlocking, hi));
+            CK(cudaEventCreateWithFlags(&la_side_.fork, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&la_side_.join, cudaEventDisableTiming));
+        }
+        return &la_side_;
+    }
     Dev d_{};
     Ctl* hctl_ = nullptr;       // pinned mirror of the control block
     LogEntry* hlog_ = nullptr;  // pinned mirror of the pivot log (a ring of log_cap entries)
@@ -165,7 +177,9 @@ private:
 
 public:
     // ---- counters and optional per-kernel CUDA-event profile
-    enum Kind { K_RATIO = 0, K_PIVOT, K_PRICE, K_UPDATE, K_OTHER, K_COMM, K_NUM };
+    // K_LA_*: the batched tie-break lookahead; their "bytes" are fp64 flops
+    // (2 per multiply-add of the batched dots)
+    enum Kind { K_RATIO = 0, K_PIVOT, K_PRICE, K_UPDATE, K_OTHER, K_COMM, K_LA_PRICE, K_LA_THETA, K_NUM };
     struct KStat {
         long launches = 0;
         double ms = 0.0;
@@ -232,7 +246,7 @@ void Solver::L(int kind, double bytes, F&& f) {
 // optimality, a tie) exit at once and move nothing.
 void Solver::flush_profile() {
     std::vector<cudaEvent_t> seen;
-    const int widx[K_NUM] = {-1, 2, 0, 1, -1, -1};
+    const int widx[K_NUM] = {-1, 2, 0, 1, -1, -1, -1, -1};
     for (int k = 0; k < K_NUM; ++k) {
         if (widx[k] < 0) continue;
         const unsigned long long w = hctl_->work[widx[k]];
@@ -519,6 +533,11 @@ Solver::~Solver() {
     if (hone_) cudaFreeHost(hone_);
     if (ev_snap_) cudaEventDestroy(ev_snap_);
     if (pool_) cudaMemPoolDestroy(pool_);
+    if (la_side_.side) {
+        cudaStreamDestroy(la_side_.side);
+        cudaEventDestroy(la_side_.fork);
+        cudaEventDestroy(la_side_.join);
+    }
     if (st_) cudaStreamDestroy(st_);
 }
 
@@ -857,14 +876,17 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     for (int k0 = 0; k0 < K; k0 += kb) {
         la.K = std::min(kb, K - k0);
         CK(cudaMemcpyAsync(rows_d, rows.data() + k0, sizeof(int) * la.K, cudaMemcpyHostToDevice, st_));
-        launch_la_x(d_, la, st_);
-        if (sharded_) comm_->sum_i64(reinterpret_cast<long long*>(la.X), (size_t)la.K * ldx, st_);
-        launch_la_price(d_, la, st_);
-        if (sharded_) comm_->allgather(la.pm, la.pm_all, sizeof(PriceMsg) * la.K, st_);
-        launch_la_decide(d_, la, sharded_ ? la.pm_all : la.pm, G, st_);
-        launch_la_theta(d_, la, st_);
-        if (sharded_) comm_->allgather(la.tl, la.tl_all, sizeof(double) * la.K, st_);
-        launch_la_score(d_, la, sharded_ ? la.tl_all : la.tl, G, st_);
+        ev_chain_ = nullptr;  // the copy is not a kernel of the profile
+        // flops of the batched dots: pricing K x m x n_scan(shard), theta K x m x mloc
+        const double kf = 2.0 * la.K * (double)m;
+        L(K_OTHER, 0.0, [&] { launch_la_x(d_, la, st_); });
+        if (sharded_) L(K_COMM, 0.0, [&] { comm_->sum_i64(reinterpret_cast<long long*>(la.X), (size_t)la.K * ldx, st_); });
+        L(K_LA_PRICE, kf * (double)hctl_->n_scan, [&] { launch_la_price(d_, la, st_, side()); });
+        if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.pm, la.pm_all, sizeof(PriceMsg) * la.K, st_); });
+        L(K_OTHER, 0.0, [&] { launch_la_decide(d_, la, sharded_ ? la.pm_all : la.pm, G, st_); });
+        L(K_LA_THETA, kf * (double)d_.mloc, [&] { launch_la_theta(d_, la, st_, side()); });
+        if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.tl, la.tl_all, sizeof(double) * la.K, st_); });
+        L(K_OTHER, 0.0, [&] { launch_la_score(d_, la, sharded_ ? la.tl_all : la.tl, G, st_); });
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(scores.data() + k0, la.score, sizeof(double) * la.K, cudaMemcpyDeviceToHost, st_));
         CK(cudaStreamSynchronize(st_));
@@ -1475,7 +1497,9 @@ int lpsg_profile(lpsg_solver* s, int enable) {
 
 int lpsg_profile_get(lpsg_solver* s, lpsg_kernel_stat* out, int cap, int* n) {
     if (!s || !n) return bad("lpsg_profile_get: null argument");
-    static const char* names[] = {"ratio", "pivot", "price", "update_ftran", "other", "exchange"};
+    static const char* names[] = {"ratio", "pivot", "price", "update_ftran", "other", "exchange",
+                                  "lookahead_price", "lookahead_theta"};
+    static_assert(sizeof(names) / sizeof(names[0]) == lpsg::Solver::K_NUM, "kernel kind names");
     *n = lpsg::Solver::K_NUM;
     for (int k = 0; out && k < std::min(cap, (int)lpsg::Solver::K_NUM); ++k) {
         out[k].name = names[k];
@@ -1484,6 +1508,15 @@ int lpsg_profile_get(lpsg_solver* s, lpsg_kernel_stat* out, int cap, int* n) {
         out[k].algorithmic_bytes = s->s->kstat[k].bytes;
     }
     return LPSG_OK;
+}
+
+int lpsg_fp64_peak(int device, double* tflops) {
+    if (!tflops) return bad("lpsg_fp64_peak: null argument");
+    return guard([&] {
+        CK_SET_DEVICE(device);
+        *tflops = lpsg::fp64_probe_tflops(0);
+        if (*tflops <= 0.0) throw lpsg::Error(LPSG_CUDA_ERROR, "lpsg_fp64_peak: probe failed");
+    });
 }
 
 int lpsg_host_alloc(size_t bytes, void** out) {

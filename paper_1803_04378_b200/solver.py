@@ -322,11 +322,11 @@ class SimplexSolver:
 
     def profile_stats(self) -> dict:
         n = C.c_int()
-        buf = (L.KernelStat * 8)()
-        _check(self.lib.lpsg_profile_get(self._h, buf, 8, C.byref(n)))
+        buf = (L.KernelStat * 16)()
+        _check(self.lib.lpsg_profile_get(self._h, buf, 16, C.byref(n)))
         return {buf[k].name.decode(): dict(launches=buf[k].launches, ms=buf[k].milliseconds,
                                            bytes=buf[k].algorithmic_bytes)
-                for k in range(min(n.value, 8))}
+                for k in range(min(n.value, 16))}
 
     def device_ms(self) -> float:
         v = C.c_double()
@@ -424,6 +424,14 @@ def two_phase_solve(lp: StandardFormLP, cfg: Optional[SolverConfig] = None) -> S
 
 def device_count() -> int:
     return L.load().lpsg_device_count()
+
+
+def fp64_peak(device: int = 0) -> float:
+    """Measured fp64 SIMT throughput (TFLOP/s, DMUL/DADD without FMA), the
+    roofline denominator of the batched lookahead (include/lpsg.h)."""
+    v = C.c_double()
+    _check(L.load().lpsg_fp64_peak(int(device), C.byref(v)))
+    return v.value
 
 
 def shard_range(n: int, world: int, rank: int):

@@ -14,7 +14,7 @@ for c in ("c3", "c2"):
     try:
         l = json.loads(open(f"gpurun_out/bench_{c}_{tag}.log").read().strip().splitlines()[-1])
         print(c, round(l["value"], 1), "it/s", "frac", l["roofline"]["per_pivot"]["frac"],
-              {k: (v["us_per_launch"], v["gbs"]) for k, v in l["roofline"]["kernels"].items()})
+              {k: (v["us_per_launch"], v.get("gbs", v.get("tflops"))) for k, v in l["roofline"]["kernels"].items()})
     except Exception as e:
         print(c, "ERR", e)
 PY
