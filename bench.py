@@ -362,9 +362,10 @@ def run_ours(args, cfg):
                         "hbm_side": {"kernel": dom, "achieved_gbs": ach, "peak_gbs": peak,
                                      "frac": round(ach / peak, 4)},
                         "kernels": kern, "instrumented_pivots": prof_range,
-                        "note": "flops = 2 per multiply-add of the batched per-candidate dots "
-                                "(K x m x n_scan pricing + K x m x m theta); per-kernel CUDA events "
-                                "on the solver stream over a second window"}
+                        "note": "fp64 flops of the batched lookahead: 2 per pricing term "
+                                "(K x m x n_scan) and 4 per theta term (K x m x m: the updated "
+                                "element T_ij - y_i X_kj, then its product into y'); per-kernel "
+                                "CUDA events on the solver stream over a second window"}
         t = _ncu_traffic(NCU_NAMES.get(dom, dom)) if args.config == "c3" else None  # captures are of C3
         if t is not None and world == 1:
             traffic = t[0]

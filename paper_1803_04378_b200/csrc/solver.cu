@@ -877,14 +877,16 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
         la.K = std::min(kb, K - k0);
         CK(cudaMemcpyAsync(rows_d, rows.data() + k0, sizeof(int) * la.K, cudaMemcpyHostToDevice, st_));
         ev_chain_ = nullptr;  // the copy is not a kernel of the profile
-        // flops of the batched dots: pricing K x m x n_scan(shard), theta K x m x mloc
+        // fp64 flops of the batched work: pricing K x m x n_scan(shard) dot terms
+        // (DMUL + DADD); theta K x mloc x m terms of (T_ij - y_i X_kj) a_j
+        // (two more for the updated element)
         const double kf = 2.0 * la.K * (double)m;
         L(K_OTHER, 0.0, [&] { launch_la_x(d_, la, st_); });
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->sum_i64(reinterpret_cast<long long*>(la.X), (size_t)la.K * ldx, st_); });
         L(K_LA_PRICE, kf * (double)hctl_->n_scan, [&] { launch_la_price(d_, la, st_, side()); });
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.pm, la.pm_all, sizeof(PriceMsg) * la.K, st_); });
         L(K_OTHER, 0.0, [&] { launch_la_decide(d_, la, sharded_ ? la.pm_all : la.pm, G, st_); });
-        L(K_LA_THETA, kf * (double)d_.mloc, [&] { launch_la_theta(d_, la, st_, side()); });
+        L(K_LA_THETA, 2.0 * kf * (double)d_.mloc, [&] { launch_la_theta(d_, la, st_, side()); });
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.tl, la.tl_all, sizeof(double) * la.K, st_); });
         L(K_OTHER, 0.0, [&] { launch_la_score(d_, la, sharded_ ? la.tl_all : la.tl, G, st_); });
         CK(cudaGetLastError());
