@@ -61,8 +61,9 @@ def _ncu_traffic(kernel: str):
     `ncu --set full` summary under profiles/ (tools/ncu_summary.py), or None."""
     import glob
     best = None
+    # a checkout gives every file the same mtime: the *_final_* summary wins
     for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")),
-                    key=os.path.getmtime):
+                    key=lambda p: ("_final_" in os.path.basename(p), os.path.getmtime(p))):
         try:
             with open(p) as f:
                 cap = json.load(f).get("captures", {}).get(kernel)
