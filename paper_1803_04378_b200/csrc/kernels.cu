@@ -1392,74 +1392,94 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_price(Dev d, LookaheadDev la
     }
 }
 
+// CTA-batched per-candidate sequential dots acc_c = sum_i u_c[i] v_c[i] for
+// kDC candidates per CTA (u_c = a row of X or W', v_c = A_cm column vcol_c;
+// vcol_c < 0: no dot). All kDT threads stage kDR-row chunks of the 2 x kDC
+// vectors in shared memory (each warp load is 32 consecutive rows of one
+// vector: 256 contiguous bytes), double-buffered so the next chunk's loads are
+// in flight while threads 0..kDC-1 run their chains over the current one in
+// ascending i. The chains are latency-bound (8 cycles per DADD), so a CTA per
+// 16 candidates spreads them over ~K/16 SMs; the earlier warp-per-32-candidates
+// form kept 32 warps busy for 0.4-1.2 ms at K = 1000, m = 4000.
+constexpr int kDC = 16;   // candidates per CTA
+constexpr int kDR = 64;   // rows per chunk
+constexpr int kDT = 128;  // threads per CTA
+
+struct DotSmem {
+    double u[2][kDC][kDR + 1];  // +1: chain reads of 16 candidates hit 16 bank pairs
+    double v[2][kDC][kDR + 1];
+    const double* ub[kDC];
+    int vc[kDC];
+};
+
+// Returns acc in threads c < kDC (candidate c of the CTA); sm.ub / sm.vc set
+// and synchronised by the caller.
+__device__ __forceinline__ double cta_batched_dot(DotSmem& sm, const double* __restrict__ A_cm, size_t ld_cm,
+                                                  int n) {
+    const int t = threadIdx.x;
+    const int r = t & (kDR - 1), c0 = t / kDR;  // row in chunk, first candidate
+    constexpr int kPer = kDC * kDR / kDT;       // loads per thread per vector
+    double ru[kPer], rv[kPer];
+    auto fetch = [&](int i0) {
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int c = c0 + q * (kDT / kDR);
+            const int i = i0 + r;
+            const double* ub = sm.ub[c];
+            const int vc = sm.vc[c];
+            ru[q] = (ub && i < n) ? __ldg(ub + i) : 0.0;
+            rv[q] = (vc >= 0 && i < n) ? __ldg(A_cm + (size_t)vc * ld_cm + i) : 0.0;
+        }
+    };
+    auto stash = [&](int b) {
+#pragma unroll
+        for (int q = 0; q < kPer; ++q) {
+            const int c = c0 + q * (kDT / kDR);
+            sm.u[b][c][r] = ru[q];
+            sm.v[b][c][r] = rv[q];
+        }
+    };
+    double acc = 0.0;
+    const int nch = (n + kDR - 1) / kDR;
+    fetch(0);
+    stash(0);
+    __syncthreads();
+    for (int ch = 0; ch < nch; ++ch) {
+        const int b = ch & 1;
+        if (ch + 1 < nch) fetch((ch + 1) * kDR);
+        if (t < kDC && sm.vc[t] >= 0) {
+            const int lim = min(kDR, n - ch * kDR);
+            const double* __restrict__ uu = sm.u[b][t];
+            const double* __restrict__ vv = sm.v[b][t];
+            for (int e = 0; e < lim; ++e) acc = dadd(acc, dmul(uu[e], vv[e]));
+        }
+        if (ch + 1 < nch) stash(b ^ 1);
+        __syncthreads();
+    }
+    return acc;
+}
+
 // The leaving variable of candidate k re-enters the nonbasic set
 // (solver.cpp:186-188): priced by the shard owning its column, into the last
 // partial slot (index nblk - 1).
-// One thread's sequential dot (ascending index) with 16 loads in flight ahead
-// of the chain: one-thread-per-output dots are otherwise load-latency bound.
-__device__ __forceinline__ double seq_dot(const double* __restrict__ x, const double* __restrict__ y, int n) {
-    double acc = 0.0;
-    int i = 0;
-    for (; i + 16 <= n; i += 16) {
-        double xv[16], yv[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-            xv[u] = __ldg(x + i + u);
-            yv[u] = __ldg(y + i + u);
+__global__ void __launch_bounds__(kDT) k_la_leave(Dev d, LookaheadDev la) {
+    __shared__ DotSmem sm;
+    const int k0 = blockIdx.x * kDC;
+    if (threadIdx.x < kDC) {
+        const int k = k0 + threadIdx.x;
+        int p = -1;
+        if (k < la.K) {
+            const int pl = d.basic[la.rows[k]];
+            if (pl < d.n_total && pl != la.q && pl >= d.col0 && pl < d.col1) p = pl;
         }
-#pragma unroll
-        for (int u = 0; u < 16; ++u) acc = dadd(acc, dmul(xv[u], yv[u]));
+        sm.vc[threadIdx.x] = p;
+        sm.ub[threadIdx.x] = k < la.K ? la.Wp + (size_t)k * la.ldx : nullptr;
     }
-    for (; i < n; ++i) acc = dadd(acc, dmul(x[i], y[i]));
-    return acc;
-}
-
-// Warp-cooperative batch of per-candidate sequential dots acc_k = sum_i u_k[i]
-// v_k[i] (u_k = U + k*ldu, v_k = A_cm column vcol_k; vcol_k < 0: no dot). Lane
-// l owns candidate 32w + l; every 32-element chunk of the warp's 32 (u, v)
-// pairs is loaded coalesced (one candidate's 32 contiguous doubles per load
-// instruction) into shared memory, transposed, and each lane runs its chain
-// over it in ascending i. One thread per candidate reading its own rows was
-// load-latency bound (1.3 ms for 1000 candidates at m = 4000).
-__device__ __forceinline__ double warp_batched_dot(const double* __restrict__ U, size_t ldu,
-                                                   const double* __restrict__ A_cm, size_t ld_cm, int vcol,
-                                                   int n, int lane, double (*su)[33], double (*sv)[33]) {
-    double acc = 0.0;
-    for (int i0 = 0; i0 < n; i0 += 32) {
-        const int i = i0 + lane;
-        for (int c = 0; c < 32; ++c) {
-            const int vc = __shfl_sync(0xffffffffu, vcol, c);
-            const double* uc = reinterpret_cast<const double*>(
-                __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(U), c));
-            su[c][lane] = (uc && i < n) ? __ldg(uc + i) : 0.0;
-            sv[c][lane] = (vc >= 0 && i < n) ? __ldg(A_cm + (size_t)vc * ld_cm + i) : 0.0;
-        }
-        __syncwarp();
-        if (vcol >= 0) {
-            const int lim = min(32, n - i0);
-            for (int e = 0; e < lim; ++e) acc = dadd(acc, dmul(su[lane][e], sv[lane][e]));
-        }
-        __syncwarp();
-    }
-    (void)ldu;
-    return acc;
-}
-
-// The leaving variable of candidate k re-enters the nonbasic set
-// (solver.cpp:186-188): priced by the shard owning its column, into the last
-// partial slot (index nblk - 1). Warp per 32 candidates.
-__global__ void __launch_bounds__(64) k_la_leave(Dev d, LookaheadDev la) {
-    __shared__ double su[2][32][33], sv[2][32][33];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int k = (blockIdx.x * 2 + w) * 32 + lane;
-    int p = -1;
-    if (k < la.K) {
-        const int pl = d.basic[la.rows[k]];
-        if (pl < d.n_total && pl != la.q && pl >= d.col0 && pl < d.col1) p = pl;
-    }
-    const double* u = k < la.K ? la.Wp + (size_t)k * la.ldx : nullptr;
-    const double acc = warp_batched_dot(u, la.ldx, d.A_cm, d.ld_cm, p, d.m, lane, su[w], sv[w]);
-    if (k >= la.K) return;
+    __syncthreads();
+    const double acc = cta_batched_dot(sm, d.A_cm, d.ld_cm, d.m);
+    const int k = k0 + threadIdx.x;
+    if (threadIdx.x >= kDC || k >= la.K) return;
+    const int p = sm.vc[threadIdx.x];
     double bz = -kInf;
     int bj = INT_MAX;
     if (p >= 0) {
@@ -1472,21 +1492,26 @@ __global__ void __launch_bounds__(64) k_la_leave(Dev d, LookaheadDev la) {
 
 // The candidate's own pivot row r_k becomes X_k (solver.cpp:176): its y' is
 // dot(X_k, a_{b_k}) and its b_bar' is X_k[m]. The tiled kernel skips that row;
-// this one computes its ratio into own_t[k]. Warp per 32 candidates.
-__global__ void __launch_bounds__(64) k_la_own(Dev d, LookaheadDev la) {
-    __shared__ double su[2][32][33], sv[2][32][33];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int k = (blockIdx.x * 2 + w) * 32 + lane;
-    int col = -1;
-    if (k < la.K) {
-        const int rk = la.rows[k], bj = la.bj[k];
-        if (bj >= 0 && rk >= d.row0 && rk < d.row0 + d.mloc && !d.frozen[rk]) col = bj;
+// this one computes its ratio into own_t[k].
+__global__ void __launch_bounds__(kDT) k_la_own(Dev d, LookaheadDev la) {
+    __shared__ DotSmem sm;
+    const int k0 = blockIdx.x * kDC;
+    if (threadIdx.x < kDC) {
+        const int k = k0 + threadIdx.x;
+        int col = -1;
+        if (k < la.K) {
+            const int rk = la.rows[k], bj = la.bj[k];
+            if (bj >= 0 && rk >= d.row0 && rk < d.row0 + d.mloc && !d.frozen[rk]) col = bj;
+        }
+        sm.vc[threadIdx.x] = col;
+        sm.ub[threadIdx.x] = k < la.K ? la.X + (size_t)k * la.ldx : nullptr;
     }
-    const double* x = k < la.K ? la.X + (size_t)k * la.ldx : nullptr;
-    const double acc = warp_batched_dot(x, la.ldx, d.A_cm, d.ld_cm, col, d.m, lane, su[w], sv[w]);
-    if (k >= la.K) return;
+    __syncthreads();
+    const double acc = cta_batched_dot(sm, d.A_cm, d.ld_cm, d.m);
+    const int k = k0 + threadIdx.x;
+    if (threadIdx.x >= kDC || k >= la.K) return;
     double th = kInf;
-    if (col >= 0 && !(acc <= d.pivot_tol)) th = ddiv(x[d.m], acc);
+    if (sm.vc[threadIdx.x] >= 0 && !(acc <= d.pivot_tol)) th = ddiv(sm.ub[threadIdx.x][d.m], acc);
     la.own_t[k] = th;
 }
 
@@ -1866,26 +1891,11 @@ void launch_la_x(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     k_la_x<<<dim3((d.m + 1 + 255) / 256, la.K), 256, 0, st>>>(d, la);
 }
 
-// The per-candidate dot kernels use (K + 63) / 64 CTAs only, so they run on a
-// high-priority side stream next to the batched GEMM that fills the GPU,
-// instead of after it: they are independent of it until the merge kernel.
-static void fork_side(const LaSide* sd, cudaStream_t st) {
-    cudaEventRecord(sd->fork, st);
-    cudaStreamWaitEvent(sd->side, sd->fork, 0);
-}
-
-static void join_side(const LaSide* sd, cudaStream_t st) {
-    cudaEventRecord(sd->join, sd->side);
-    cudaStreamWaitEvent(st, sd->join, 0);
-}
-
-void launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st, const LaSide* sd) {
+void launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     k_la_wp<<<dim3((d.m + 255) / 256, la.K), 256, 0, st>>>(d, la);
-    if (sd) fork_side(sd, st);
     // la.nblk = slot tiles + 1 (the last partial holds the leaving column)
-    k_la_leave<<<(la.K + 63) / 64, 64, 0, sd ? sd->side : st>>>(d, la);  // 2 warps x 32 candidates
     if (la.nblk > 1) k_la_gemm_price<<<dim3(la.nblk - 1, (la.K + kLT - 1) / kLT), 256, 0, st>>>(d, la);
-    if (sd) join_side(sd, st);
+    k_la_leave<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
     k_la_price_local<<<la.K, 32, 0, st>>>(d, la);
 }
 
@@ -1893,11 +1903,9 @@ void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int 
     k_la_decide<<<(la.K + 127) / 128, 128, 0, st>>>(d, la, msgs, nsrc);
 }
 
-void launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st, const LaSide* sd) {
-    if (sd) fork_side(sd, st);
-    k_la_own<<<(la.K + 63) / 64, 64, 0, sd ? sd->side : st>>>(d, la);
+void launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     k_la_gemm_theta<<<dim3(la.nblk_t, (la.K + kLT - 1) / kLT), 256, 0, st>>>(d, la);
-    if (sd) join_side(sd, st);
+    k_la_own<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
     k_la_theta_local<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);
 }
 

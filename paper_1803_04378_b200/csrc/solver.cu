@@ -144,18 +144,6 @@ private:
     long long n_scan_host_ = 0;
 
     cudaStream_t st_ = nullptr;
-    LaSide la_side_{};          // lookahead side stream (created on first use)
-    const LaSide* side() {
-        if (getenv("LPSG_LA_SERIAL")) return nullptr;  // A/B experiments
-        if (!la_side_.side) {
-            int lo = 0, hi = 0;
-            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-            CK(cudaStreamCreateWithPriority(&la_side_.side, cudaStreamNonBlocking, hi));
-            CK(cudaEventCreateWithFlags(&la_side_.fork, cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&la_side_.join, cudaEventDisableTiming));
-        }
-        return &la_side_;
-    }
     Dev d_{};
     Ctl* hctl_ = nullptr;       // pinned mirror of the control block
     LogEntry* hlog_ = nullptr;  // pinned mirror of the pivot log (a ring of log_cap entries)
@@ -533,11 +521,6 @@ Solver::~Solver() {
     if (hone_) cudaFreeHost(hone_);
     if (ev_snap_) cudaEventDestroy(ev_snap_);
     if (pool_) cudaMemPoolDestroy(pool_);
-    if (la_side_.side) {
-        cudaStreamDestroy(la_side_.side);
-        cudaEventDestroy(la_side_.fork);
-        cudaEventDestroy(la_side_.join);
-    }
     if (st_) cudaStreamDestroy(st_);
 }
 
@@ -883,10 +866,10 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
         const double kf = 2.0 * la.K * (double)m;
         L(K_OTHER, 0.0, [&] { launch_la_x(d_, la, st_); });
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->sum_i64(reinterpret_cast<long long*>(la.X), (size_t)la.K * ldx, st_); });
-        L(K_LA_PRICE, kf * (double)hctl_->n_scan, [&] { launch_la_price(d_, la, st_, side()); });
+        L(K_LA_PRICE, kf * (double)hctl_->n_scan, [&] { launch_la_price(d_, la, st_); });
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.pm, la.pm_all, sizeof(PriceMsg) * la.K, st_); });
         L(K_OTHER, 0.0, [&] { launch_la_decide(d_, la, sharded_ ? la.pm_all : la.pm, G, st_); });
-        L(K_LA_THETA, 2.0 * kf * (double)d_.mloc, [&] { launch_la_theta(d_, la, st_, side()); });
+        L(K_LA_THETA, 2.0 * kf * (double)d_.mloc, [&] { launch_la_theta(d_, la, st_); });
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.tl, la.tl_all, sizeof(double) * la.K, st_); });
         L(K_OTHER, 0.0, [&] { launch_la_score(d_, la, sharded_ ? la.tl_all : la.tl, G, st_); });
         CK(cudaGetLastError());
