@@ -209,6 +209,7 @@ struct LookaheadDev {
     int nblk_t;       // theta' partials per candidate (64-row tiles)
     int q;            // entering column
     double d;         // entering reduced cost
+    int* nonfinite;   // set by k_la_wp when some X_kj (j < m) is inf/NaN (host zeroes it)
 };
 
 // ---- launchers (kernels.cu) -------------------------------------------------

@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdlib>
 
+#include <type_traits>
 #include <vector>
 
 #include "device.cuh"
@@ -1294,10 +1295,14 @@ __global__ void k_la_wp(Dev d, LookaheadDev la) {
     const int k = blockIdx.y;
     const double dk = d.top[d.m + 1];
     const double* X = la.X + (size_t)k * la.ldx;
+    bool bad = false;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d.m; j += gridDim.x * blockDim.x) {
         const double w = d.top[j];
-        la.Wp[(size_t)k * la.ldx + j] = dk == 0.0 ? w : dsub(w, dmul(dk, X[j]));
+        const double x = X[j];
+        bad |= !isfinite(x);
+        la.Wp[(size_t)k * la.ldx + j] = dk == 0.0 ? w : dsub(w, dmul(dk, x));
     }
+    if (bad) atomicOr(la.nonfinite, 1);
 }
 
 // ---- register-tiled batched lookahead (a SIMT "GEMM" with sequential sums) --
@@ -1349,8 +1354,7 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_price(Dev d, LookaheadDev la
         }
         __syncthreads();
         if (i0 + kLC < m) fetch(i0 + kLC);
-        const int lim = min(kLC, m - i0);
-        for (int ii = 0; ii < lim; ++ii) {
+        auto step = [&](int ii) {
             double w[4], a[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -1361,6 +1365,12 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_price(Dev d, LookaheadDev la
             for (int u = 0; u < 4; ++u)
 #pragma unroll
                 for (int v = 0; v < 4; ++v) acc[u][v] = dadd(acc[u][v], dmul(w[u], a[v]));
+        };
+        if (i0 + kLC <= m) {
+#pragma unroll
+            for (int ii = 0; ii < kLC; ++ii) step(ii);
+        } else {
+            for (int ii = 0; ii < m - i0; ++ii) step(ii);
         }
         __syncthreads();
     }
@@ -1563,6 +1573,7 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_theta(Dev d, LookaheadDev la
     bool zrow[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) zrow[u] = yv[u] == 0.0;
+    const bool exact = *la.nonfinite != 0;  // some X_kj is inf/NaN: keep the select
     double rt[4], rx[4], rb[4];
     auto fetch = [&](int j0) {
 #pragma unroll
@@ -1589,8 +1600,12 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_theta(Dev d, LookaheadDev la
         }
         __syncthreads();
         if (j0 + kLC < m) fetch(j0 + kLC);
-        const int lim = min(kLC, m - j0);
-        for (int jj = 0; jj < lim; ++jj) {
+        // exact: rows with y_i == 0 take T_ij itself (a select per element).
+        // fast: T_ij - y_i X_kj for every row. With y_i = +-0 and X_kj finite
+        // that differs from T_ij only in the sign of a zero, and a zero term
+        // never changes the chain (acc starts at +0.0 and round-to-nearest
+        // never produces -0.0 from it), so the chains are bit-identical.
+        auto step = [&](int jj, auto sel) {
             double tv[4], xv[4], bv[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -1603,8 +1618,16 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_theta(Dev d, LookaheadDev la
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
                     const double sub = dsub(tv[u], dmul(yv[u], xv[v]));
-                    acc[u][v] = dadd(acc[u][v], dmul(zrow[u] ? tv[u] : sub, bv[v]));
+                    acc[u][v] = dadd(acc[u][v], dmul(decltype(sel)::value && zrow[u] ? tv[u] : sub, bv[v]));
                 }
+        };
+        if (exact) {
+            for (int jj = 0; jj < min(kLC, m - j0); ++jj) step(jj, std::true_type{});
+        } else if (j0 + kLC <= m) {
+#pragma unroll
+            for (int jj = 0; jj < kLC; ++jj) step(jj, std::false_type{});
+        } else {
+            for (int jj = 0; jj < m - j0; ++jj) step(jj, std::false_type{});
         }
         __syncthreads();
     }

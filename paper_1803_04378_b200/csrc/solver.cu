@@ -853,12 +853,14 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     la.tl = talloc<double>(kb, st_, pool_);
     la.own_t = talloc<double>(kb, st_, pool_);
     la.tl_all = sharded_ ? talloc<double>((size_t)kb * G, st_, pool_) : nullptr;
+    la.nonfinite = talloc<int>(1, st_, pool_);
     CK(cudaMemsetAsync(la.X, 0, sizeof(double) * (size_t)kb * ldx, st_));
     if (dbg_trace_) fprintf(stderr, "[solver r%d] lookahead K=%d\n", rank_, K);
     temp_alloc_fence();
     for (int k0 = 0; k0 < K; k0 += kb) {
         la.K = std::min(kb, K - k0);
         CK(cudaMemcpyAsync(rows_d, rows.data() + k0, sizeof(int) * la.K, cudaMemcpyHostToDevice, st_));
+        CK(cudaMemsetAsync(la.nonfinite, 0, sizeof(int), st_));
         ev_chain_ = nullptr;  // the copy is not a kernel of the profile
         // fp64 flops of the batched work: pricing K x m x n_scan(shard) dot terms
         // (DMUL + DADD); theta K x mloc x m terms of (T_ij - y_i X_kj) a_j
@@ -877,7 +879,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
         CK(cudaStreamSynchronize(st_));
     }
     void* bufs[] = {rows_d, la.X, la.Wp, la.bz, la.bj, la.theta, la.score, la.part_z, la.part_j, la.part_t,
-                    la.pm, la.pm_all, la.tl, la.tl_all, la.own_t};
+                    la.pm, la.pm_all, la.tl, la.tl_all, la.own_t, la.nonfinite};
     for (void* p : bufs)
         if (p) CK(cudaFreeAsync(p, st_));
 }
