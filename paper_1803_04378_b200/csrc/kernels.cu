@@ -80,7 +80,7 @@ __device__ __forceinline__ void price_decide(const Dev& d, Ctl* c, bool budget_h
     } else {
         c->q = j == INT_MAX ? -1 : j;
         c->d = j == INT_MAX ? 0.0 : z;
-        if (j == INT_MAX || (z <= d.opt_tol && !d.dbg)) c->status = ST_OPTIMAL;
+        if (j == INT_MAX || (z <= d.opt_tol && !(d.dbg & 15))) c->status = ST_OPTIMAL;
     }
 }
 
@@ -1573,7 +1573,9 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_theta(Dev d, LookaheadDev la
     bool zrow[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) zrow[u] = yv[u] == 0.0;
-    const bool exact = *la.nonfinite != 0;  // some X_kj is inf/NaN: keep the select
+    // some X_kj is inf/NaN: keep the select (dbg bit 4 forces it: a parity check
+    // of that path, tests/test_gpu_parity.py)
+    const bool exact = *la.nonfinite != 0 || (d.dbg & 16) != 0;
     double rt[4], rx[4], rb[4];
     auto fetch = [&](int j0) {
 #pragma unroll

@@ -98,7 +98,8 @@ class SolverConfig:
     nccl_id: bytes = b""
     nccl_single: bool = False  # run the NCCL exchange path even for world_size 1 (testing)
     peer: Optional["PeerHeap"] = None  # P2P transport (NVLink stores + flags) instead of NCCL
-    experiment: int = 0        # kernel experiment knobs (results are NOT valid); 0 = production
+    experiment: int = 0        # kernel experiment knobs (bits 0-3: results NOT valid; bit 4:
+                               # exact-select lookahead, valid); 0 = production
 
     def _c(self) -> L.Config:
         c = L.Config()

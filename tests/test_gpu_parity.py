@@ -72,6 +72,23 @@ def test_golden_trace_parity(name):
     assert np.array_equal(_bits(rep.x), _bits(g.x)), name
 
 
+TIE_NAMES = [n for n in NAMES if "_f2_" in n or n.startswith("beale")]
+
+
+@pytest.mark.parametrize("name", TIE_NAMES)
+def test_lookahead_exact_select_path(name):
+    """The lookahead's theta kernel drops the y_i == 0 select when every X_kj
+    is finite (a zero-sign-only difference). Forcing the select
+    path (experiment bit 16) must give the same pivots, bit for bit."""
+    P = _P()
+    g = Golden(name)
+    rep, tr = _solve_traced(_golden_lp(g), max_iter=g.max_iter, pivot_tol=g.pivot_tol,
+                            anticycle=P.Anticycle(g.anticycle), experiment=16)
+    assert int(rep.status) == g.status
+    _assert_trace(tr, g.trace[: g.trace_len], name)
+    assert np.array_equal(_bits(rep.x), _bits(g.x)), name
+
+
 @pytest.mark.parametrize("rows,cols,form,seed", [
     (48, 80, 0, 11), (48, 80, 1, 12), (48, 80, 2, 13), (150, 300, 0, 21), (150, 300, 2, 22),
     (333, 500, 1, 31), (300, 450, 2, 32), (513, 700, 0, 33), (1, 3, 0, 4), (2, 2, 1, 5),
