@@ -1,7 +1,6 @@
 """k_price / k_update rates with the experiment bits: 0 = production, 1 = no
 math in k_price (memory-only), 2 = no loads in k_price (compute-only), 4 = no
-update/FTRAN math, 8 = no update loads, 64 = no FTRAN math, 128 = no update
-math. Timing only (bits != 0 give invalid
+update/FTRAN math, 8 = no update loads. Timing only (bits != 0 give invalid
 pivots). Usage: PYTHONPATH=. python tools/dbg/price_rate_probe.py [m] [bits,bits,...]"""
 import sys
 import paper_1803_04378_b200 as P
