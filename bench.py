@@ -90,8 +90,9 @@ class ClockSampler:
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device: int):
+    def __init__(self, device: int, interval: float = 0.2):
         self.device = device
+        self.interval = interval
         self.rows = []
         self._stop = threading.Event()
         self._t = None
@@ -107,7 +108,7 @@ class ClockSampler:
                         self.rows.append([v.strip() for v in line.split(",")])
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(self.interval)
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
         return self
@@ -397,6 +398,8 @@ def run_ours(args, cfg):
     lp_pinned = make_lp(cfg, pinned=True)
     cfg2 = solver_config(P, args, world, rank, local, max_iter=args.e2e_max_iter)
     barrier(world)
+    # (no nvidia-smi sampling here: each call stalls the host side of the
+    # create/upload it overlaps, ~0.7 s over this region in a measured A/B)
     t0 = time.perf_counter()
     s2 = P.SimplexSolver(lp_pinned, cfg2)
     rep2 = s2.solve()
@@ -455,7 +458,7 @@ def run_ours(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=1000)  # ~0.34 s timed at C3: several clock samples
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
