@@ -226,7 +226,9 @@ void launch_pivot_row(const Dev& d, cudaStream_t st);         // world > 1
 void launch_update(const Dev& d, cudaStream_t st);
 void launch_ratio(const Dev& d, cudaStream_t st);
 void launch_pivot(const Dev& d, cudaStream_t st);
-void launch_transpose(const double* A_rm, double* A_cm, int m, int n, long long ld, cudaStream_t st);
+// also sets *nonfinite (device int) to 1 when some A entry is inf/NaN
+void launch_transpose(const double* A_rm, double* A_cm, int m, int n, long long ld, int* nonfinite,
+                      cudaStream_t st);
 void launch_build_nb_from(const Dev& d, const double* A_rm, int n_scan, cudaStream_t st);
 // drive-out: scan this shard's slots against g = B^-1 row (m doubles) -> ctl.found
 // (local min j); then, after the cross-shard min, the entering reduced cost.

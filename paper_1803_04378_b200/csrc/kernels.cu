@@ -135,14 +135,23 @@ __global__ void k_init_tableau(Dev d, const double* __restrict__ b) {
 }
 
 // A_cm[j*ld + i] = A_rm[i*n + j]  (tiled transpose through shared memory)
+// Also flags a non-finite coefficient (*nonfinite = 1): the pricing argmax
+// equals the reference's first-scanned-column rule only for finite reduced
+// costs, so such inputs are rejected.
 __global__ void k_transpose(const double* __restrict__ A_rm, double* __restrict__ A_cm, int m,
-                            int n, long long ld) {
+                            int n, long long ld, int* nonfinite) {
     __shared__ double tile[32][33];
     const int j0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+    bool bad = false;
     for (int k = threadIdx.y; k < 32; k += blockDim.y) {
         const int i = i0 + k, j = j0 + threadIdx.x;
-        if (i < m && j < n) tile[k][threadIdx.x] = A_rm[(size_t)i * n + j];
+        if (i < m && j < n) {
+            const double v = A_rm[(size_t)i * n + j];
+            bad |= !isfinite(v);
+            tile[k][threadIdx.x] = v;
+        }
     }
+    if (bad) atomicOr(nonfinite, 1);
     __syncthreads();
     for (int k = threadIdx.y; k < 32; k += blockDim.y) {
         const int j = j0 + k, i = i0 + threadIdx.x;
@@ -1729,9 +1738,10 @@ void launch_init_tableau(const Dev& d, const double* b, cudaStream_t st) {
     k_init_tableau<<<(d.mloc + 255) / 256, 256, 0, st>>>(d, b);
 }
 
-void launch_transpose(const double* A_rm, double* A_cm, int m, int n, long long ld, cudaStream_t st) {
+void launch_transpose(const double* A_rm, double* A_cm, int m, int n, long long ld, int* nonfinite,
+                      cudaStream_t st) {
     dim3 grid((n + 31) / 32, (m + 31) / 32);
-    k_transpose<<<grid, dim3(32, 8), 0, st>>>(A_rm, A_cm, m, n, ld);
+    k_transpose<<<grid, dim3(32, 8), 0, st>>>(A_rm, A_cm, m, n, ld, nonfinite);
 }
 
 void launch_build_nb_from(const Dev& d, const double* A_rm, int n_scan, cudaStream_t st) {

@@ -346,7 +346,11 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
         if (basic_[i] < 0) ++n_art_;
     n_work_ = n + n_art_;
     std::vector<double> cost(2 * (size_t)n_work_, 0.0);  // [c_phase1 | c_true]
-    for (int j = 0; j < n; ++j) cost[n_work_ + j] = lp.c[j];
+    for (int j = 0; j < n; ++j) {
+        if (!std::isfinite(lp.c[j]))  // see the A check below
+            throw Error(LPSG_INVALID_ARGUMENT, "c holds an inf/NaN cost: reduced costs would not be finite");
+        cost[n_work_ + j] = lp.c[j];
+    }
     {
         int next = n;
         for (int i = 0; i < m; ++i) {
@@ -452,9 +456,11 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     n_scan_host_ = n_scan;
     {
         double* A_rm = dalloc<double>((size_t)m * n);
+        int* nonfinite = reinterpret_cast<int*>(scratch_);
+        CK(cudaMemsetAsync(nonfinite, 0, sizeof(int), st_));
         CK(cudaMemcpyAsync(A_rm, lp.A, sizeof(double) * (size_t)m * n, cudaMemcpyHostToDevice, st_));
         CK(cudaMemsetAsync(A_cm, 0, sizeof(double) * ((size_t)n * d_.ld_cm + 64), st_));
-        launch_transpose(A_rm, A_cm, m, n, d_.ld_cm, st_);
+        launch_transpose(A_rm, A_cm, m, n, d_.ld_cm, nonfinite, st_);
         CK(cudaMemsetAsync(d_.slot2col, 0xff, sizeof(int) * d_.ld_nb, st_));
         if (n_scan)
             CK(cudaMemcpyAsync(d_.slot2col, slot2col.data(), sizeof(int) * n_scan, cudaMemcpyHostToDevice, st_));
@@ -462,8 +468,14 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
         CK(cudaMemsetAsync(d_.A_nb, 0, sizeof(double) * ((size_t)m * d_.ld_nb + 64), st_));
         launch_build_nb_from(d_, A_rm, n_scan, st_);
         CK(cudaGetLastError());
+        int bad = 0;
+        CK(cudaMemcpyAsync(&bad, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, st_));
         CK(cudaStreamSynchronize(st_));
         CK(cudaFree(A_rm));
+        if (bad)
+            throw Error(LPSG_INVALID_ARGUMENT,
+                        "A holds an inf/NaN coefficient: reduced costs would not be finite, and the "
+                        "reference's first-scanned-column pricing rule is not reproduced for them");
     }
     CK(cudaMemcpyAsync(d_.basic, basic_.data(), sizeof(int) * m, cudaMemcpyHostToDevice, st_));
     CK(cudaMemsetAsync(d_.frozen, 0, m, st_));

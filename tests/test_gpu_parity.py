@@ -211,3 +211,48 @@ def test_lookahead_scores_match_port_select(port):
         sc = s.lookahead_scores([0, 1], p.entering)
         assert sc.shape == (2,)
         assert s.select_leaving([0, 1], p.entering) in (0, 1)
+
+
+def test_non_finite_costs_or_coefficients_are_rejected():
+    """The (max z, min j) pricing reduction equals the reference's strict '>'
+    scan only for finite reduced costs, so inf/NaN in
+    A or c is refused at create with LPSG_INVALID_ARGUMENT instead of silently
+    diverging."""
+    P = _P()
+    A = np.array([[1.0, 2.0, 1.0, 0.0], [3.0, 1.0, 0.0, 1.0]])
+    b = np.array([4.0, 5.0])
+    c = np.array([-1.0, -1.0, 0.0, 0.0])
+    ck = np.array([0, 0, 1, 1], np.uint8)
+    for bad_A, bad_c in ((np.nan, None), (np.inf, None), (None, np.inf), (None, np.nan)):
+        A2, c2 = A.copy(), c.copy()
+        if bad_A is not None:
+            A2[1, 0] = bad_A
+        if bad_c is not None:
+            c2[1] = bad_c
+        with pytest.raises(P.Error, match="inf/NaN"):
+            P.two_phase_solve(P.StandardFormLP(2, 4, A2, b, c2, ck))
+
+
+def test_infinite_rhs_matches_port(port):
+    """A non-finite right-hand side only reaches b_bar and the ratio test,
+    whose std::min / <= comparisons the kernels reproduce: accepted, and the
+    pivots match the CPU restatement."""
+    P = _P()
+    from oracle.oracle import LP, make_config
+    A = np.array([[1.0, 2.0, 1.0, 0.0, 0.0], [3.0, 1.0, 0.0, 1.0, 0.0], [1.0, 1.0, 0.0, 0.0, 1.0]])
+    b = np.array([4.0, np.inf, 3.0])
+    c = np.array([-1.0, -2.0, 0.0, 0.0, 0.0])
+    ck = np.array([0, 0, 1, 1, 1], np.uint8)
+    ref = port.solve(LP(3, 5, A, b, c, ck, 1.0, 0.0, "inf_rhs"), make_config())
+    rep, tr = _solve_traced(P.StandardFormLP(3, 5, A, b, c, ck))
+    assert int(rep.status) == ref.status
+    want = ref.trace[: ref.trace_len]
+    assert len(tr) == len(want)
+    for f in ("iteration", "phase", "row", "leaving", "entering"):
+        assert np.array_equal(tr[f], want[f]), f
+    # the objective is inf - inf here: NaN on both sides (a NaN's sign bit is
+    # not specified by IEEE and differs between x86 and the GPU)
+    o, w = tr["objective"], want["objective"]
+    assert np.array_equal(np.isnan(o), np.isnan(w))
+    assert np.array_equal(_bits(o[~np.isnan(o)]), _bits(w[~np.isnan(w)]))
+    assert np.array_equal(_bits(rep.x), _bits(ref.x))
