@@ -256,3 +256,11 @@ def test_infinite_rhs_matches_port(port):
     assert np.array_equal(np.isnan(o), np.isnan(w))
     assert np.array_equal(_bits(o[~np.isnan(o)]), _bits(w[~np.isnan(w)]))
     assert np.array_equal(_bits(rep.x), _bits(ref.x))
+
+
+def test_fp64_peak_probe():
+    """lpsg_fp64_peak (the lookahead's roofline denominator) measures the fp64
+    SIMT pipe: B200 does ~18.5 TFLOP/s counting DMUL and DADD as one flop each."""
+    P = _P()
+    v = P.fp64_peak(0)
+    assert 5.0 < v < 40.0, v
