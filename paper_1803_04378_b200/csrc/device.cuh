@@ -149,6 +149,7 @@ struct Dev {
     const CUtensorMap* tm_T;   // 2D TMA descriptor of T, box {h rows, C columns}
     const CUtensorMap* tm_nb;  // 2D TMA descriptors of A_nb, box {wbx slots, price_rows(wbx) rows}
     int price_nwc, price_S, price_smem, price_threads;
+    int price_spt;             // slots per consumer thread: 1 (one chain per lane) or 2 (pairs)
     int dbg;               // experiment knobs (cfg.reserved[2]); 0 in production
     int pdl;               // launch the pivot chain with programmatic dependent launch
     int upd_tma_store;     // k_update writes tiles back with TMA stores (else per-warp STG)

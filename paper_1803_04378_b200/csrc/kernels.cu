@@ -324,6 +324,40 @@ __device__ __forceinline__ void chain_group(double& acc0, double& acc1, const do
     }
 }
 
+// one slot: 8 rows (row pitch in doubles) and the matching 8 W values
+__device__ __forceinline__ void lds_group1(const double* col, int pitch, const double* ws, double (&a)[8],
+                                           double2 (&w)[4]) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a[u]) : "r"(su32(col + u * pitch)));
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(w[u].x), "=d"(w[u].y) : "r"(su32(ws + 2 * u)));
+}
+
+__device__ __forceinline__ void pin1(double& a) { asm volatile("" : "+d"(a)); }
+
+// products of one group (independent of the chain) ...
+__device__ __forceinline__ void mul_group1(double (&p)[8], const double (&a)[8], const double2 (&w)[4]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        p[2 * u] = dmul(w[u].x, a[2 * u]);
+        p[2 * u + 1] = dmul(w[u].y, a[2 * u + 1]);
+    }
+}
+
+// ... and its 8 dependent adds, in row order
+__device__ __forceinline__ void add_group1(double& acc, const double (&p)[8]) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = dadd(acc, p[u]);
+}
+
+// pins the 8 products: the adds after it cannot absorb the multiplies before it
+__device__ __forceinline__ void pin8(double (&p)[8]) {
+    asm volatile("" : "+d"(p[0]), "+d"(p[1]), "+d"(p[2]), "+d"(p[3]), "+d"(p[4]), "+d"(p[5]), "+d"(p[6]),
+                 "+d"(p[7]));
+}
+
 // ---------------------------------------------------------------- price ---
 // solver.cpp:79-129 (+ the loop-top budget check, solver.cpp:281).
 // One CTA per SM; CTA b owns the contiguous slot range [b*w, b*w + w) of the
@@ -390,6 +424,64 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
                     }
                     if (++st == S) { st = 0; ph ^= 1; }
                 }
+            }
+        } else if (warp < nwc && d.price_spt == 1) {
+            // one slot per consumer lane, the CTA's slots split evenly over the
+            // nwc consumer warps: a warp then issues 2 fp64 instructions per row
+            // instead of 4 (one warp issues an fp64 instruction per ~3 cycles:
+            // one chain per lane runs at 8-11 cycles a row, two at 16-19). That
+            // matters where the chains, not the stream, bound the kernel: few
+            // slots per CTA (sharded pricing, small n).
+            const int spw = (ns + nwc - 1) / nwc;
+            const int s = warp * spw + lane;
+            const bool act = lane < spw && s < ns;
+            const int wbx = g.wbx;
+            const int q = s / wbx, tq = s - q * wbx;
+            double acc = 0.0;
+            int st = 0;
+            uint32_t ph = 0;
+            for (int k = 0; k < nst; ++k) {
+                mbar_wait(&full[st], ph);
+                const int nr = min(R, m - k * R);
+                const double* sb = reinterpret_cast<const double*>(smem + (size_t)st * stage_stride);
+                const double* ws = sb + (size_t)R * w;
+                if (act && !(d.dbg & 1)) {
+                    const double* col = sb + q * wbx * R + tq;
+                    const int ng = nr >> 3;
+                    // two-deep pipeline: group g+1's loads and products are in
+                    // flight while group g's adds run
+                    double a0[8], a1[8], p0[8], p1[8];
+                    double2 w0[4], w1[4];
+                    if (ng > 0) {
+                        lds_group1(col, wbx, ws, a0, w0);
+                        mul_group1(p0, a0, w0);
+                    }
+                    int gi = 0;
+                    for (; gi + 2 <= ng; gi += 2) {
+                        lds_group1(col + (gi + 1) * 8 * wbx, wbx, ws + (gi + 1) * 8, a1, w1);
+                        mul_group1(p1, a1, w1);
+                        pin8(p1);
+                        add_group1(acc, p0);
+                        pin1(acc);
+                        if (gi + 2 < ng) {
+                            lds_group1(col + (gi + 2) * 8 * wbx, wbx, ws + (gi + 2) * 8, a0, w0);
+                            mul_group1(p0, a0, w0);
+                            pin8(p0);
+                        }
+                        add_group1(acc, p1);
+                        pin1(acc);
+                    }
+                    if (gi < ng) add_group1(acc, p0);
+                    for (int rr = ng * 8; rr < nr; ++rr) acc = dadd(acc, dmul(ws[rr], col[rr * wbx]));
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[st]);
+                if (++st == S) { st = 0; ph ^= 1; }
+            }
+            if (act) {
+                const int j = d.slot2col[s0 + s];
+                bz = dsub(acc, cost[j]);
+                bj = j;
             }
         } else if (warp < nwc) {
             // consumer thread t owns the adjacent slot pair (2t, 2t+1): one
@@ -1815,7 +1907,16 @@ void configure_kernels(Dev& d) {
     const PriceGeom gm = price_geom(ncols_local, G);
     d.pivot_grid = std::max(1, std::min(2 * G, (d.m + 1 + 255) / 256));
     d.price_grid = G;
-    d.price_nwc = (gm.w + 63) / 64;  // consumer threads own slot pairs
+    // one slot per consumer lane while 11 consumer warps cover the widest CTA
+    // range, spread over at least min(4, w/8) warps (all four SM sub-partitions);
+    // wider ranges (n_total > ~50k per GPU) use slot pairs
+    if (gm.w <= 11 * 32 && !getenv("LPSG_PRICE_PAIRS")) {  // env: A/B experiments
+        d.price_spt = 1;
+        d.price_nwc = std::max((gm.w + 31) / 32, std::min(4, (gm.w + 7) / 8));
+    } else {
+        d.price_spt = 2;
+        d.price_nwc = (gm.w + 63) / 64;  // consumer threads own slot pairs
+    }
     d.price_threads = (d.price_nwc + 1) * 32;
     d.price_stage_bytes = 0;
     for (int n = 1; n <= ncols_local; n = (n < 64 ? n + 1 : n + n / 64)) {
