@@ -808,21 +808,34 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                 if (m - j0 < C) f_bbar = tile[(m - j0) * h + t];  // updated b_bar_i (column m)
                 const double* as = tile + tile_el + C;
                 const double* col = tile + t;
-                int jj = 0;
-                for (; jj + 8 <= nf; jj += 8) {
-                    double tv[8], av[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) tv[u] = col[(jj + u) * h];
-#pragma unroll
-                    for (int u = 0; u < 8; u += 2) {
-                        const double2 a2 = *reinterpret_cast<const double2*>(as + jj + u);
-                        av[u] = a2.x;
-                        av[u + 1] = a2.y;
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) acc = dadd(acc, dmul(tv[u], av[u]));
+                // as in k_price's narrow path: group g+1's loads and products are
+                // issued before group g's 8 dependent adds, so the chain pays
+                // only the DADD latency (the chain bounds this kernel when the
+                // stream is short: small m, or per GPU when sharded)
+                const int ng = nf >> 3;
+                double a0[8], a1[8], p0[8], p1[8];
+                double2 w0[4], w1[4];
+                if (ng > 0) {
+                    lds_group1(col, h, as, a0, w0);
+                    mul_group1(p0, a0, w0);
                 }
-                for (; jj < nf; ++jj) acc = dadd(acc, dmul(col[jj * h], as[jj]));
+                int gi = 0;
+                for (; gi + 2 <= ng; gi += 2) {
+                    lds_group1(col + (gi + 1) * 8 * h, h, as + (gi + 1) * 8, a1, w1);
+                    mul_group1(p1, a1, w1);
+                    pin8(p1);
+                    add_group1(acc, p0);
+                    pin1(acc);
+                    if (gi + 2 < ng) {
+                        lds_group1(col + (gi + 2) * 8 * h, h, as + (gi + 2) * 8, a0, w0);
+                        mul_group1(p0, a0, w0);
+                        pin8(p0);
+                    }
+                    add_group1(acc, p1);
+                    pin1(acc);
+                }
+                if (gi < ng) add_group1(acc, p0);
+                for (int jj = ng * 8; jj < nf; ++jj) acc = dadd(acc, dmul(col[jj * h], as[jj]));
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
