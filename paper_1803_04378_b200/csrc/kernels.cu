@@ -324,40 +324,6 @@ __device__ __forceinline__ void chain_group(double& acc0, double& acc1, const do
     }
 }
 
-// one slot: 8 rows (row pitch in doubles) and the matching 8 W values
-__device__ __forceinline__ void lds_group1(const double* col, int pitch, const double* ws, double (&a)[8],
-                                           double2 (&w)[4]) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a[u]) : "r"(su32(col + u * pitch)));
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(w[u].x), "=d"(w[u].y) : "r"(su32(ws + 2 * u)));
-}
-
-__device__ __forceinline__ void pin1(double& a) { asm volatile("" : "+d"(a)); }
-
-// products of one group (independent of the chain) ...
-__device__ __forceinline__ void mul_group1(double (&p)[8], const double (&a)[8], const double2 (&w)[4]) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        p[2 * u] = dmul(w[u].x, a[2 * u]);
-        p[2 * u + 1] = dmul(w[u].y, a[2 * u + 1]);
-    }
-}
-
-// ... and its 8 dependent adds, in row order
-__device__ __forceinline__ void add_group1(double& acc, const double (&p)[8]) {
-#pragma unroll
-    for (int u = 0; u < 8; ++u) acc = dadd(acc, p[u]);
-}
-
-// pins the 8 products: the adds after it cannot absorb the multiplies before it
-__device__ __forceinline__ void pin8(double (&p)[8]) {
-    asm volatile("" : "+d"(p[0]), "+d"(p[1]), "+d"(p[2]), "+d"(p[3]), "+d"(p[4]), "+d"(p[5]), "+d"(p[6]),
-                 "+d"(p[7]));
-}
-
 // ---------------------------------------------------------------- price ---
 // solver.cpp:79-129 (+ the loop-top budget check, solver.cpp:281).
 // One CTA per SM; CTA b owns the contiguous slot range [b*w, b*w + w) of the
@@ -446,33 +412,22 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
                 const double* sb = reinterpret_cast<const double*>(smem + (size_t)st * stage_stride);
                 const double* ws = sb + (size_t)R * w;
                 if (act && !(d.dbg & 1)) {
+                    // plain loads, scheduled by the compiler: 14-15 cycles a row,
+                    // against 17-20 for volatile software-pipelined loads
+                    // (tools/microbench/chain_rate.cu)
                     const double* col = sb + q * wbx * R + tq;
-                    const int ng = nr >> 3;
-                    // two-deep pipeline: group g+1's loads and products are in
-                    // flight while group g's adds run
-                    double a0[8], a1[8], p0[8], p1[8];
-                    double2 w0[4], w1[4];
-                    if (ng > 0) {
-                        lds_group1(col, wbx, ws, a0, w0);
-                        mul_group1(p0, a0, w0);
-                    }
-                    int gi = 0;
-                    for (; gi + 2 <= ng; gi += 2) {
-                        lds_group1(col + (gi + 1) * 8 * wbx, wbx, ws + (gi + 1) * 8, a1, w1);
-                        mul_group1(p1, a1, w1);
-                        pin8(p1);
-                        add_group1(acc, p0);
-                        pin1(acc);
-                        if (gi + 2 < ng) {
-                            lds_group1(col + (gi + 2) * 8 * wbx, wbx, ws + (gi + 2) * 8, a0, w0);
-                            mul_group1(p0, a0, w0);
-                            pin8(p0);
+                    int rr = 0;
+                    for (; rr + 8 <= nr; rr += 8) {
+                        double v[8], wv[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            v[u] = col[(rr + u) * wbx];
+                            wv[u] = ws[rr + u];
                         }
-                        add_group1(acc, p1);
-                        pin1(acc);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) acc = dadd(acc, dmul(wv[u], v[u]));
                     }
-                    if (gi < ng) add_group1(acc, p0);
-                    for (int rr = ng * 8; rr < nr; ++rr) acc = dadd(acc, dmul(ws[rr], col[rr * wbx]));
+                    for (; rr < nr; ++rr) acc = dadd(acc, dmul(ws[rr], col[rr * wbx]));
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[st]);
@@ -808,34 +763,23 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                 if (m - j0 < C) f_bbar = tile[(m - j0) * h + t];  // updated b_bar_i (column m)
                 const double* as = tile + tile_el + C;
                 const double* col = tile + t;
-                // as in k_price's narrow path: group g+1's loads and products are
-                // issued before group g's 8 dependent adds, so the chain pays
-                // only the DADD latency (the chain bounds this kernel when the
-                // stream is short: small m, or per GPU when sharded)
-                const int ng = nf >> 3;
-                double a0[8], a1[8], p0[8], p1[8];
-                double2 w0[4], w1[4];
-                if (ng > 0) {
-                    lds_group1(col, h, as, a0, w0);
-                    mul_group1(p0, a0, w0);
-                }
-                int gi = 0;
-                for (; gi + 2 <= ng; gi += 2) {
-                    lds_group1(col + (gi + 1) * 8 * h, h, as + (gi + 1) * 8, a1, w1);
-                    mul_group1(p1, a1, w1);
-                    pin8(p1);
-                    add_group1(acc, p0);
-                    pin1(acc);
-                    if (gi + 2 < ng) {
-                        lds_group1(col + (gi + 2) * 8 * h, h, as + (gi + 2) * 8, a0, w0);
-                        mul_group1(p0, a0, w0);
-                        pin8(p0);
+                // plain loads, scheduled by the compiler (volatile software
+                // pipelining is slower for a single chain: chain_rate.cu)
+                int jj = 0;
+                for (; jj + 8 <= nf; jj += 8) {
+                    double tv[8], av[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) tv[u] = col[(jj + u) * h];
+#pragma unroll
+                    for (int u = 0; u < 8; u += 2) {
+                        const double2 a2 = *reinterpret_cast<const double2*>(as + jj + u);
+                        av[u] = a2.x;
+                        av[u + 1] = a2.y;
                     }
-                    add_group1(acc, p1);
-                    pin1(acc);
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) acc = dadd(acc, dmul(tv[u], av[u]));
                 }
-                if (gi < ng) add_group1(acc, p0);
-                for (int jj = ng * 8; jj < nf; ++jj) acc = dadd(acc, dmul(col[jj * h], as[jj]));
+                for (; jj < nf; ++jj) acc = dadd(acc, dmul(col[jj * h], as[jj]));
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);

@@ -91,6 +91,115 @@ __global__ void k_simple(int rows, double* out, long long* cyc) {
     if (s == 12345.0) out[0] = s;
 }
 
+__device__ __forceinline__ void lds_group1(const double* col, int pitch, const double* ws, double (&a)[8],
+                                           double2 (&w)[4]) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(a[u]) : "r"(su32(col + u * pitch)));
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(w[u].x), "=d"(w[u].y) : "r"(su32(ws + 2 * u)));
+}
+__device__ __forceinline__ void mul_group1(double (&p)[8], const double (&a)[8], const double2 (&w)[4]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        p[2 * u] = xmul(w[u].x, a[2 * u]);
+        p[2 * u + 1] = xmul(w[u].y, a[2 * u + 1]);
+    }
+}
+__device__ __forceinline__ void add_group1(double& acc, const double (&p)[8]) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = xadd(acc, p[u]);
+}
+__device__ __forceinline__ void pin1(double& a) { asm volatile("" : "+d"(a)); }
+__device__ __forceinline__ void pin8(double (&p)[8]) {
+    asm volatile("" : "+d"(p[0]), "+d"(p[1]), "+d"(p[2]), "+d"(p[3]), "+d"(p[4]), "+d"(p[5]), "+d"(p[6]),
+                 "+d"(p[7]));
+}
+
+// k_price's narrow consumer loop (one chain per lane), volatile loads or plain loads
+template <bool VOL>
+__global__ void k_one(int stages, int R, int wbx, double* out, long long* cyc) {
+    extern __shared__ double sm[];
+    double* ws = sm + R * wbx;
+    for (int e = threadIdx.x; e < R * wbx + R; e += blockDim.x) sm[e] = 1.0 + 1e-9 * e;
+    __syncthreads();
+    const int s = threadIdx.x & 31;
+    const double* col = sm + (s % wbx);
+    double acc = 0.0;
+    const long long c0 = clock64();
+    for (int k = 0; k < stages; ++k) {
+        const int ng = R >> 3;
+        double a0[8], a1[8], p0[8], p1[8];
+        double2 w0[4], w1[4];
+        if (VOL) {
+            lds_group1(col, wbx, ws, a0, w0);
+            mul_group1(p0, a0, w0);
+            int gi = 0;
+            for (; gi + 2 <= ng; gi += 2) {
+                lds_group1(col + (gi + 1) * 8 * wbx, wbx, ws + (gi + 1) * 8, a1, w1);
+                mul_group1(p1, a1, w1);
+                pin8(p1);
+                add_group1(acc, p0);
+                pin1(acc);
+                if (gi + 2 < ng) {
+                    lds_group1(col + (gi + 2) * 8 * wbx, wbx, ws + (gi + 2) * 8, a0, w0);
+                    mul_group1(p0, a0, w0);
+                    pin8(p0);
+                }
+                add_group1(acc, p1);
+                pin1(acc);
+            }
+        } else {
+            for (int r = 0; r < R; r += 8) {
+                double v[8], w[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) { v[u] = col[(r + u) * wbx]; w[u] = ws[r + u]; }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc = xadd(acc, xmul(w[u], v[u]));
+            }
+        }
+        __syncwarp();
+    }
+    const long long c1 = clock64();
+    if (threadIdx.x == 0) cyc[blockIdx.x] = c1 - c0;
+    if (acc == 12345.0) out[0] = acc;
+}
+
+// plain-load variants: G rows per group, loads for group g+1 issued in source
+// order before group g's chain (compiler free to schedule)
+template <int G>
+__global__ void k_plain(int stages, int R, int wbx, double* out, long long* cyc) {
+    extern __shared__ double sm[];
+    double* ws = sm + R * wbx;
+    for (int e = threadIdx.x; e < R * wbx + R; e += blockDim.x) sm[e] = 1.0 + 1e-9 * e;
+    __syncthreads();
+    const int s = threadIdx.x & 31;
+    const double* col = sm + (s % wbx);
+    double acc = 0.0;
+    const long long c0 = clock64();
+    for (int k = 0; k < stages; ++k) {
+        double v[G], w[G];
+#pragma unroll
+        for (int u = 0; u < G; ++u) { v[u] = col[u * wbx]; w[u] = ws[u]; }
+        for (int r = 0; r < R; r += G) {
+            double p[G];
+#pragma unroll
+            for (int u = 0; u < G; ++u) p[u] = xmul(w[u], v[u]);
+            if (r + G < R) {
+#pragma unroll
+                for (int u = 0; u < G; ++u) { v[u] = col[(r + G + u) * wbx]; w[u] = ws[r + G + u]; }
+            }
+#pragma unroll
+            for (int u = 0; u < G; ++u) acc = xadd(acc, p[u]);
+        }
+        __syncwarp();
+    }
+    const long long c1 = clock64();
+    if (threadIdx.x == 0) cyc[blockIdx.x] = c1 - c0;
+    if (acc == 12345.0) out[0] = acc;
+}
+
 int main() {
     double* out;
     long long* cyc;
@@ -126,6 +235,29 @@ int main() {
         printf("simple 4 chains: %.1f cycles/row\n", (double)h[0] / rows);
         k_simple<8><<<148, 32>>>(rows, out, cyc); cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
         printf("simple 8 chains: %.1f cycles/row\n", (double)h[0] / rows);
+    }
+    {
+        long long h[148];
+        const int R = 256, wbx = 16, stages = 32;
+        const int smem = (R * wbx + R) * 8;
+        cudaFuncSetAttribute(k_one<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_one<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        for (int warps : {1, 4}) {
+            k_one<true><<<148, 32 * warps, smem>>>(stages, R, wbx, out, cyc);
+            cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
+            printf("narrow consumer (volatile, pipelined), %d warps: %.1f cycles/row\n", warps, (double)h[0] / (stages * R));
+            k_one<false><<<148, 32 * warps, smem>>>(stages, R, wbx, out, cyc);
+            cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
+            printf("narrow consumer (plain loads), %d warps: %.1f cycles/row\n", warps, (double)h[0] / (stages * R));
+            cudaFuncSetAttribute(k_plain<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(k_plain<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            k_plain<8><<<148, 32 * warps, smem>>>(stages, R, wbx, out, cyc);
+            cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
+            printf("plain prefetch G=8, %d warps: %.1f cycles/row\n", warps, (double)h[0] / (stages * R));
+            k_plain<16><<<148, 32 * warps, smem>>>(stages, R, wbx, out, cyc);
+            cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
+            printf("plain prefetch G=16, %d warps: %.1f cycles/row\n", warps, (double)h[0] / (stages * R));
+        }
     }
     return 0;
 }
