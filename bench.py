@@ -74,6 +74,14 @@ def _ncu_traffic(kernel: str):
     return best
 
 
+def _sm_max_mhz() -> float:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["sm_max_mhz"])
+    except Exception:
+        return 1965.0
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -345,6 +353,18 @@ def run_ours(args, cfg):
                     "kernels": kern, "instrumented_pivots": prof_range,
                     "note": "per-kernel CUDA events on the solver stream over a second window of "
                             "K pivots (rank 0); the headline value is the un-instrumented window"}
+        # the other floor of a pivot: pricing and FTRAN are each one sequential
+        # chain of m fp64 adds per output (8-cycle DADD latency, measured), plus
+        # three kernel boundaries. Small m (C1, C2) sits on this floor, not on HBM.
+        clk_ghz = _sm_max_mhz() / 1e3
+        chain_us = 2 * (lp.m + 1) * 8 / clk_ghz / 1e3
+        hbm_us = pivot_bytes / (peak * 1e9) * 1e6
+        roofline["latency_floor"] = {
+            "chain_us_per_pivot": round(chain_us, 2), "hbm_us_per_pivot": round(hbm_us, 2),
+            "measured_us_per_pivot": round(1e6 / value, 2) if value else None,
+            "regime": "hbm" if hbm_us >= chain_us else "chain/latency",
+            "note": "chain = 2 sequential dots of m+1 DADDs at 8 cycles (pricing, FTRAN); the "
+                    "pivot cannot beat max(chain, hbm)"}
         la = {k: v for k, v in kern.items() if "tflops" in v}
         la_ms = sum(v["ms_total"] for v in la.values())
         if la and la_ms > sum(v["ms_total"] for v in hbm.values()):
