@@ -622,6 +622,59 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
     }
 }
 
+// Short row blocks (h <= 32): a column has only h/2 row pairs, so one warp
+// covers 32 / (h/2) columns per iteration (lane = column offset x row pair)
+// instead of leaving most lanes idle on one column. Same per-element
+// arithmetic as update_role.
+__device__ __forceinline__ void update_role_small(const Dev& d, unsigned char* smem, uint64_t* full,
+                                                  uint64_t* upd, size_t stage_stride, size_t tile_el,
+                                                  int nst, int S, int C, int h, int i0, int r, int U,
+                                                  bool up, int warp, int lane) {
+    const int m = d.m, mloc = d.mloc;
+    const int hp = h >> 1;                 // row pairs per column (h is even)
+    const int cpw = 32 / hp;               // columns per warp iteration
+    const int lc = lane / hp, lr = lane - lc * hp;
+    const bool act = lc < cpw;
+    const int i = i0 + 2 * lr;             // local row of this lane's pair
+    const double ny0 = (act && i < mloc && i != r) ? -d.Y[i] : 0.0;
+    const double ny1 = (act && i + 1 < mloc && i + 1 != r) ? -d.Y[i + 1] : 0.0;
+    const size_t ldT = (size_t)d.ldT;
+    const bool nomath = (d.dbg & 4) != 0;
+    const bool tstore = d.upd_tma_store != 0;
+    double2* const gbase = reinterpret_cast<double2*>(d.T + i0) + lr;
+    const int ncols = m + 1;
+    const int step = U * cpw;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int k = 0; k < nst; ++k) {
+        mbar_wait(&full[st], ph);
+        if (up && act) {
+            const int j0 = k * C, nc = min(C, ncols - j0);
+            double* tile = reinterpret_cast<double*>(smem + (size_t)st * stage_stride);
+            const double* xs = tile + tile_el;
+            for (int jj = warp * cpw + lc; jj < nc; jj += step) {
+                double2* tp = reinterpret_cast<double2*>(tile + (size_t)jj * h) + lr;
+                double2 tv = *tp;
+                if (!nomath) {
+                    const double xj = xs[jj];
+                    const double p0 = dmul(ny0, xj);
+                    const double p1 = dmul(ny1, xj);
+                    const double s0v = dadd(tv.x, p0);
+                    const double s1v = dadd(tv.y, p1);
+                    tv.x = (p0 != 0.0) ? s0v : tv.x;
+                    tv.y = (p1 != 0.0) ? s1v : tv.y;
+                    *tp = tv;
+                }
+                if (!tstore) gbase[(size_t)(j0 + jj) * (ldT / 2)] = tv;
+            }
+        }
+        if (up) fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&upd[st]);
+        if (++st == S) { st = 0; ph ^= 1; }
+    }
+}
+
 // P2P, fused: the last CTA of k_update copies this shard's RatioMsg (just
 // written to d.rmsg by its threads) into every peer's mailbox slot [rank] and
 // raises the flags. All threads of the CTA call it.
@@ -741,7 +794,9 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         // its multiplier is 0 and the skip leaves it untouched, exactly like the
         // zeroed multiplier of tiled_engine.cpp:241.
         const int nit = (h + 63) >> 6;
-        switch (nit) {
+        if (h <= 32 && !(d.dbg & 32)) {  // dbg bit 5: the one-column-per-warp path (A/B)
+            update_role_small(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, warp, lane);
+        } else switch (nit) {
             case 1: update_role<1>(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, warp, lane); break;
             case 2: update_role<2>(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, warp, lane); break;
             case 3: update_role<3>(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, warp, lane); break;
