@@ -330,9 +330,10 @@ __device__ __forceinline__ void chain_group(double& acc0, double& acc1, const do
 // row-major nonbasic matrix A_nb (w = ceil(n_scan/G) rounded up to 8, split
 // into nb TMA boxes of wbx <= 256 slots). A producer warp streams R-row tiles
 // through an S-stage ring with 2D TMA (one cp.async.bulk.tensor per box) plus a
-// 1D bulk copy of the matching W segment; consumer thread t accumulates
-// z_t = sum_i W_i * a_i,t strictly in ascending i. The grid-wide
-// (max z, min j) reduction is finished by the last CTA.
+// 1D bulk copy of the matching W segment; a consumer lane accumulates
+// z_s = sum_i W_i * a_i,s strictly in ascending i for one slot (ranges up to
+// 352 slots, spread over >= min(4, w/8) warps) or for a slot pair (wider
+// ranges). The grid-wide (max z, min j) reduction is finished by the last CTA.
 __global__ void __launch_bounds__(384) k_price(Dev d) {
     extern __shared__ __align__(1024) unsigned char smem[];
     pdl_wait();
