@@ -1900,6 +1900,7 @@ void configure_kernels(Dev& d) {
     // update + FTRAN: h rows per CTA (even, so the TMA box row is a 16-byte multiple)
     int h = (d.mloc + G - 1) / G;
     h = std::min(224, std::max(2, (h + 1) & ~1));  // <= 224 rows: 8 update + 7 FTRAN + 1 producer warps = 512 threads
+    if (const char* e = getenv("LPSG_UPD_H")) h = std::min(224, std::max(2, atoi(e) & ~1));  // shape experiments
     d.upd_h = h;
     d.update_grid = (d.mloc + h - 1) / h;
     // columns per stage: short row blocks (small m) take wide stages so the
