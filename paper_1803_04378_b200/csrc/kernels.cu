@@ -324,6 +324,13 @@ __device__ __forceinline__ void chain_group(double& acc0, double& acc1, const do
     }
 }
 
+// rows per load group of the one-chain pricing path (chain_rate.cu: 32 rows
+// 12.6-13.7 cycles/row, 8 rows 13.9-14.7)
+constexpr int kNG = 32;
+// columns per load group of the FTRAN chain in k_update (A/B: 32 vs 8 cut the
+// forced h = 8 shape 330 -> 307 us and C2's update 32.5 -> 30.6 us)
+constexpr int kFG = 32;
+
 // ---------------------------------------------------------------- price ---
 // solver.cpp:79-129 (+ the loop-top budget check, solver.cpp:281).
 // One CTA per SM; CTA b owns the contiguous slot range [b*w, b*w + w) of the
@@ -418,15 +425,15 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
                     // (tools/microbench/chain_rate.cu)
                     const double* col = sb + q * wbx * R + tq;
                     int rr = 0;
-                    for (; rr + 8 <= nr; rr += 8) {
-                        double v[8], wv[8];
+                    for (; rr + kNG <= nr; rr += kNG) {
+                        double v[kNG], wv[kNG];
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
+                        for (int u = 0; u < kNG; ++u) {
                             v[u] = col[(rr + u) * wbx];
                             wv[u] = ws[rr + u];
                         }
 #pragma unroll
-                        for (int u = 0; u < 8; ++u) acc = dadd(acc, dmul(wv[u], v[u]));
+                        for (int u = 0; u < kNG; ++u) acc = dadd(acc, dmul(wv[u], v[u]));
                     }
                     for (; rr < nr; ++rr) acc = dadd(acc, dmul(ws[rr], col[rr * wbx]));
                 }
@@ -822,18 +829,18 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                 // plain loads, scheduled by the compiler (volatile software
                 // pipelining is slower for a single chain: chain_rate.cu)
                 int jj = 0;
-                for (; jj + 8 <= nf; jj += 8) {
-                    double tv[8], av[8];
+                for (; jj + kFG <= nf; jj += kFG) {
+                    double tv[kFG], av[kFG];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) tv[u] = col[(jj + u) * h];
+                    for (int u = 0; u < kFG; ++u) tv[u] = col[(jj + u) * h];
 #pragma unroll
-                    for (int u = 0; u < 8; u += 2) {
+                    for (int u = 0; u < kFG; u += 2) {
                         const double2 a2 = *reinterpret_cast<const double2*>(as + jj + u);
                         av[u] = a2.x;
                         av[u + 1] = a2.y;
                     }
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) acc = dadd(acc, dmul(tv[u], av[u]));
+                    for (int u = 0; u < kFG; ++u) acc = dadd(acc, dmul(tv[u], av[u]));
                 }
                 for (; jj < nf; ++jj) acc = dadd(acc, dmul(col[jj * h], as[jj]));
             }
