@@ -327,9 +327,11 @@ __device__ __forceinline__ void chain_group(double& acc0, double& acc1, const do
 // rows per load group of the one-chain pricing path (chain_rate.cu: 32 rows
 // 12.6-13.7 cycles/row, 8 rows 13.9-14.7)
 constexpr int kNG = 32;
-// columns per load group of the FTRAN chain in k_update (A/B: 32 vs 8 cut the
-// forced h = 8 shape 330 -> 307 us and C2's update 32.5 -> 30.6 us)
-constexpr int kFG = 32;
+// columns per load group of the FTRAN chain in k_update. A/B: 32 cut the forced
+// h = 8 shape 330 -> 307 us and C2's update 32.5 -> 30.6 us but cost C3 (h = 56)
+// 2 us; selecting it per h (a runtime branch or a templated kernel) lost the
+// gain on both sides, so the headline's 8 stays.
+constexpr int kFG = 8;
 
 // ---------------------------------------------------------------- price ---
 // solver.cpp:79-129 (+ the loop-top budget check, solver.cpp:281).

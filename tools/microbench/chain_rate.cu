@@ -200,6 +200,32 @@ __global__ void k_plain(int stages, int R, int wbx, double* out, long long* cyc)
     if (acc == 12345.0) out[0] = acc;
 }
 
+// plain single-chain loop with G rows per group (loads then chain)
+template <int G>
+__global__ void k_plainG(int stages, int R, int wbx, double* out, long long* cyc) {
+    extern __shared__ double sm[];
+    double* ws = sm + R * wbx;
+    for (int e = threadIdx.x; e < R * wbx + R; e += blockDim.x) sm[e] = 1.0 + 1e-9 * e;
+    __syncthreads();
+    const int s = threadIdx.x & 31;
+    const double* col = sm + (s % wbx);
+    double acc = 0.0;
+    const long long c0 = clock64();
+    for (int k = 0; k < stages; ++k) {
+        for (int r = 0; r + G <= R; r += G) {
+            double v[G], w[G];
+#pragma unroll
+            for (int u = 0; u < G; ++u) { v[u] = col[(r + u) * wbx]; w[u] = ws[r + u]; }
+#pragma unroll
+            for (int u = 0; u < G; ++u) acc = xadd(acc, xmul(w[u], v[u]));
+        }
+        __syncwarp();
+    }
+    const long long c1 = clock64();
+    if (threadIdx.x == 0) cyc[blockIdx.x] = c1 - c0;
+    if (acc == 12345.0) out[0] = acc;
+}
+
 int main() {
     double* out;
     long long* cyc;
@@ -257,6 +283,18 @@ int main() {
             k_plain<16><<<148, 32 * warps, smem>>>(stages, R, wbx, out, cyc);
             cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
             printf("plain prefetch G=16, %d warps: %.1f cycles/row\n", warps, (double)h[0] / (stages * R));
+            cudaFuncSetAttribute(k_plainG<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(k_plainG<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            cudaFuncSetAttribute(k_plainG<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            k_plainG<4><<<148, 32 * warps, smem>>>(stages, R, wbx, out, cyc);
+            cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
+            printf("plainG G=4, %d warps: %.1f cycles/row\n", warps, (double)h[0] / (stages * R));
+            k_plainG<16><<<148, 32 * warps, smem>>>(stages, R, wbx, out, cyc);
+            cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
+            printf("plainG G=16, %d warps: %.1f cycles/row\n", warps, (double)h[0] / (stages * R));
+            k_plainG<32><<<148, 32 * warps, smem>>>(stages, R, wbx, out, cyc);
+            cudaMemcpy(h, cyc, 8, cudaMemcpyDeviceToHost);
+            printf("plainG G=32, %d warps: %.1f cycles/row\n", warps, (double)h[0] / (stages * R));
         }
     }
     return 0;
