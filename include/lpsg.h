@@ -54,9 +54,11 @@ typedef struct {
     const uint8_t* col_kind;
 } lpsg_problem;
 
-/* lps::SolverConfig (solver.hpp:34-45) plus device placement. memory_budget,
- * kernel and workers select simulation behaviour in the reference
- * (solver.hpp:41-43): accepted and ignored here (case_used is always in-core). */
+/* lps::SolverConfig (solver.hpp:34-45) plus device placement. `kernel` is
+ * honoured: KernelMode::cached (0, the `temp != 0` store skip) or naive (1,
+ * every element stored; tiled_engine.cpp:56-111) -- they differ only in the
+ * signs of zeros. `workers` selects CPU threading in the reference and is
+ * ignored (its results are worker-independent, solver.cpp:99-121). */
 typedef struct {
     double opt_tol;        /* 1e-7 */
     double pivot_tol;      /* 1e-9 */
@@ -64,14 +66,19 @@ typedef struct {
     double ratio_tie_tol;  /* 1e-9, relative */
     long max_iter;         /* 0 = 50 * (m + n_work)  (solver.cpp:64) */
     int anticycle;         /* 0 tabu, 1 none (solver.hpp:16) */
-    int kernel;            /* ignored (0 cached, 1 naive) */
+    int kernel;            /* 0 cached, 1 naive; anything else is LPSG_INVALID_ARGUMENT */
     int workers;           /* ignored */
     int device;            /* CUDA device ordinal, default 0 */
     int batch;             /* pivots enqueued per host check (0 = auto) */
     int use_graphs;        /* reserved (CUDA-graph capture of pivot batches) */
-    int reserved[6];       /* [0] bit 0: standalone ratio kernel (debug);
+    int reserved[6];       /* verification switches, result-identical to 0:
+                              [0] bit 0: standalone ratio kernel instead of the
+                                  fused epilogue;
                               [1] bit 0: attach the NCCL exchange path even for
-                                  world_size 1 (exercises NCCL on one GPU) */
+                                  world_size 1 (exercises NCCL on one GPU);
+                              [2] bit 4: lookahead theta' keeps the y_i == 0 select.
+                              Other bits of [2] are read only by the
+                              -DLPSG_EXPERIMENTS build (device.cuh). */
     /* Sharded solve over NCCL, one process (or thread) per GPU:
      * world_size > 1 makes this handle shard `rank`; every rank passes the same
      * problem, config and nccl_id (from lpsg_nccl_unique_id on rank 0) and must
@@ -110,6 +117,42 @@ typedef struct {
 
 typedef void (*lpsg_observer)(const lpsg_trace* pivot, void* user);
 
+/* lps::MemoryCounters (tiled_engine.hpp:56-74) counterpart. The reference
+ * counts the accesses of its simulated device arena; lpsg reports the real
+ * traffic: host<->device bytes the library moved, kernel launches, and the
+ * ALGORITHMIC HBM bytes of the pivots done (what the reference's steps must
+ * touch: pricing reads A's nonbasic columns and W, the update
+ * reads and writes [B^-1 | b_bar] once, the pivot row). */
+typedef struct {
+    uint64_t device_read_bytes;
+    uint64_t device_write_bytes;
+    uint64_t h2d_bytes;
+    uint64_t d2h_bytes;
+    uint64_t kernel_launches;
+} lpsg_memory;
+
+/* lps::IterationView (solver.hpp:21-30), handed to a view observer after
+ * every pivot: phase, cumulative iteration, T[0][m] after the pivot, the whole
+ * basis (`basic[i]` = variable of row i, num_rows entries; valid only during
+ * the callback), the pivot itself, and the counters so far. With rows enabled
+ * (lpsg_set_view_observer's with_rows) the callback may call
+ * lpsg_read_row(view->solver, i, out) to read tableau row i (row_width
+ * doubles) exactly as the reference's view.row(i) returns it; the solver then
+ * runs one pivot per device round trip, unfused. */
+typedef struct {
+    int phase;
+    long iteration;
+    double objective;
+    const int* basic;
+    int num_rows;
+    int row_width;
+    int row, leaving, entering;
+    const lpsg_memory* counters;
+    struct lpsg_solver* solver;
+} lpsg_iteration_view;
+
+typedef void (*lpsg_view_observer)(const lpsg_iteration_view* view, void* user);
+
 typedef struct lpsg_solver lpsg_solver;
 
 /* ---- library ---------------------------------------------------------- */
@@ -136,6 +179,12 @@ int lpsg_two_phase_solve(const lpsg_problem* lp, const lpsg_config* cfg, lpsg_re
 int lpsg_set_observer(lpsg_solver* s, lpsg_observer cb, void* user);
 int lpsg_keep_trace(lpsg_solver* s, int keep);
 int lpsg_get_trace(lpsg_solver* s, lpsg_trace* out, long cap, long* len);
+/* SolverConfig::observer with the full IterationView (solver.hpp:21-32). A
+ * sharded solve calls it on every rank; with rows, every rank must read the
+ * same rows in the same order (lpsg_read_row is a collective there). */
+int lpsg_set_view_observer(lpsg_solver* s, lpsg_view_observer cb, void* user, int with_rows);
+/* SolveReport::memory (solver.hpp:55). */
+int lpsg_get_memory(lpsg_solver* s, lpsg_memory* out);
 
 /* ---- multi-GPU -------------------------
  * NCCL unique id for lpsg_config.nccl_id (rank 0 creates it, the caller

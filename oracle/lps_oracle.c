@@ -292,6 +292,27 @@ static void ban(S* s, int k, int v) {
     ++s->n_ban;
 }
 
+/* Optional record of every scored tie (tests/test_gpu_parity.py compares the
+ * device lookahead's scores with these bit for bit): per tie, meta = (pivots
+ * done before it, entering, offset into rows/scores, survivor count). */
+static struct {
+    long* meta;
+    int* rows;
+    double* scores;
+    long cap_ties, cap_rows, n_ties, n_rows;
+} g_tie;
+
+void lpo_set_tie_log(long* meta, long cap_ties, int* rows, double* scores, long cap_rows) {
+    g_tie.meta = meta;
+    g_tie.rows = rows;
+    g_tie.scores = scores;
+    g_tie.cap_ties = meta ? cap_ties : 0;
+    g_tie.cap_rows = cap_rows;
+    g_tie.n_ties = g_tie.n_rows = 0;
+}
+
+long lpo_tie_log_len(void) { return g_tie.n_ties; }
+
 /* solver.cpp:215-238 */
 static int select_leaving(S* s, const int* cand, int n, int entering) {
     if (n == 1) return cand[0];
@@ -307,8 +328,20 @@ static int select_leaving(S* s, const int* cand, int n, int entering) {
     int chosen = surv[0];
     if (ns > 1) {
         double best = -1.0;
+        const int log = g_tie.n_ties < g_tie.cap_ties && g_tie.n_rows + ns <= g_tie.cap_rows;
+        if (log) {
+            long* e = g_tie.meta + 4 * g_tie.n_ties++;
+            e[0] = s->total_iter;
+            e[1] = entering;
+            e[2] = g_tie.n_rows;
+            e[3] = ns;
+        }
         for (int q = 0; q < ns; ++q) {
             const double score = lookahead_score(s, surv[q], entering);
+            if (log) {
+                g_tie.rows[g_tie.n_rows] = surv[q];
+                g_tie.scores[g_tie.n_rows++] = score;
+            }
             if (score > best) {
                 best = score;
                 chosen = surv[q];
@@ -321,7 +354,8 @@ static int select_leaving(S* s, const int* cand, int n, int entering) {
 }
 
 /* solver.cpp:240-254 + tiled_engine.cpp:230-266 (in-core) + tile_kernel
- * cached mode (tiled_engine.cpp:79-106). Returns nonzero on PivotTooSmall. */
+ * cached mode (tiled_engine.cpp:79-106) or, with cfg.kernel == 1, naive mode
+ * (61-77). Returns nonzero on PivotTooSmall. */
 static int pivot_update(S* s, int leaving_row, int entering) {
     const int m = s->m, width = s->width, rows = s->rows;
     const double y_rk = ROW(s, leaving_row + 1)[m + 1];
@@ -337,6 +371,11 @@ static int pivot_update(S* s, int leaving_row, int entering) {
     for (int i = 0; i < rows; ++i) {
         double* row = ROW(s, i);
         const double y = -s->col_buf[i];
+        if (s->cfg.kernel == 1) {
+            /* naive mode (tiled_engine.cpp:61-77): every element is stored */
+            for (int j = 0; j < width; ++j) row[j] = y * s->pivot_buf[j] + row[j];
+            continue;
+        }
         for (int j = 0; j < width; ++j) {
             const double temp = y * s->pivot_buf[j];
             if (temp != 0.0) row[j] += temp;

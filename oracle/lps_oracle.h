@@ -22,7 +22,7 @@ typedef struct {
     long max_iter;
     int anticycle; /* 0 tabu, 1 none */
     int workers;   /* accepted, ignored (results are worker-independent, solver.cpp:99-121) */
-    int kernel;    /* accepted, ignored: cached-kernel semantics (tiled_engine.cpp:79-106) */
+    int kernel;    /* 0 cached (tiled_engine.cpp:79-106), 1 naive (61-77): zero signs differ */
 } lpo_config;
 
 typedef struct {
@@ -51,6 +51,14 @@ int lpo_generate(int rows, int cols, int sparsity, uint64_t seed, int form, doub
 int lpo_solve(int m, int n_total, const double* A, const double* b, const double* c,
               const uint8_t* col_kind, const lpo_config* cfg, lpo_result* out, double* x,
               lpo_trace* trace, long trace_cap);
+
+/* Test hook: the next lpo_solve calls record every tie that select_leaving
+ * scores (solver.cpp:225-235): meta[4k..4k+3] = (pivots done before the tie,
+ * entering column, offset into rows/scores, number of scored survivors);
+ * rows/scores = the survivors and their lookahead_score values. NULL meta
+ * turns it off. Not thread-safe (test infrastructure). */
+void lpo_set_tie_log(long* meta, long cap_ties, int* rows, double* scores, long cap_rows);
+long lpo_tie_log_len(void);
 
 #ifdef __cplusplus
 }

@@ -158,6 +158,37 @@ class Ref(_Lib):
     def last_error(self) -> str:
         return self.lib.ref_last_error().decode()
 
+    def solve_window(self, lp: LP, cfg: Config, warmup: int, steps: int):
+        """bench.py's reference arm: two_phase_solve with max_iter = warmup +
+        steps and per-pivot timestamps (ref_solve_timed); returns (seconds of
+        pivots [warmup, warmup + steps), pivots done in that window, SolveOut-ish
+        dict)."""
+        L = self.lib
+        L.ref_solve_timed.restype = C.c_int
+        L.ref_solve_timed.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double), C.POINTER(C.c_uint8), C.POINTER(Config),
+                                      C.POINTER(Result), C.POINTER(C.c_double), C.c_long,
+                                      C.POINTER(C.c_double)]
+        cfg.max_iter = int(warmup + steps)
+        A = np.ascontiguousarray(lp.A, dtype=np.float64)
+        b = np.ascontiguousarray(lp.b, dtype=np.float64)
+        c = np.ascontiguousarray(lp.c, dtype=np.float64)
+        ck = np.ascontiguousarray(lp.col_kind, dtype=np.uint8)
+        stamps = np.zeros(warmup + steps + 1)
+        res = Result()
+        t_ret = C.c_double()
+        rc = L.ref_solve_timed(lp.m, lp.n_total, _ptr(A, C.c_double), _ptr(b, C.c_double),
+                               _ptr(c, C.c_double), _ptr(ck, C.c_uint8), C.byref(cfg), C.byref(res),
+                               _ptr(stamps, C.c_double), len(stamps), C.byref(t_ret))
+        if rc != 0:
+            raise RuntimeError(self.last_error())
+        n = int(res.trace_len)
+        done = max(0, min(n, warmup + steps) - warmup)
+        if done == 0:
+            return 0.0, 0, res
+        t0 = stamps[warmup - 1] if warmup > 0 else t_ret.value - res.total_seconds
+        return float(stamps[warmup + done - 1] - t0), done, res
+
     def _take(self, h, name="") -> LP:
         if not h:
             raise RuntimeError(self.last_error())
@@ -268,6 +299,27 @@ class Port(_Lib):
                                    C.POINTER(C.c_double), C.POINTER(C.c_uint8)]
         L.lpo_generated_n_total.restype = C.c_int
         L.lpo_generated_n_total.argtypes = [C.c_int, C.c_int, C.c_int]
+
+    def solve_with_ties(self, lp: LP, cfg: Config, cap_ties: int = 64, cap_rows: int = 1 << 16):
+        """solve() plus the lookahead scores of every scored tie (lpo_set_tie_log):
+        returns (SolveOut, [(pivots_before, entering, rows, scores), ...])."""
+        L = self.lib
+        L.lpo_set_tie_log.argtypes = [C.c_void_p, C.c_long, C.c_void_p, C.c_void_p, C.c_long]
+        L.lpo_tie_log_len.restype = C.c_long
+        meta = np.zeros(4 * cap_ties, np.int64)
+        rows = np.zeros(cap_rows, np.int32)
+        scores = np.zeros(cap_rows, np.float64)
+        L.lpo_set_tie_log(meta.ctypes.data, cap_ties, rows.ctypes.data, scores.ctypes.data, cap_rows)
+        try:
+            out = self.solve(lp, cfg)
+            n = L.lpo_tie_log_len()
+        finally:
+            L.lpo_set_tie_log(None, 0, None, None, 0)
+        ties = []
+        for k in range(n):
+            it, q, off, cnt = (int(v) for v in meta[4 * k: 4 * k + 4])
+            ties.append((it, q, rows[off: off + cnt].copy(), scores[off: off + cnt].copy()))
+        return out, ties
 
     def generate(self, rows: int, cols: int, seed: int = 1, form: int = 0,
                  sparsity: int = 0) -> LP:

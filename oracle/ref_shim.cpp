@@ -19,6 +19,7 @@
 //   * ref_solve        — lps::two_phase_solve (solver.cpp:394-397) with a
 //     per-pivot trace taken through SolverConfig::observer (solver.hpp:21-32,
 //     solver.cpp:264-275): the changed basis row is found by diffing `basic`.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -300,6 +301,58 @@ int ref_solve(int m, int n_total, const double* A, const double* b, const double
         g_err = e.what();
         out->status = -2;
         return 2;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        out->status = -1;
+        return 1;
+    }
+}
+
+// Same solve, for bench.py's reference arm: `stamps[k]` = steady_clock seconds
+// at the observer call of pivot k+1 (solver.cpp:264-275, right after the
+// pivot's update), and *t_return = steady_clock seconds when two_phase_solve
+// returned. A pivot window [W, W+K) is then stamps[W+K-1] - stamps[W-1]; for W
+// = 0 the start is t_return - total_seconds (solve()'s own clock start,
+// solver.cpp:332, up to the report's construction after the clock stops).
+int ref_solve_timed(int m, int n_total, const double* A, const double* b, const double* c,
+                    const std::uint8_t* col_kind, const ref_config* cfg, ref_result* out,
+                    double* stamps, long cap, double* t_return) {
+    try {
+        lps::StandardFormLP lp;
+        lp.m = m;
+        lp.n_total = n_total;
+        lp.A.assign(A, A + std::size_t(m) * n_total);
+        lp.b.assign(b, b + m);
+        lp.c.assign(c, c + n_total);
+        lp.col_kind.resize(n_total);
+        for (int j = 0; j < n_total; ++j) lp.col_kind[j] = static_cast<lps::ColKind>(col_kind[j]);
+        lps::SolverConfig sc;
+        sc.opt_tol = cfg->opt_tol;
+        sc.pivot_tol = cfg->pivot_tol;
+        sc.feas_tol = cfg->feas_tol;
+        sc.ratio_tie_tol = cfg->ratio_tie_tol;
+        sc.max_iter = cfg->max_iter;
+        sc.anticycle = cfg->anticycle == 1 ? lps::Anticycle::none : lps::Anticycle::tabu;
+        sc.workers = cfg->workers;
+        sc.kernel = cfg->kernel == 1 ? lps::KernelMode::naive : lps::KernelMode::cached;
+        long count = 0;
+        auto now = [] {
+            return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+        };
+        sc.observer = [&](const lps::IterationView&) {
+            if (count < cap) stamps[count] = now();
+            ++count;
+        };
+        const lps::SolveReport r = lps::two_phase_solve(lp, sc);
+        *t_return = now();
+        out->status = static_cast<int>(r.status);
+        out->objective = r.objective;
+        out->iterations_phase1 = r.iterations_phase1;
+        out->iterations_phase2 = r.iterations_phase2;
+        out->total_seconds = r.total_seconds;
+        out->tpi_seconds = r.tpi_seconds;
+        out->trace_len = count;
+        return 0;
     } catch (const std::exception& e) {
         g_err = e.what();
         out->status = -1;

@@ -48,6 +48,22 @@ class KernelStat(C.Structure):
 
 OBSERVER = C.CFUNCTYPE(None, C.POINTER(Trace), C.c_void_p)
 
+
+class Memory(C.Structure):
+    _fields_ = [("device_read_bytes", C.c_uint64), ("device_write_bytes", C.c_uint64),
+                ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("kernel_launches", C.c_uint64)]
+
+
+class View(C.Structure):
+    _fields_ = [("phase", C.c_int), ("iteration", C.c_long), ("objective", C.c_double),
+                ("basic", C.POINTER(C.c_int)), ("num_rows", C.c_int), ("row_width", C.c_int),
+                ("row", C.c_int), ("leaving", C.c_int), ("entering", C.c_int),
+                ("counters", C.POINTER(Memory)), ("solver", C.c_void_p)]
+
+
+VIEW_OBSERVER = C.CFUNCTYPE(None, C.POINTER(View), C.c_void_p)
+
 # (name, restype, argtypes) for every symbol include/lpsg.h declares.
 _P = C.c_void_p
 _PD = C.POINTER(C.c_double)
@@ -65,6 +81,8 @@ SIGNATURES = [
                                        C.POINTER(Report), _PD]),
     ("lpsg_set_observer", C.c_int, [_P, OBSERVER, _P]),
     ("lpsg_keep_trace", C.c_int, [_P, C.c_int]),
+    ("lpsg_set_view_observer", C.c_int, [_P, VIEW_OBSERVER, _P, C.c_int]),
+    ("lpsg_get_memory", C.c_int, [_P, C.POINTER(Memory)]),
     ("lpsg_get_trace", C.c_int, [_P, C.POINTER(Trace), C.c_long, C.POINTER(C.c_long)]),
     ("lpsg_price", C.c_int, [_P, _PI, _PI, _PD]),
     ("lpsg_compute_direction", C.c_int, [_P, C.c_int, C.c_double]),
@@ -106,15 +124,19 @@ _lib = None
 
 
 def load(build_if_missing: bool = True) -> C.CDLL:
-    """Loads the in-tree liblpsg.so (building it first when it is missing)."""
+    """Loads the in-tree liblpsg.so (building it first when it is missing).
+    LPSG_EXPERIMENTS_LIB=1 loads the performance-experiment build instead
+    (tools/dbg only: its knobs produce invalid solves)."""
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB_PATH):
+    xp = os.environ.get("LPSG_EXPERIMENTS_LIB") == "1"
+    path = _build.LIB_XP if xp else LIB_PATH
+    if not os.path.exists(path):
         if not build_if_missing:
-            raise OSError(f"lpsg library not built: {LIB_PATH}")
-        _build.build()
-    lib = C.CDLL(LIB_PATH)
+            raise OSError(f"lpsg library not built: {path}")
+        _build.build(experiments=xp)
+    lib = C.CDLL(path)
     for name, res, args in SIGNATURES:
         f = getattr(lib, name)
         f.restype = res

@@ -2,8 +2,6 @@
 #include "comm.h"
 
 #include <dlfcn.h>
-#include <execinfo.h>
-#include <signal.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -20,27 +18,6 @@
 namespace lpsg {
 
 namespace {
-
-// Shards of one process spin-wait on device flags. If two shards' streams
-// shared a hardware work queue, a spinning exchange kernel would block the
-// other shard's kernels queued behind it (deadlock), so ask for the maximum
-// number of queues before the CUDA context exists (the caller's own setting
-// wins; the runtime reads it at context creation).
-void segv_trace(int sig) {
-    void* frames[64];
-    const int n = backtrace(frames, 64);
-    fprintf(stderr, "lpsg: signal %d, native backtrace:\n", sig);
-    backtrace_symbols_fd(frames, n, 2);
-    signal(sig, SIG_DFL);
-    raise(sig);
-}
-
-struct ConnectionsDefault {
-    ConnectionsDefault() {
-        setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
-        if (getenv("LPSG_SEGV_TRACE")) signal(SIGSEGV, segv_trace);  // diagnostics
-    }
-} g_connections_default;
 
 void cuda_ok(cudaError_t e, const char* what) {
     if (e != cudaSuccess) {
@@ -200,7 +177,7 @@ private:
             if (g != rank) cuda_ok(cudaStreamWaitEvent(st, hub_->done[g], 0), "cudaStreamWaitEvent");
         if (debug_sync_) cuda_ok(cudaStreamSynchronize(st), "debug sync");
     }
-    bool debug_sync_ = getenv("LPSG_LOCAL_SYNC") != nullptr;
+    bool debug_sync_ = xp_env("LPSG_LOCAL_SYNC") != nullptr;
     void* scratch(size_t b) {
         if (b > scratch_bytes_) {
             if (scratch_) cudaFree(scratch_);

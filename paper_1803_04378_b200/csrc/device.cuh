@@ -19,10 +19,33 @@
 #include <cudaTypedefs.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "peer.cuh"
 
+// Performance experiments (memory-only / compute-only rates, kernel-shape
+// overrides). Their results are NOT valid solves, so they exist only in a build
+// compiled with -DLPSG_EXPERIMENTS (tools/, never the default library): there
+// LPSG_XP reads the knob bits of lpsg_config.reserved[2] and xp_env the LPSG_*
+// shape variables; in the default build both fold to constants.
+#ifdef LPSG_EXPERIMENTS
+#define LPSG_XP(d, bits) ((((d).dbg) & (bits)) != 0)
+#else
+#define LPSG_XP(d, bits) false
+#endif
+
 namespace lpsg {
+
+constexpr int kLookaheadExactBit = 16;  // lpsg_config.reserved[2]: see Dev::la_exact
+
+inline const char* xp_env(const char* name) {
+#ifdef LPSG_EXPERIMENTS
+    return getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
 
 enum CtlStatus : int {
     ST_RUNNING = 0,
@@ -150,7 +173,12 @@ struct Dev {
     const CUtensorMap* tm_nb;  // 2D TMA descriptors of A_nb, box {wbx slots, price_rows(wbx) rows}
     int price_nwc, price_S, price_smem, price_threads;
     int price_spt;             // slots per consumer thread: 1 (one chain per lane) or 2 (pairs)
-    int dbg;               // experiment knobs (cfg.reserved[2]); 0 in production
+    int dbg;               // perf-experiment knobs (cfg.reserved[2] minus bit 4); read only
+                           // through LPSG_XP, i.e. only in a -DLPSG_EXPERIMENTS build
+    int la_exact;          // lookahead theta' keeps the y_i == 0 select (cfg.reserved[2] bit 4):
+                           // result-identical verification mode
+    int naive;             // KernelMode::naive (tiled_engine.cpp:61-77): every element is stored,
+                           // no `temp != 0` skip (only zero signs differ from cached mode)
     int pdl;               // launch the pivot chain with programmatic dependent launch
     int upd_tma_store;     // k_update writes tiles back with TMA stores (else per-warp STG)
     int l2_hint;           // streaming TMA traffic carries an L2 evict-first hint
@@ -230,7 +258,8 @@ void launch_pivot(const Dev& d, cudaStream_t st);
 // also sets *nonfinite (device int) to 1 when some A entry is inf/NaN
 void launch_transpose(const double* A_rm, double* A_cm, int m, int n, long long ld, int* nonfinite,
                       cudaStream_t st);
-void launch_build_nb_from(const Dev& d, const double* A_rm, int n_scan, cudaStream_t st);
+// A_nb (this shard's n_scan slots, slot2col set) from d.A_cm
+void launch_build_nb_from_cm(const Dev& d, int n_scan, cudaStream_t st);
 // drive-out: scan this shard's slots against g = B^-1 row (m doubles) -> ctl.found
 // (local min j); then, after the cross-shard min, the entering reduced cost.
 void launch_drive_scan(const Dev& d, const double* g, cudaStream_t st);

@@ -80,7 +80,7 @@ __device__ __forceinline__ void price_decide(const Dev& d, Ctl* c, bool budget_h
     } else {
         c->q = j == INT_MAX ? -1 : j;
         c->d = j == INT_MAX ? 0.0 : z;
-        if (j == INT_MAX || (z <= d.opt_tol && !(d.dbg & 15))) c->status = ST_OPTIMAL;
+        if (j == INT_MAX || (z <= d.opt_tol && !LPSG_XP(d, 15))) c->status = ST_OPTIMAL;
     }
 }
 
@@ -159,13 +159,23 @@ __global__ void k_transpose(const double* __restrict__ A_rm, double* __restrict_
     }
 }
 
-// A_nb[i*ld_nb + s] = A_rm[i*n + slot2col[s]]
-__global__ void k_build_nb(const double* __restrict__ A_rm, Dev d, int n_scan) {
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= n_scan) return;
-    const int j = d.slot2col[s];
-    for (int i = blockIdx.y; i < d.m; i += gridDim.y)
-        d.A_nb[(size_t)i * d.ld_nb + s] = A_rm[(size_t)i * d.n_total + j];
+// A_nb[i*ld_nb + s] = A_cm[slot2col[s]*ld_cm + i]: a gathered transpose through
+// 32 x 32 shared tiles, coalesced along i on the read and along s on the write.
+__global__ void k_build_nb_cm(Dev d, int n_scan) {
+    __shared__ double tile[32][33];
+    __shared__ int col[32];
+    const int s0 = blockIdx.x * 32, i0 = blockIdx.y * 32;
+    if (threadIdx.y == 0) col[threadIdx.x] = s0 + (int)threadIdx.x < n_scan ? d.slot2col[s0 + threadIdx.x] : -1;
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int i = i0 + threadIdx.x, j = col[k];
+        tile[k][threadIdx.x] = (j >= 0 && i < d.m) ? d.A_cm[(size_t)j * d.ld_cm + i] : 0.0;
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int i = i0 + k, s = s0 + threadIdx.x;
+        if (i < d.m && s < n_scan) d.A_nb[(size_t)i * d.ld_nb + s] = tile[threadIdx.x][k];
+    }
 }
 
 // ------------------------------------------------------ rebuild_top_row ---
@@ -387,7 +397,7 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
                     const int i0 = k * R;
                     unsigned char* sb = smem + (size_t)st * stage_stride;
                     double* ws = reinterpret_cast<double*>(sb) + (size_t)R * w;
-                    if (d.dbg & 2) {  // experiment: no loads (compute-only rate)
+                    if (LPSG_XP(d, 2)) {  // experiment: no loads (compute-only rate)
                         mbar_arrive(&full[st]);
                     } else {
                         mbar_expect_tx(&full[st], (uint32_t)(R * w * 8 + R * 8));
@@ -421,7 +431,7 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
                 const int nr = min(R, m - k * R);
                 const double* sb = reinterpret_cast<const double*>(smem + (size_t)st * stage_stride);
                 const double* ws = sb + (size_t)R * w;
-                if (act && !(d.dbg & 1)) {
+                if (act && !LPSG_XP(d, 1)) {
                     // plain loads, scheduled by the compiler: 14-15 cycles a row,
                     // against 17-20 for volatile software-pipelined loads
                     // (tools/microbench/chain_rate.cu)
@@ -465,7 +475,7 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
                 const int nr = min(R, m - k * R);
                 const double* sb = reinterpret_cast<const double*>(smem + (size_t)st * stage_stride);
                 const double* ws = sb + (size_t)R * w;
-                if (s2 < ns && !(d.dbg & 1)) {  // dbg bit 0: no math (memory-only rate)
+                if (s2 < ns && !LPSG_XP(d, 1)) {  // experiment bit 0: no math (memory-only rate)
                     const double2* col = reinterpret_cast<const double2*>(sb + q * wbx * R + tq);
                     const int pitch = wbx / 2;  // row pitch in double2
                     const int ng = nr >> 3;
@@ -576,6 +586,8 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
                                             int nst, int S, int C, int h, int i0, int r, int U,
                                             bool up, int warp, int lane) {
     const int m = d.m, mloc = d.mloc;
+    const bool naive = d.naive != 0;
+    const double nz_r = naive ? -0.0 : 0.0;  // row r's multiplier: -(zeroed y_r) (tiled_engine.cpp:241)
     double ny0[NIT], ny1[NIT];
     bool ok[NIT];
 #pragma unroll
@@ -583,11 +595,11 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
         const int t = 2 * lane + 64 * u;
         const int i = i0 + t;  // local row
         ok[u] = t < h;
-        ny0[u] = (ok[u] && i < mloc && i != r) ? -d.Y[i] : 0.0;
-        ny1[u] = (ok[u] && i + 1 < mloc && i + 1 != r) ? -d.Y[i + 1] : 0.0;
+        ny0[u] = (ok[u] && i < mloc && i != r) ? -d.Y[i] : (i == r ? nz_r : 0.0);
+        ny1[u] = (ok[u] && i + 1 < mloc && i + 1 != r) ? -d.Y[i + 1] : (i + 1 == r ? nz_r : 0.0);
     }
     const size_t ldT = (size_t)d.ldT;
-    const bool nomath = (d.dbg & 4) != 0;  // experiment: stores without the update math
+    const bool nomath = LPSG_XP(d, 4);  // experiment: stores without the update math
     const bool tstore = d.upd_tma_store != 0;  // the tile goes back by TMA store (producer warp)
     double2* const gbase = reinterpret_cast<double2*>(d.T + i0) + lane;  // + col * ldT/2
     const int ncols = m + 1;
@@ -617,8 +629,8 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
                         const double p1 = dmul(ny1[u], xj);
                         const double s0v = dadd(tv.x, p0);
                         const double s1v = dadd(tv.y, p1);
-                        tv.x = (p0 != 0.0) ? s0v : tv.x;
-                        tv.y = (p1 != 0.0) ? s1v : tv.y;
+                        tv.x = (naive || p0 != 0.0) ? s0v : tv.x;
+                        tv.y = (naive || p1 != 0.0) ? s1v : tv.y;
                         tcol[32 * u] = tv;
                         if (!tstore) gcol[32 * u] = tv;
                     }
@@ -646,10 +658,12 @@ __device__ __forceinline__ void update_role_small(const Dev& d, unsigned char* s
     const int lc = lane / hp, lr = lane - lc * hp;
     const bool act = lc < cpw;
     const int i = i0 + 2 * lr;             // local row of this lane's pair
-    const double ny0 = (act && i < mloc && i != r) ? -d.Y[i] : 0.0;
-    const double ny1 = (act && i + 1 < mloc && i + 1 != r) ? -d.Y[i + 1] : 0.0;
+    const bool naive = d.naive != 0;
+    const double nz_r = naive ? -0.0 : 0.0;
+    const double ny0 = (act && i < mloc && i != r) ? -d.Y[i] : (i == r ? nz_r : 0.0);
+    const double ny1 = (act && i + 1 < mloc && i + 1 != r) ? -d.Y[i + 1] : (i + 1 == r ? nz_r : 0.0);
     const size_t ldT = (size_t)d.ldT;
-    const bool nomath = (d.dbg & 4) != 0;
+    const bool nomath = LPSG_XP(d, 4);
     const bool tstore = d.upd_tma_store != 0;
     double2* const gbase = reinterpret_cast<double2*>(d.T + i0) + lr;
     const int ncols = m + 1;
@@ -671,8 +685,8 @@ __device__ __forceinline__ void update_role_small(const Dev& d, unsigned char* s
                     const double p1 = dmul(ny1, xj);
                     const double s0v = dadd(tv.x, p0);
                     const double s1v = dadd(tv.y, p1);
-                    tv.x = (p0 != 0.0) ? s0v : tv.x;
-                    tv.y = (p1 != 0.0) ? s1v : tv.y;
+                    tv.x = (naive || p0 != 0.0) ? s0v : tv.x;
+                    tv.y = (naive || p1 != 0.0) ? s1v : tv.y;
                     *tp = tv;
                 }
                 if (!tstore) gbase[(size_t)(j0 + jj) * (ldT / 2)] = tv;
@@ -759,7 +773,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                 unsigned char* sb = smem + (size_t)st * stage_stride;
                 double* xs = reinterpret_cast<double*>(sb) + tile_el;
                 double* as = xs + C;
-                if (d.dbg & 8) {  // experiment: no loads (compute-only rate)
+                if (LPSG_XP(d, 8)) {  // experiment: no loads (compute-only rate)
                     mbar_arrive(&full[st]);
                 } else {
                     mbar_expect_tx(&full[st], (uint32_t)(tile_el * 8) + (up ? seg : 0u) + (ft ? seg : 0u));
@@ -804,7 +818,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         // its multiplier is 0 and the skip leaves it untouched, exactly like the
         // zeroed multiplier of tiled_engine.cpp:241.
         const int nit = (h + 63) >> 6;
-        if (h <= 32 && !(d.dbg & 32)) {  // dbg bit 5: the one-column-per-warp path (A/B)
+        if (h <= 32 && !LPSG_XP(d, 32)) {  // experiment bit 5: the one-column-per-warp path (A/B)
             update_role_small(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, warp, lane);
         } else switch (nit) {
             case 1: update_role<1>(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, warp, lane); break;
@@ -822,7 +836,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         uint32_t ph = 0;
         for (int k = 0; k < nst; ++k) {
             mbar_wait(&upd[st], ph);
-            if (ft && valid && !(d.dbg & 4)) {  // dbg bit 2: no FTRAN math
+            if (ft && valid && !LPSG_XP(d, 4)) {  // experiment bit 2: no FTRAN math
                 const int j0 = k * C, nf = min(C, m - j0);
                 const double* tile = reinterpret_cast<const double*>(smem + (size_t)st * stage_stride);
                 if (m - j0 < C) f_bbar = tile[(m - j0) * h + t];  // updated b_bar_i (column m)
@@ -850,7 +864,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
             if (lane == 0) mbar_arrive(&empty[st]);
             if (++st == S) { st = 0; ph ^= 1; }
         }
-        if ((d.dbg & 12) && ft) acc = 1.0 + 1e-6 * i;  // experiments: keep pivoting on a valid column
+        if (LPSG_XP(d, 12) && ft) acc = 1.0 + 1e-6 * i;  // experiments: keep pivoting on a valid column
         if (valid) {
             if (ft) {
                 d.Y[i] = acc;
@@ -862,7 +876,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                 if (i == r) d.Y[i] = 1.0;
                 else {
                     const double p = dmul(-yi, d.xrow[m + 1]);
-                    if (p != 0.0) d.Y[i] = dadd(yi, p);
+                    if (d.naive || p != 0.0) d.Y[i] = dadd(yi, p);
                 }
             }
         }
@@ -880,7 +894,9 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         const int i = d.row0 + i0 + (threadIdx.x - U * 32);  // global row
         bool elig = f_ok && !d.frozen[i] && !(f_y <= d.pivot_tol);
         const double ratio = elig ? ddiv(f_bbar, f_y) : kInf;
-        const double th = block_min(elig ? ratio : kInf);
+        // std::min(theta, NaN) keeps theta (solver.cpp:147): a NaN ratio must not
+        // reach block_min, whose shuffle steps keep a NaN left operand
+        const double th = block_min((elig && !isnan(ratio)) ? ratio : kInf);
         const int any = __syncthreads_or(elig);
         if (threadIdx.x == 0) { s_theta = th; s_any = any; }
         __syncthreads();
@@ -939,17 +955,13 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
     }
     const double gth = s_th2;
     const double window = dadd(gth, dmul(d.ratio_tie_tol, fmax(1.0, fabs(gth))));
-    constexpr int kMaxLocal = 8;
-    int n = 0;
-    int rows_keep[kMaxLocal];
-    double ratio_keep[kMaxLocal];
+    // (no per-thread candidate arrays: dynamically indexed, they would live in
+    // local memory; the few in-window entries are re-read from L2 below)
+    int n = 0, first_row = -1;
     for (int e = 0; e < cnt; ++e) {
         const double ra = __ldcg(d.rc_ratio + (size_t)b * h + e);
         if (ra <= window) {
-            if (n < kMaxLocal) {
-                rows_keep[n] = __ldcg(d.rc_row + (size_t)b * h + e);
-                ratio_keep[n] = ra;
-            }
+            if (n == 0) first_row = __ldcg(d.rc_row + (size_t)b * h + e);
             ++n;
         }
     }
@@ -975,19 +987,12 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
     __syncthreads();
     int pos = s_pre[warp] + incl - n;
     if (n > 0) {
-        if (pos == 0) s_first = n <= kMaxLocal ? rows_keep[0] : -2;
-        if (n <= kMaxLocal) {
-            for (int e = 0; e < n; ++e) {
-                d.cand[pos + e] = rows_keep[e];
-                d.cand_ratio[pos + e] = ratio_keep[e];
-            }
-        } else {
-            for (int e = 0; e < cnt; ++e) {
-                const double ra = __ldcg(d.rc_ratio + (size_t)b * h + e);
-                if (ra <= window) {
-                    d.cand_ratio[pos] = ra;
-                    d.cand[pos++] = __ldcg(d.rc_row + (size_t)b * h + e);
-                }
+        if (pos == 0) s_first = first_row;
+        for (int e = 0; e < cnt; ++e) {
+            const double ra = __ldcg(d.rc_ratio + (size_t)b * h + e);
+            if (ra <= window) {
+                d.cand_ratio[pos] = ra;
+                d.cand[pos++] = __ldcg(d.rc_row + (size_t)b * h + e);
             }
         }
     }
@@ -1245,7 +1250,7 @@ __global__ void __launch_bounds__(256) k_pivot(Dev d) {
     const double yr = sharded ? d.xbuf[m + 2] : d.Y[r];
     const double dk = d.top[m + 1];
     const int p_leave = d.basic[r];
-    const int s_q = d.col2slot[q];
+    const int s_q = q < d.n_total ? d.col2slot[q] : -1;  // artificials have no slot
     const int last_col = n_scan > 0 ? d.slot2col[n_scan - 1] : -1;
     const bool one = gtid <= m && gtid + gstride > m;  // this thread owns at most one j
     double tj = 0.0, topj = 0.0;
@@ -1290,8 +1295,9 @@ __global__ void __launch_bounds__(256) k_pivot(Dev d) {
             d.T[(size_t)gtid * ldT + r] = xj;  // in place, like pr[j] /= y_rk (solver.cpp:246-247)
         }
         const double p = dmul(ndk, xj);
-        const double nt = (p != 0.0) ? dadd(topj, p) : topj;
-        if (p != 0.0) d.top[gtid] = nt;
+        const bool wr = d.naive || p != 0.0;
+        const double nt = wr ? dadd(topj, p) : topj;
+        if (wr) d.top[gtid] = nt;
         if (gtid == m) ent->objective = nt;
     } else {
         for (int j = gtid; j <= m; j += gstride) {
@@ -1302,8 +1308,9 @@ __global__ void __launch_bounds__(256) k_pivot(Dev d) {
             }
             const double p = dmul(ndk, x);
             const double t0 = d.top[j];
-            const double nt = (p != 0.0) ? dadd(t0, p) : t0;
-            if (p != 0.0) d.top[j] = nt;
+            const bool wr = d.naive || p != 0.0;
+            const double nt = wr ? dadd(t0, p) : t0;
+            if (wr) d.top[j] = nt;
             if (j == m) ent->objective = nt;
         }
     }
@@ -1319,7 +1326,7 @@ __global__ void __launch_bounds__(256) k_pivot(Dev d) {
     {
         // the d slot (T[0][m+1]) is every CTA's multiplier source
         const double p = dmul(ndk, xl);
-        if (p != 0.0) d.top[m + 1] = dadd(dk, p);
+        if (d.naive || p != 0.0) d.top[m + 1] = dadd(dk, p);
     }
     int ns = n_scan;
     if (p_local) {
@@ -1696,9 +1703,9 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_theta(Dev d, LookaheadDev la
     bool zrow[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) zrow[u] = yv[u] == 0.0;
-    // some X_kj is inf/NaN: keep the select (dbg bit 4 forces it: a parity check
+    // some X_kj is inf/NaN: keep the select (la_exact forces it: a parity check
     // of that path, tests/test_gpu_parity.py)
-    const bool exact = *la.nonfinite != 0 || (d.dbg & 16) != 0;
+    const bool exact = *la.nonfinite != 0 || d.la_exact != 0;
     double rt[4], rx[4], rb[4];
     auto fetch = [&](int j0) {
 #pragma unroll
@@ -1858,10 +1865,10 @@ void launch_transpose(const double* A_rm, double* A_cm, int m, int n, long long 
     k_transpose<<<grid, dim3(32, 8), 0, st>>>(A_rm, A_cm, m, n, ld, nonfinite);
 }
 
-void launch_build_nb_from(const Dev& d, const double* A_rm, int n_scan, cudaStream_t st) {
+void launch_build_nb_from_cm(const Dev& d, int n_scan, cudaStream_t st) {
     if (n_scan <= 0) return;
-    dim3 grid((n_scan + 255) / 256, (unsigned)std::min(d.m, 1024));
-    k_build_nb<<<grid, 256, 0, st>>>(A_rm, d, n_scan);
+    dim3 grid((n_scan + 31) / 32, (d.m + 31) / 32);
+    k_build_nb_cm<<<grid, dim3(32, 8), 0, st>>>(d, n_scan);
 }
 
 void launch_rebuild_top(const Dev& d, const double* init, double* out, cudaStream_t st) {
@@ -1909,18 +1916,18 @@ void configure_kernels(Dev& d) {
     // update + FTRAN: h rows per CTA (even, so the TMA box row is a 16-byte multiple)
     int h = (d.mloc + G - 1) / G;
     h = std::min(224, std::max(2, (h + 1) & ~1));  // <= 224 rows: 8 update + 7 FTRAN + 1 producer warps = 512 threads
-    if (const char* e = getenv("LPSG_UPD_H")) h = std::min(224, std::max(2, atoi(e) & ~1));  // shape experiments
+    if (const char* e = xp_env("LPSG_UPD_H")) h = std::min(224, std::max(2, atoi(e) & ~1));  // shape experiments
     d.upd_h = h;
     d.update_grid = (d.mloc + h - 1) / h;
     // columns per stage: short row blocks (small m) take wide stages so the
     // per-stage handshakes amortise (C2 m=2000: +12 %); TMA boxes stop at 256
     d.upd_C = h <= 16 ? 128 : h <= 32 ? 64 : h <= 64 ? 32 : h <= 160 ? 16 : 8;
-    if (const char* e = getenv("LPSG_UPD_COLS")) d.upd_C = std::max(2, atoi(e)) & ~1;  // tuning experiments
+    if (const char* e = xp_env("LPSG_UPD_COLS")) d.upd_C = std::max(2, atoi(e)) & ~1;  // tuning experiments
     d.upd_U = 8;
     const size_t tile_el = (size_t)d.upd_C * h;
     const size_t stage = ((tile_el + 2 * (size_t)d.upd_C) * 8 + 1023) / 1024 * 1024;
     size_t s_cap = 8;
-    if (const char* e = getenv("LPSG_UPD_STAGES")) s_cap = (size_t)std::max(2, atoi(e));  // tuning experiments
+    if (const char* e = xp_env("LPSG_UPD_STAGES")) s_cap = (size_t)std::max(2, atoi(e));  // tuning experiments
     // >= 3 stages: the storer keeps 2 TMA stores in flight behind the update warps
     d.upd_S = (int)std::max<size_t>(3, std::min<size_t>(s_cap, (size_t)(200 * 1024) / stage));
     d.upd_smem = (int)(d.upd_S * stage + 3 * d.upd_S * 8);
@@ -1933,7 +1940,7 @@ void configure_kernels(Dev& d) {
     // one slot per consumer lane while 11 consumer warps cover the widest CTA
     // range, spread over at least min(4, w/8) warps (all four SM sub-partitions);
     // wider ranges (n_total > ~50k per GPU) use slot pairs
-    if (gm.w <= 11 * 32 && !getenv("LPSG_PRICE_PAIRS")) {  // env: A/B experiments
+    if (gm.w <= 11 * 32 && !xp_env("LPSG_PRICE_PAIRS")) {  // env: A/B experiments
         d.price_spt = 1;
         d.price_nwc = std::max((gm.w + 31) / 32, std::min(4, (gm.w + 7) / 8));
     } else {
@@ -1961,7 +1968,7 @@ void configure_kernels(Dev& d) {
     // shard's spin-waiting exchange kernel can share an SM with another shard's
     // streaming CTA when shards share a GPU (a different carveout would make the
     // streaming kernel wait for the spinner to exit: deadlock).
-    const void* all[] = {(const void*)k_init_tableau, (const void*)k_transpose, (const void*)k_build_nb,
+    const void* all[] = {(const void*)k_init_tableau, (const void*)k_transpose, (const void*)k_build_nb_cm,
                          (const void*)k_rebuild_top, (const void*)k_price, (const void*)k_price_final,
                          (const void*)k_update, (const void*)k_ratio_final, (const void*)k_ratio,
                          (const void*)k_pivot_row, (const void*)k_pivot, (const void*)k_gather_row,

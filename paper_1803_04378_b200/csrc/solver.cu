@@ -75,13 +75,55 @@ double now_s() {
 }
 
 long long round_up(long long v, long long a) { return (v + a - 1) / a * a; }
+
+// Owns one device allocation until released (staging buffers freed on throw).
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+// The LP's row-major A (host) -> column-major A_cm (n columns of pitch ld) on
+// the current device, in row blocks of <= 128 MB through one staging buffer,
+// so the upload never holds a second full-size copy of A in HBM (9.2 GB at
+// C5). Throws LPSG_INVALID_ARGUMENT when A holds an inf/NaN (SURVEY.md
+// Appendix A.8), after the upload has been drained.
+void upload_A_cm(const lpsg_problem& lp, double* A_cm, long long ld, cudaStream_t st) {
+    const int m = lp.m, n = lp.n_total;
+    const long long chunk_el = 16LL << 20;  // 128 MB of doubles
+    const int rows = (int)std::max<long long>(32, std::min<long long>(m, chunk_el / std::max(1, n) / 32 * 32));
+    DevBuf stage, flag;
+    CK(cudaMalloc(&stage.p, sizeof(double) * (size_t)rows * n));
+    CK(cudaMalloc(&flag.p, sizeof(int)));
+    int* nonfinite = static_cast<int*>(flag.p);
+    CK(cudaMemsetAsync(nonfinite, 0, sizeof(int), st));
+    CK(cudaMemsetAsync(A_cm, 0, sizeof(double) * ((size_t)n * ld + 64), st));
+    for (int i0 = 0; i0 < m; i0 += rows) {
+        const int nr = std::min(rows, m - i0);
+        CK(cudaMemcpyAsync(stage.p, lp.A + (size_t)i0 * n, sizeof(double) * (size_t)nr * n,
+                           cudaMemcpyHostToDevice, st));
+        launch_transpose(static_cast<const double*>(stage.p), A_cm + i0, nr, n, ld, nonfinite, st);
+        CK(cudaGetLastError());
+    }
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (bad)
+        throw Error(LPSG_INVALID_ARGUMENT,
+                    "A holds an inf/NaN coefficient: reduced costs would not be finite, and the "
+                    "reference's first-scanned-column pricing rule is not reproduced for them");
+}
 }  // namespace
 
 class Solver {
 public:
     // comm == nullptr: single GPU. Otherwise this object is shard comm->rank of
     // comm->size; every rank must make the same calls.
-    Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm = nullptr);
+    // shared_A_cm: a column-major A (upload_A_cm, pitch round_up(m, 4)) owned by
+    // the caller and shared by the in-process shards of one device (read-only)
+    Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm = nullptr,
+           double* shared_A_cm = nullptr);
     ~Solver();
 
     void solve(lpsg_report* rep);
@@ -105,11 +147,21 @@ public:
 
     lpsg_observer observer = nullptr;
     void* observer_user = nullptr;
+    // SolverConfig::observer with the whole IterationView (solver.hpp:21-32)
+    lpsg_view_observer view_observer = nullptr;
+    void* view_user = nullptr;
+    bool view_rows = false;      // the callback may read tableau rows: unfused, one pivot per round trip
+    lpsg_solver* handle = nullptr;  // the C handle, for lpsg_read_row from inside the callback
+    lpsg_memory memory() const;
     bool keep_trace = false;
     std::vector<lpsg_trace> trace;
 
 private:
+    void init(const lpsg_problem& lp);
+    void release();
     int run_phase();
+    int run_phase_stepwise();
+    int handle_stop(int st, bool* resumed);
     void enter_phase2();
     void drive_out_artificials();
     void rebuild_top_row();
@@ -122,7 +174,6 @@ private:
     void seq_pivot();
     void seq_price();
     void seq_update();
-    void resume_with_row(int r);
     std::vector<int> gather_overflow_candidates();
     void single_gpu_only(const char* what) const;
     int owner_of_row(int i) const;
@@ -158,6 +209,7 @@ private:
     int batch_ = 16;
     bool unfused_ratio_ = false;  // debug knob (cfg.reserved[0] & 1): standalone ratio kernel
     Comm* comm_ = nullptr;
+    double* shared_A_cm_ = nullptr;  // not owned (lpsg_solve_sharded)
     bool sharded_ = false;        // comm_ attached: the exchange path runs even for one rank
     bool dbg_trace_ = getenv("LPSG_TRACE_COMM") != nullptr;
     int world_ = 1, rank_ = 0;
@@ -177,6 +229,7 @@ public:
     long launches_total = 0;
     double last_device_ms = 0.0;   // CUDA-event span of the last solve() on the solver stream
     long long h2d_bytes = 0, d2h_bytes = 0;
+    double dev_read_bytes = 0.0, dev_write_bytes = 0.0;  // algorithmic, per pivot done (lpsg_memory)
     void set_profile(bool on);
     void set_max_iter(long long v);
 
@@ -283,8 +336,20 @@ void Solver::set_max_iter(long long v) {
     CK(cudaStreamSynchronize(st_));
 }
 
-Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
-    : cfg_(cfg), m_(lp.m), n_total_(lp.n_total), comm_(comm) {
+// A constructor that throws never runs ~Solver, so everything init() acquired
+// is released here before the exception leaves (lpsg_create then reports it).
+Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm, double* shared_A_cm)
+    : cfg_(cfg), m_(lp.m), n_total_(lp.n_total), comm_(comm), shared_A_cm_(shared_A_cm) {
+    try {
+        init(lp);
+    } catch (...) {
+        release();
+        throw;
+    }
+}
+
+void Solver::init(const lpsg_problem& lp) {
+    const lpsg_config& cfg = cfg_;
     if (comm_) {
         sharded_ = true;
         world_ = comm_->size;
@@ -388,17 +453,20 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     d_.feas_tol = cfg_.feas_tol;
     d_.ratio_tie_tol = cfg_.ratio_tie_tol;
     d_.anticycle = cfg_.anticycle;
-    d_.dbg = cfg_.reserved[2];
+    if (cfg_.kernel != 0 && cfg_.kernel != 1) throw Error(LPSG_INVALID_ARGUMENT, "lpsg_create: kernel must be 0 (cached) or 1 (naive)");
+    d_.naive = cfg_.kernel == 1 ? 1 : 0;
+    d_.dbg = cfg_.reserved[2] & ~kLookaheadExactBit;  // perf experiments (-DLPSG_EXPERIMENTS only)
+    d_.la_exact = (cfg_.reserved[2] & kLookaheadExactBit) != 0;
     // PDL hides kernel-boundary latency; it pays up to m ~ 10^4 (C1 +21 %, C3
     // +1.4 %) and was measured to cost ~17 % at m = 24000, where the boundaries
     // are noise against 3 ms pivots
-    d_.pdl = (!comm && m <= 12000 && getenv("LPSG_NO_PDL") == nullptr) ? 1 : 0;
-    d_.upd_tma_store = getenv("LPSG_UPD_STG") == nullptr ? 1 : 0;
-    d_.l2_hint = getenv("LPSG_NO_L2_HINT") == nullptr ? 1 : 0;
+    d_.pdl = (!comm_ && m <= 12000 && xp_env("LPSG_NO_PDL") == nullptr) ? 1 : 0;
+    d_.upd_tma_store = xp_env("LPSG_UPD_STG") == nullptr ? 1 : 0;
+    d_.l2_hint = xp_env("LPSG_NO_L2_HINT") == nullptr ? 1 : 0;
     configure_kernels(d_);
     CK(cudaGetLastError());
     d_.ldT = round_up(std::max<long long>(d_.mloc + 1, (long long)d_.update_grid * d_.upd_h), 32);
-    unfused_ratio_ = !sharded_ && (cfg_.reserved[0] & 1) != 0;
+    unfused_ratio_ = !sharded_ && (cfg_.reserved[0] & 1) != 0;  // standalone k_ratio (result-identical)
     batch_ = cfg_.batch > 0 ? cfg_.batch : (m <= 1024 ? 64 : m <= 4096 ? 16 : 4);
     d_.log_cap = 2 * batch_ + 8;  // ring: the drained batch + the one in flight
 
@@ -413,7 +481,7 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
         d_.rmsg = dalloc<RatioMsg>(world_ + 1);
         chain_ = dalloc<double>(m + 1);
     }
-    double* A_cm = dalloc<double>((size_t)n * d_.ld_cm + 64);
+    double* A_cm = shared_A_cm_ ? shared_A_cm_ : dalloc<double>((size_t)n * d_.ld_cm + 64);
     d_.A_cm = A_cm;
     d_.A_nb = dalloc<double>((size_t)m * d_.ld_nb + 64);
     d_.slot2col = dalloc<int>(d_.ld_nb);
@@ -454,29 +522,14 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
         }
     const int n_scan = (int)slot2col.size();
     n_scan_host_ = n_scan;
-    {
-        double* A_rm = dalloc<double>((size_t)m * n);
-        int* nonfinite = reinterpret_cast<int*>(scratch_);
-        CK(cudaMemsetAsync(nonfinite, 0, sizeof(int), st_));
-        CK(cudaMemcpyAsync(A_rm, lp.A, sizeof(double) * (size_t)m * n, cudaMemcpyHostToDevice, st_));
-        CK(cudaMemsetAsync(A_cm, 0, sizeof(double) * ((size_t)n * d_.ld_cm + 64), st_));
-        launch_transpose(A_rm, A_cm, m, n, d_.ld_cm, nonfinite, st_);
-        CK(cudaMemsetAsync(d_.slot2col, 0xff, sizeof(int) * d_.ld_nb, st_));
-        if (n_scan)
-            CK(cudaMemcpyAsync(d_.slot2col, slot2col.data(), sizeof(int) * n_scan, cudaMemcpyHostToDevice, st_));
-        CK(cudaMemcpyAsync(d_.col2slot, col2slot.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st_));
-        CK(cudaMemsetAsync(d_.A_nb, 0, sizeof(double) * ((size_t)m * d_.ld_nb + 64), st_));
-        launch_build_nb_from(d_, A_rm, n_scan, st_);
-        CK(cudaGetLastError());
-        int bad = 0;
-        CK(cudaMemcpyAsync(&bad, nonfinite, sizeof(int), cudaMemcpyDeviceToHost, st_));
-        CK(cudaStreamSynchronize(st_));
-        CK(cudaFree(A_rm));
-        if (bad)
-            throw Error(LPSG_INVALID_ARGUMENT,
-                        "A holds an inf/NaN coefficient: reduced costs would not be finite, and the "
-                        "reference's first-scanned-column pricing rule is not reproduced for them");
-    }
+    CK(cudaMemsetAsync(d_.slot2col, 0xff, sizeof(int) * d_.ld_nb, st_));
+    if (n_scan)
+        CK(cudaMemcpyAsync(d_.slot2col, slot2col.data(), sizeof(int) * n_scan, cudaMemcpyHostToDevice, st_));
+    CK(cudaMemcpyAsync(d_.col2slot, col2slot.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st_));
+    if (!shared_A_cm_) upload_A_cm(lp, A_cm, d_.ld_cm, st_);
+    CK(cudaMemsetAsync(d_.A_nb, 0, sizeof(double) * ((size_t)m * d_.ld_nb + 64), st_));
+    launch_build_nb_from_cm(d_, n_scan, st_);
+    CK(cudaGetLastError());
     CK(cudaMemcpyAsync(d_.basic, basic_.data(), sizeof(int) * m, cudaMemcpyHostToDevice, st_));
     CK(cudaMemsetAsync(d_.frozen, 0, m, st_));
     CK(cudaMemcpyAsync(cost_buf_, cost.data(), sizeof(double) * cost.size(), cudaMemcpyHostToDevice, st_));
@@ -516,13 +569,15 @@ Solver::Solver(const lpsg_problem& lp, const lpsg_config& cfg, Comm* comm)
     last_objective_ = objective_value();
 }
 
-Solver::~Solver() {
+Solver::~Solver() { release(); }
+
+void Solver::release() {
     if (st_) cudaStreamSynchronize(st_);
     if (sharded_ && d_.xbuf) {
         comm_->sym_free(d_.xbuf);
         if (d_.xrow == d_.xbuf) d_.xrow = nullptr;
     }
-    void* bufs[] = {d_.T, d_.top, d_.Y, d_.xrow, (void*)d_.A_cm, d_.A_nb, d_.slot2col, d_.col2slot,
+    void* bufs[] = {d_.T, d_.top, d_.Y, d_.xrow, shared_A_cm_ ? nullptr : (void*)d_.A_cm, d_.A_nb, d_.slot2col, d_.col2slot,
                     d_.basic, d_.frozen, cost_buf_, d_.ctl, d_.cand, d_.pz, d_.pj, d_.log, scratch_, tmaps_,
                     d_.rc_theta, d_.rc_cnt, d_.rc_row, d_.rc_ratio, d_.cand_ratio, d_.pmsg, d_.rmsg,
                     chain_};
@@ -532,8 +587,25 @@ Solver::~Solver() {
     if (hlog_) cudaFreeHost(hlog_);
     if (hone_) cudaFreeHost(hone_);
     if (ev_snap_) cudaEventDestroy(ev_snap_);
+    for (cudaEvent_t e : ev_pool_) cudaEventDestroy(e);
+    for (auto& r : ev_used_) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
     if (pool_) cudaMemPoolDestroy(pool_);
     if (st_) cudaStreamDestroy(st_);
+    d_ = Dev{};
+    cost_buf_ = scratch_ = chain_ = nullptr;
+    tmaps_ = nullptr;
+    hctl_ = nullptr;
+    hlog_ = nullptr;
+    hone_ = nullptr;
+    ev_snap_ = nullptr;
+    ev_pool_.clear();
+    ev_used_.clear();
+    pool_ = nullptr;
+    st_ = nullptr;
+    cudaGetLastError();
 }
 
 void Solver::push() {
@@ -612,9 +684,34 @@ void Solver::note_pivot(const LogEntry& e) {
     n_scan_host_ += (p_local ? 1 : 0) - (q_local ? 1 : 0);
     if (last_objective_ - e.objective > cfg_.opt_tol) banned_.clear();
     last_objective_ = e.objective;
+    {
+        // algorithmic HBM traffic of this pivot: pricing reads
+        // the scanned A columns and W; the update reads + writes this shard's
+        // [B^-1 | b_bar] rows; the pivot row is read, divided, written; W updated
+        const double m = m_;
+        dev_read_bytes += 8.0 * m * (double)n_scan_host_ + 8.0 * m + 8.0 * d_.mloc * (m + 1.0) +
+                          8.0 * (m + 1.0) * 2.0 + 8.0 * m;
+        dev_write_bytes += 8.0 * d_.mloc * (m + 1.0) + 8.0 * (m + 1.0) * 2.0;
+    }
     lpsg_trace t{(long)e.iteration, e.phase, e.row, e.leaving, e.entering, e.objective};
     if (keep_trace) trace.push_back(t);
     if (observer) observer(&t, observer_user);
+    if (view_observer) {
+        const lpsg_memory mem = memory();
+        lpsg_iteration_view v{e.phase, (long)e.iteration, e.objective, basic_.data(), m_, m_ + 2,
+                              e.row, e.leaving, e.entering, &mem, handle};
+        view_observer(&v, view_user);
+    }
+}
+
+lpsg_memory Solver::memory() const {
+    lpsg_memory mm{};
+    mm.device_read_bytes = (uint64_t)dev_read_bytes;
+    mm.device_write_bytes = (uint64_t)dev_write_bytes;
+    mm.h2d_bytes = (uint64_t)h2d_bytes;
+    mm.d2h_bytes = (uint64_t)d2h_bytes;
+    mm.kernel_launches = (uint64_t)launches_total;
+    return mm;
 }
 
 // The device appends to a ring (log_len is monotonic); entries
@@ -694,15 +791,6 @@ void Solver::enqueue_pivots(int n) {
     CK(cudaGetLastError());
 }
 
-void Solver::resume_with_row(int r) {
-    hctl_->r = r;
-    hctl_->status = ST_RUNNING;
-    push();
-    seq_pivot();
-    seq_price();
-    seq_update();
-}
-
 // ST_OVERFLOW (world > 1): a shard had more local candidates than a RatioMsg
 // holds. Gather every shard's full local list and apply the global window on
 // the host with the device's formula (solver.cpp:154-160).
@@ -753,7 +841,7 @@ int Solver::run_phase() {
     // stop (optimal, tie, budget) seen in snapshot k leaves the state exactly as
     // batch k ended. Profiling windows stay synchronous (their events must be
     // complete when read).
-    const bool pipelined = !prof_ && getenv("LPSG_NO_PIPELINE") == nullptr && (!comm_ || comm_->allows_pipelining());
+    const bool pipelined = !prof_ && xp_env("LPSG_NO_PIPELINE") == nullptr && (!comm_ || comm_->allows_pipelining());
     bool enqueued = false;
     // Adaptive batch: a tie stops the device chain, and the rest of the batch (and
     // the one in flight) then runs as no-op launches. Degenerate LPs tie on most
@@ -785,25 +873,86 @@ int Solver::run_phase() {
         }
         if (st == ST_TIE || st == ST_OVERFLOW) cur = std::max(1, cur / 4);
         enqueued = false;  // an in-flight batch (if any) no-ops: the device stopped
+        bool resumed = false;
+        const int out = handle_stop(st, &resumed);
+        if (resumed) {
+            seq_pivot();
+            seq_price();
+            seq_update();
+            continue;
+        }
+        return out;
+    }
+}
+
+// A stopped device chain: a ratio-test tie (select_leaving on the host, then
+// *resumed with hctl_->r set and pushed: the caller enqueues the pivot) or a
+// final status of the phase (returned).
+int Solver::handle_stop(int st, bool* resumed) {
+    *resumed = false;
+    if (st == ST_TIE || st == ST_OVERFLOW) {
+        std::vector<int> cand;
         if (st == ST_TIE) {
-            std::vector<int> cand(hctl_->ncand);
+            cand.resize(hctl_->ncand);
             CK(cudaMemcpyAsync(cand.data(), d_.cand, sizeof(int) * cand.size(), cudaMemcpyDeviceToHost, st_));
             CK(cudaStreamSynchronize(st_));
-            resume_with_row(select_leaving(cand, hctl_->q));
-            continue;
-        }
-        if (st == ST_OVERFLOW) {
-            const std::vector<int> cand = gather_overflow_candidates();
+        } else {
+            cand = gather_overflow_candidates();
             if (cand.empty()) throw Error(LPSG_CUDA_ERROR, "sharded ratio test lost its candidates");
-            resume_with_row(cand.size() == 1 || cfg_.anticycle == 1 ? cand.front()
-                                                                    : select_leaving(cand, hctl_->q));
-            continue;
         }
-        if (st == ST_PIVOT_ERR) throw Error(LPSG_PIVOT_TOO_SMALL, "pivot element below pivot_tol");
-        if (st == ST_OPTIMAL) return LPSG_OPTIMAL;
-        if (st == ST_UNBOUNDED) return LPSG_UNBOUNDED;
-        if (st == ST_ITER_LIMIT) return LPSG_ITERATION_LIMIT;
-        throw Error(LPSG_CUDA_ERROR, "unexpected control status " + std::to_string(st));
+        const int r = cand.size() == 1 || cfg_.anticycle == 1 ? cand.front() : select_leaving(cand, hctl_->q);
+        hctl_->r = r;
+        hctl_->status = ST_RUNNING;
+        push();
+        *resumed = true;
+        return 0;
+    }
+    if (st == ST_PIVOT_ERR) throw Error(LPSG_PIVOT_TOO_SMALL, "pivot element below pivot_tol");
+    if (st == ST_OPTIMAL) return LPSG_OPTIMAL;
+    if (st == ST_UNBOUNDED) return LPSG_UNBOUNDED;
+    if (st == ST_ITER_LIMIT) return LPSG_ITERATION_LIMIT;
+    throw Error(LPSG_CUDA_ERROR, "unexpected control status " + std::to_string(st));
+}
+
+// run_phase (solver.cpp:278-293) one pivot per host round trip, unfused: price,
+// FTRAN + ratio test, [select_leaving], pivot, update without the next FTRAN.
+// After every pivot the device holds exactly the reference's tableau at its
+// observer call (column m+1 included: tiled_engine.cpp:240-242,265), so a
+// view observer with rows can read any row (lpsg_read_row).
+int Solver::run_phase_stepwise() {
+    hctl_->status = ST_RUNNING;
+    hctl_->pending = 0;
+    hctl_->no_ftran = 0;
+    hctl_->no_ratio = unfused_ratio_ ? 1 : 0;
+    hctl_->phase = phase_;
+    push();
+    for (;;) {
+        seq_price();
+        if (unfused_ratio_) {
+            seq_update();  // FTRAN only
+            L(K_RATIO, bytes_of(K_RATIO), [&] { launch_ratio(d_, st_); });
+        } else {
+            seq_update();  // FTRAN + fused ratio test
+        }
+        CK(cudaGetLastError());
+        pull(false);
+        if (prof_) flush_profile();
+        const int st = hctl_->status;
+        if (st != ST_RUNNING) {
+            bool resumed = false;
+            const int out = handle_stop(st, &resumed);
+            if (!resumed) return out;
+        }
+        seq_pivot();
+        CK(cudaMemcpyAsync(&d_.ctl->no_ftran, hone_, sizeof(int), cudaMemcpyHostToDevice, st_));
+        seq_update();  // the rank-1 update only
+        CK(cudaGetLastError());
+        pull(true);
+        if (prof_) flush_profile();
+        if (hctl_->status == ST_PIVOT_ERR) throw Error(LPSG_PIVOT_TOO_SMALL, "pivot element below pivot_tol");
+        drain_log();
+        hctl_->no_ftran = 0;
+        push();
     }
 }
 
@@ -968,7 +1117,7 @@ void Solver::solve(lpsg_report* rep) {
         status = LPSG_OPTIMAL;
         bool finished = false;
         if (phase_ == 1) {
-            const int st = run_phase();
+            const int st = view_rows ? run_phase_stepwise() : run_phase();
             if (st == LPSG_ITERATION_LIMIT) {
                 status = LPSG_ITERATION_LIMIT;
                 finished = true;
@@ -980,7 +1129,7 @@ void Solver::solve(lpsg_report* rep) {
                 enter_phase2();
             }
         }
-        if (!finished) status = run_phase();
+        if (!finished) status = view_rows ? run_phase_stepwise() : run_phase();
         done_ = status != LPSG_ITERATION_LIMIT;
     }
     hctl_->status = ST_HOLD;
@@ -1302,6 +1451,55 @@ int lpsg_solve_sharded(const lpsg_problem* lp, const lpsg_config* cfg, int shard
         lpsg::g_err = "lpsg_solve_sharded: no CUDA device available (the solver has no CPU fallback)";
         return LPSG_CUDA_ERROR;
     }
+    if (p2p && !spread && shards > 1) {
+        // P2P shards sharing one GPU spin-wait on each other's flags, so every
+        // shard's stream needs its own hardware work queue; the CUDA runtime sizes
+        // them from CUDA_DEVICE_MAX_CONNECTIONS when the context is created
+        // (default 8). The library never sets it itself (it would change every
+        // other CUDA user of the process); the caller exports it before the
+        // first CUDA call (tests/conftest.py does).
+        const char* e = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+        if (!e || atoi(e) < 2 * shards)
+            return bad("lpsg_solve_sharded: P2P shards sharing one GPU need CUDA_DEVICE_MAX_CONNECTIONS >= "
+                       "2 * shards in the environment before the CUDA context is created");
+    }
+    // One column-major A per device, shared read-only by the shards placed on
+    // it (C5: 9.2 GB once instead of once per shard).
+    std::vector<double*> shared_A(ndev, nullptr);
+    struct SharedAFree {
+        std::vector<double*>& v;
+        ~SharedAFree() {
+            for (size_t dv = 0; dv < v.size(); ++dv)
+                if (v[dv]) {
+                    cudaSetDevice((int)dv);
+                    cudaFree(v[dv]);
+                }
+        }
+    } shared_A_free{shared_A};
+    {
+        const int rc = guard([&] {
+            for (int g = 0; g < shards; ++g) {
+                const int dv = spread ? (c.device + g) % ndev : c.device;
+                if (dv < 0 || dv >= ndev) throw lpsg::Error(LPSG_INVALID_ARGUMENT, "lpsg_solve_sharded: bad device");
+                if (shared_A[dv] || lp->m <= 0 || lp->n_total <= 0 || !lp->A) continue;
+                CK_SET_DEVICE(dv);
+                const long long ld = (lp->m + 3) / 4 * 4;  // Solver's ld_cm
+                void* p = nullptr;
+                lpsg::ck(cudaMalloc(&p, sizeof(double) * ((size_t)lp->n_total * ld + 64)), "cudaMalloc(A_cm)");
+                shared_A[dv] = static_cast<double*>(p);
+                cudaStream_t st = nullptr;
+                lpsg::ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "cudaStreamCreate");
+                try {
+                    lpsg::upload_A_cm(*lp, shared_A[dv], ld, st);
+                } catch (...) {
+                    cudaStreamDestroy(st);
+                    throw;
+                }
+                cudaStreamDestroy(st);
+            }
+        });
+        if (rc != LPSG_OK) return rc;
+    }
     lpsg::LocalHub hub(shards);
     std::vector<char*> bases(shards, nullptr);
     std::vector<int> rc(shards, LPSG_OK);
@@ -1337,7 +1535,7 @@ int lpsg_solve_sharded(const lpsg_problem* lp, const lpsg_config* cfg, int shard
                 } else {
                     comm = lpsg::make_local_comm(&hub, g);
                 }
-                lpsg::Solver s(*lp, cg, comm.get());
+                lpsg::Solver s(*lp, cg, comm.get(), shared_A[cg.device]);
                 s.keep_trace = g == 0 && trace != nullptr;
                 lpsg_report r{};
                 s.solve(&r);
@@ -1405,6 +1603,21 @@ int lpsg_set_observer(lpsg_solver* s, lpsg_observer cb, void* user) {
     if (!s) return bad("lpsg_set_observer: null solver");
     s->s->observer = cb;
     s->s->observer_user = user;
+    return LPSG_OK;
+}
+
+int lpsg_set_view_observer(lpsg_solver* s, lpsg_view_observer cb, void* user, int with_rows) {
+    if (!s) return bad("lpsg_set_view_observer: null solver");
+    s->s->view_observer = cb;
+    s->s->view_user = user;
+    s->s->view_rows = cb != nullptr && with_rows != 0;
+    s->s->handle = s;
+    return LPSG_OK;
+}
+
+int lpsg_get_memory(lpsg_solver* s, lpsg_memory* out) {
+    if (!s || !out) return bad("lpsg_get_memory: null argument");
+    *out = s->s->memory();
     return LPSG_OK;
 }
 

@@ -22,6 +22,7 @@ import statistics
 from dataclasses import dataclass
 from typing import Callable, List, Optional, Sequence
 
+from .lp_model import _cxx_to_string
 from .solver import (Error, GenSpec, SimplexSolver, SolverConfig, SolveStatus, StandardFormLP,
                      generate)
 
@@ -41,7 +42,7 @@ class ZeroIterations(Error):
 
 def speedup(t_ref: float, t_par: float) -> float:
     if t_par <= 0.0:
-        raise NonPositiveTime(f"speedup: t_par must be positive, got {t_par}")
+        raise NonPositiveTime(f"speedup: t_par must be positive, got {_cxx_to_string(t_par)}")
     return t_ref / t_par
 
 

@@ -84,13 +84,14 @@ class SolverConfig:
     ratio_tie_tol: float = 1e-9
     max_iter: int = 0
     anticycle: Anticycle = Anticycle.tabu
-    kernel: int = 0          # accepted, ignored (simulation knob, solver.hpp:42)
+    kernel: int = 0          # KernelMode (tiled_engine.hpp): 0 cached (zero-skip), 1 naive
+                             # (every element stored); the two differ only in zero signs
     workers: int = 1         # accepted, ignored (solver.hpp:43)
     device: int = 0
     batch: int = 0
     use_graphs: bool = True
-    debug_flags: int = 0     # bit 0: standalone ratio kernel instead of the fused epilogue
     observer: Optional[Callable[["IterationView"], None]] = None
+    observer_rows: bool = False  # view.row(i) readable in the observer (unfused, one pivot per round trip)
     # sharded solve over NCCL: one process per GPU, same problem
     # and config on every rank, nccl_id from nccl_unique_id() on rank 0
     world_size: int = 1
@@ -98,8 +99,9 @@ class SolverConfig:
     nccl_id: bytes = b""
     nccl_single: bool = False  # run the NCCL exchange path even for world_size 1 (testing)
     peer: Optional["PeerHeap"] = None  # P2P transport (NVLink stores + flags) instead of NCCL
-    experiment: int = 0        # kernel experiment knobs (bits 0-3: results NOT valid; bit 4:
-                               # exact-select lookahead, valid); 0 = production
+    # verification modes, result-identical to the default (tests/test_gpu_parity.py):
+    unfused_ratio: bool = False           # standalone ratio-test kernel, not the fused epilogue
+    lookahead_exact_select: bool = False  # theta' keeps the y_i == 0 select
 
     def _c(self) -> L.Config:
         c = L.Config()
@@ -108,11 +110,14 @@ class SolverConfig:
         c.ratio_tie_tol, c.max_iter = self.ratio_tie_tol, int(self.max_iter)
         c.anticycle, c.kernel, c.workers = int(self.anticycle), int(self.kernel), int(self.workers)
         c.device, c.batch, c.use_graphs = int(self.device), int(self.batch), int(self.use_graphs)
-        c.reserved[0] = int(self.debug_flags)
+        c.reserved[0] = 1 if self.unfused_ratio else 0
         c.world_size, c.rank = int(self.world_size), int(self.rank)
         c.reserved[1] = 1 if self.nccl_single else 0
         c.peer = self.peer.ptr if self.peer is not None else None
-        c.reserved[2] = int(self.experiment)
+        # (tools/dbg set `_experiment` on an instance; it only has an effect in
+        # the -DLPSG_EXPERIMENTS library, LPSG_EXPERIMENTS_LIB=1)
+        c.reserved[2] = (16 if self.lookahead_exact_select else 0) | (
+            int(getattr(self, "_experiment", 0)) & ~16)
         if self.nccl_id:
             if len(self.nccl_id) != 128:
                 raise Error("nccl_id must be 128 bytes")
@@ -122,13 +127,27 @@ class SolverConfig:
 
 @dataclass
 class IterationView:
-    """Per-pivot snapshot (solver.hpp:21-32) minus the tableau rows."""
+    """Per-pivot snapshot (solver.hpp:21-32): phase, cumulative iteration,
+    T[0][m], the whole basis, the pivot (row, leaving, entering), the memory
+    counters, and -- with SolverConfig.observer_rows -- `row(i)`, the i-th
+    tableau row of row_width doubles (row 0 = [W | obj | d])."""
     phase: int
     iteration: int
     objective: float
     row: int
     leaving: int
     entering: int
+    basic: np.ndarray = None
+    num_rows: int = 0
+    row_width: int = 0
+    counters: dict = None
+    _read: Optional[Callable[[int], np.ndarray]] = None
+
+    def tableau_row(self, i: int) -> np.ndarray:
+        """IterationView::row(i) (solver.hpp:29); needs SolverConfig.observer_rows."""
+        if self._read is None:
+            raise Error("IterationView.tableau_row: enable SolverConfig.observer_rows")
+        return self._read(i)
 
 
 @dataclass
@@ -142,6 +161,7 @@ class SolveReport:
     total_seconds: float = 0.0
     tpi_seconds: float = 0.0
     case_used: str = "InCore"
+    memory: dict = field(default_factory=dict)  # MemoryCounters counterpart (include/lpsg.h lpsg_memory)
 
     @property
     def iterations(self) -> int:
@@ -267,14 +287,24 @@ class SimplexSolver:
         self._cb = None
         if self.cfg.observer is not None:
             obs = self.cfg.observer
+            rows = bool(self.cfg.observer_rows)
+            width = lp.m + 2
+
+            def _read(h, i):
+                out = np.zeros(width)
+                _check(self.lib.lpsg_read_row(h, i, out.ctypes.data_as(C.POINTER(C.c_double))))
+                return out
 
             def _tramp(p, _user):
-                t = p.contents
-                obs(IterationView(t.phase, t.iteration, t.objective, t.row, t.leaving,
-                                  t.entering))
+                v = p.contents
+                basic = np.ctypeslib.as_array(v.basic, (v.num_rows,)).copy()
+                mem = v.counters.contents
+                obs(IterationView(v.phase, v.iteration, v.objective, v.row, v.leaving, v.entering,
+                                  basic, v.num_rows, v.row_width, _mem_dict(mem),
+                                  (lambda i, h=v.solver: _read(h, i)) if rows else None))
 
-            self._cb = L.OBSERVER(_tramp)
-            _check(self.lib.lpsg_set_observer(self._h, self._cb, None))
+            self._cb = L.VIEW_OBSERVER(_tramp)
+            _check(self.lib.lpsg_set_view_observer(self._h, self._cb, None, int(rows)))
 
     def close(self) -> None:
         if self._h:
@@ -312,7 +342,14 @@ class SimplexSolver:
         _check(self.lib.lpsg_get_x(self._h, x.ctypes.data_as(C.POINTER(C.c_double)),
                                    self.lp.n_total))
         return SolveReport(SolveStatus(rep.status), rep.objective, x, rep.iterations_phase1,
-                           rep.iterations_phase2, rep.total_seconds, rep.tpi_seconds)
+                           rep.iterations_phase2, rep.total_seconds, rep.tpi_seconds,
+                           memory=self.memory())
+
+    def memory(self) -> dict:
+        """SolveReport::memory counterpart (include/lpsg.h lpsg_memory)."""
+        m = L.Memory()
+        _check(self.lib.lpsg_get_memory(self._h, C.byref(m)))
+        return _mem_dict(m)
 
     # ---- measurement (extensions; include/lpsg.h "measurement")
     def set_max_iter(self, max_iter: int) -> None:
@@ -415,6 +452,10 @@ class SimplexSolver:
 
     def phase(self) -> int:
         return self.lib.lpsg_phase(self._h)
+
+
+def _mem_dict(m) -> dict:
+    return {k: int(getattr(m, k)) for k, _ in L.Memory._fields_}
 
 
 def two_phase_solve(lp: StandardFormLP, cfg: Optional[SolverConfig] = None) -> SolveReport:

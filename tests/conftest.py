@@ -3,8 +3,14 @@ import glob
 import os
 import sys
 
-import numpy as np
-import pytest
+# P2P shards that share one GPU (tests/test_gpu_sharded.py) need one hardware
+# work queue per shard stream; the CUDA runtime reads this when the context is
+# created, so it is set before anything touches CUDA (the library itself never
+# sets it: include/lpsg.h lpsg_solve_sharded).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
+import numpy as np  # noqa: E402
+import pytest  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
@@ -41,6 +47,7 @@ class Golden:
         self.max_iter = int(z["cfg_max_iter"])
         self.anticycle = int(z["cfg_anticycle"])
         self.pivot_tol = float(z["cfg_pivot_tol"])
+        self.kernel = int(z["cfg_kernel"]) if "cfg_kernel" in z.files else 0  # 1: KernelMode::naive
         self.spec = tuple(int(v) for v in z["spec"]) if "spec" in z.files else None
 
     def arrays(self, generate=None):
@@ -57,7 +64,7 @@ class Golden:
 
     def config_kwargs(self):
         return dict(max_iter=self.max_iter, anticycle="none" if self.anticycle else "tabu",
-                    pivot_tol=self.pivot_tol)
+                    pivot_tol=self.pivot_tol, kernel="naive" if self.kernel else "cached")
 
 
 @pytest.fixture(scope="session")

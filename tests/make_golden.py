@@ -58,7 +58,8 @@ def save(name: str, lp: LP, out, cfg: dict, spec=None, sparse=True) -> None:
              trace=out.trace, trace_len=out.trace_len, digest=lp_digest(lp),
              cfg_max_iter=cfg.get("max_iter", 0),
              cfg_anticycle=1 if cfg.get("anticycle") == "none" else 0,
-             cfg_pivot_tol=cfg.get("pivot_tol", 1e-9))
+             cfg_pivot_tol=cfg.get("pivot_tol", 1e-9),
+             cfg_kernel=1 if cfg.get("kernel") == "naive" else 0)
     if spec is not None:
         d["spec"] = np.array(spec, np.int64)
     else:
@@ -67,9 +68,30 @@ def save(name: str, lp: LP, out, cfg: dict, spec=None, sparse=True) -> None:
     np.savez_compressed(os.path.join(GOLDEN, name + ".npz"), **d)
 
 
+# KernelMode::naive (tiled_engine.cpp:61-77): every element stored, no zero
+# skip. On these inputs it changes the signs of zeros in x (BOEING2: 26, E226: 1).
+NAIVE_NETLIB = ["boeing2", "e226"]
+
+
+def naive_fixtures(ref) -> None:
+    over = {"kernel": "naive"}
+    for stem in NAIVE_NETLIB:
+        lp = ref.from_mps(os.path.join(NETLIB, stem + ".mps"))
+        out = ref.solve(lp, make_config(**over))
+        save(f"netlib_{stem}_naive", lp, out, over)
+        print(f"netlib_{stem}_naive", out.status_name, out.trace_len)
+    lp = ref.generate(256, 512, 1, 2)
+    out = ref.solve(lp, make_config(**over))
+    save("gen_256x512_f2_s1_naive", lp, out, over, spec=(256, 512, 2, 1, 0))
+    print("gen_256x512_f2_s1_naive", out.status_name, out.trace_len)
+
+
 def main() -> None:
     os.makedirs(GOLDEN, exist_ok=True)
     ref = Ref()
+    naive_fixtures(ref)
+    if sys.argv[1:] == ["naive"]:
+        return
     for rows, cols, form, seed, over in GENERATED:
         lp = ref.generate(rows, cols, seed, form)
         out = ref.solve(lp, make_config(**over))

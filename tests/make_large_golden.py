@@ -29,6 +29,8 @@ CASES = {
     "c4_p3": (4000, 8000, 2, 1, {"max_iter": 3, "workers": 1}),
     "c5_p10": (24000, 48000, 0, 1, {"max_iter": 10, "workers": 8}),
     "c4_p20": (4000, 8000, 2, 1, {"max_iter": 20, "workers": 1}),
+    "c5_p100": (24000, 48000, 0, 1, {"max_iter": 100, "workers": 8}),
+    "c4_p60": (4000, 8000, 2, 1, {"max_iter": 60, "workers": 1}),
 }
 
 

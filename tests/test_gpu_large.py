@@ -3,9 +3,13 @@ compiled reference (tests/golden/large/, made by tests/make_large_golden.py).
 
   c2_full  C2 m=2000 n=4000 solved to optimality: every pivot, bit for bit
   c3_p200  C3 m=8000 n=16000, first 200 pivots (the headline config)
+  c3_full  C3 solved to the reference's final status (67 548 phase-1 pivots, Infeasible)
   c4_p3    C4 m=4000 n=8000 degenerate, first 3 pivots: each is a ~1000-way ratio
-           tie resolved by the batched tabu lookahead (the reference needs ~3 min
-           per pivot on one core)
+  c4_p20   tie resolved by the batched tabu lookahead (the reference needs ~3 min
+           per pivot on one core); first 20 pivots
+  c5_p10   C5 m=24000 n=48000, first 10 pivots
+
+each on one GPU and split over 2 / 4 / 8 shards (the 8-GPU deployment shape),
 
 plus size-independent properties of the final C2 point (feasibility residual,
 reported objective == c.x) that hold without a reference run.
@@ -76,13 +80,33 @@ def test_large_single_gpu(name):
     _check(z, rep, tr, name)
 
 
+@pytest.mark.parametrize("shards", [2, 4, 8])
 @pytest.mark.parametrize("name", NAMES)
-def test_large_sharded(name):
-    """The same runs split over 4 shards (rows of B^-1 / pricing columns)."""
+def test_large_sharded(name, shards):
+    """The same runs split over 2 / 4 / 8 shards (rows of B^-1 and pricing
+    columns), in-process on one GPU. 8 is BASELINE's deployment shape for C3
+    and C5: per shard h = 8-row update CTAs (C3), the narrow one-chain pricing
+    path (n/8 columns per shard) and, on the C4 ~1000-way ties, ratio-test
+    messages that overflow (> 30 local candidates) into the host gather."""
     P = _P()
     z, lp = _load(name)
-    rep, tr = P.solve_sharded(lp, P.SolverConfig(max_iter=int(z["cfg_max_iter"])), shards=4, trace=True)
-    _check(z, rep, tr, (name, 4))
+    rep, tr = P.solve_sharded(lp, P.SolverConfig(max_iter=int(z["cfg_max_iter"])), shards=shards,
+                              trace=True)
+    _check(z, rep, tr, (name, shards))
+
+
+@pytest.mark.skipif("not __import__('paper_1803_04378_b200').device_count() > 1",
+                    reason="one GPU: the spread placement needs several devices")
+@pytest.mark.parametrize("name", [n for n in NAMES if n in ("c3_p200", "c4_p20", "c5_p10")])
+def test_large_sharded_spread(name):
+    """Shard g on device g % device_count (LPSG_SHARD_SPREAD): the deployment
+    placement, one shard per GPU, P2P exchanges over NVLink."""
+    P = _P()
+    z, lp = _load(name)
+    shards = min(8, P.device_count())
+    rep, tr = P.solve_sharded(lp, P.SolverConfig(max_iter=int(z["cfg_max_iter"])), shards=shards,
+                              trace=True, spread_devices=True, p2p=True)
+    _check(z, rep, tr, (name, shards, "spread"))
 
 
 @pytest.mark.skipif("c2_full" not in NAMES, reason="c2_full fixture not generated")

@@ -36,7 +36,7 @@ def test_nccl_one_rank_golden_parity(name):
     else:
         A, b, c, ck = g.arrays()
         lp = P.StandardFormLP(g.m, g.n_total, A, b, c, ck)
-    cfg = P.SolverConfig(max_iter=g.max_iter, pivot_tol=g.pivot_tol,
+    cfg = P.SolverConfig(max_iter=g.max_iter, pivot_tol=g.pivot_tol, kernel=g.kernel,
                          anticycle=P.Anticycle(g.anticycle), nccl_single=True,
                          nccl_id=P.nccl_unique_id())
     with P.SimplexSolver(lp, cfg) as s:

@@ -60,7 +60,7 @@ def test_golden_trace_parity(name):
     P = _P()
     g = Golden(name)
     lp = _golden_lp(g)
-    rep, tr = _solve_traced(lp, max_iter=g.max_iter, pivot_tol=g.pivot_tol,
+    rep, tr = _solve_traced(lp, max_iter=g.max_iter, pivot_tol=g.pivot_tol, kernel=g.kernel,
                             anticycle=P.Anticycle(g.anticycle))
     assert int(rep.status) == g.status, (name, rep.status, g.status)
     assert (rep.iterations_phase1, rep.iterations_phase2) == (g.p1, g.p2), name
@@ -79,11 +79,11 @@ TIE_NAMES = [n for n in NAMES if "_f2_" in n or n.startswith("beale")]
 def test_lookahead_exact_select_path(name):
     """The lookahead's theta kernel drops the y_i == 0 select when every X_kj
     is finite (a zero-sign-only difference). Forcing the select
-    path (experiment bit 16) must give the same pivots, bit for bit."""
+    path (lookahead_exact_select) must give the same pivots, bit for bit."""
     P = _P()
     g = Golden(name)
-    rep, tr = _solve_traced(_golden_lp(g), max_iter=g.max_iter, pivot_tol=g.pivot_tol,
-                            anticycle=P.Anticycle(g.anticycle), experiment=16)
+    rep, tr = _solve_traced(_golden_lp(g), max_iter=g.max_iter, pivot_tol=g.pivot_tol, kernel=g.kernel,
+                            anticycle=P.Anticycle(g.anticycle), lookahead_exact_select=True)
     assert int(rep.status) == g.status
     _assert_trace(tr, g.trace[: g.trace_len], name)
     assert np.array_equal(_bits(rep.x), _bits(g.x)), name
@@ -134,6 +134,56 @@ def test_observer_sees_every_pivot_in_order():
     assert len(seen) == rep.iterations
     assert [v.iteration for v in seen] == list(range(1, rep.iterations + 1))
     assert seen[-1].objective == rep.objective
+
+
+@pytest.mark.parametrize("name", ["gen_128x256_f2_s5", "netlib_afiro", "netlib_scsd1", "beale_3x7",
+                                  "driveout_30x60_sum", "gen_96x160_f1_s4"])
+def test_observer_rows_schedule_matches_golden(name):
+    """observer_rows switches to the unfused one-pivot-per-round-trip schedule
+     so IterationView.row(i) reads the reference's tableau at its
+    observer call: same golden trace, objective and x bits; the basis in every
+    view follows the trace; row 0 column m is the view's objective."""
+    P = _P()
+    g = Golden(name)
+    seen = []
+
+    def obs(v):
+        r0 = v.tableau_row(0)
+        seen.append((v.iteration, v.row, v.entering, v.basic.copy(), r0[g.m], v.objective,
+                     v.counters["device_read_bytes"]))
+
+    cfg = P.SolverConfig(max_iter=g.max_iter, pivot_tol=g.pivot_tol, kernel=g.kernel,
+                         anticycle=P.Anticycle(g.anticycle), observer=obs, observer_rows=True)
+    with P.SimplexSolver(_golden_lp(g), cfg) as s:
+        s.keep_trace(True)
+        rep = s.solve()
+        tr = s.trace()
+    _assert_trace(tr, g.trace[: g.trace_len], name)
+    assert np.array_equal(_bits(rep.x), _bits(g.x)), name
+    assert len(seen) == len(tr)
+    for (it, row, ent, basic, obj_row, obj, rd), t in zip(seen, tr):
+        assert it == t["iteration"] and row == t["row"] and ent == t["entering"]
+        assert basic[row] == ent
+        assert _bits(obj_row) == _bits(obj) == _bits(t["objective"])
+    assert all(b[6] > a[6] for a, b in zip(seen, seen[1:]))  # counters grow
+    assert rep.memory["device_read_bytes"] >= seen[-1][6] and rep.memory["kernel_launches"] > 0
+
+
+def test_observer_view_carries_the_basis():
+    P = _P()
+    seen = []
+    lp = P.generate(P.GenSpec(64, 128, seed=2, form=P.Form.equality))
+    with P.SimplexSolver(lp, P.SolverConfig(observer=seen.append)) as s:
+        b0 = s.basis().copy()
+        rep = s.solve()
+        final = s.basis()
+    basis = b0
+    for v in seen:
+        basis[v.row] = v.entering
+        assert np.array_equal(v.basic, basis)
+        with pytest.raises(P.Error):
+            v.tableau_row(0)  # rows need observer_rows
+    assert np.array_equal(basis, final) and len(seen) == rep.iterations
 
 
 # ---- step API: SPEC.md operation examples (SPEC.md:171-209) -----------------
@@ -200,17 +250,35 @@ def test_pivot_too_small_raises():
             s.pivot_update(1, p.entering)  # y_1 = 0
 
 
-def test_lookahead_scores_match_port_select(port):
-    """select_leaving on a degenerate tie equals the port's choice (full solve
-    parity already covers it; this checks the scores are finite/ordered)."""
+@pytest.mark.parametrize("name", ["netlib_scsd1", "netlib_lotfi", "netlib_e226", "netlib_sctap1",
+                                  "netlib_boeing2", "netlib_grow7"])
+def test_lookahead_scores_match_port_bitwise(port, name):
+    """lookahead_score (solver.cpp:164-213) values, bit for bit: the port
+    records every tie select_leaving scores (pivots done, entering, survivors,
+    scores; oracle/lps_oracle.c lpo_set_tie_log). For up to 8 ties with
+    nonzero scores the device solver runs to the same pivot count, re-prices
+    and re-runs compute_direction through the step API, and its batched
+    lookahead must return the identical doubles."""
+    from oracle.oracle import LP, make_config
     P = _P()
-    lp = _lp([[2, 1, 0], [3, 0, 1]], [4, 6], [-1, 0, 0], [0, 1, 1])
-    with P.SimplexSolver(lp) as s:
-        p = s.price()
-        s.compute_direction(p.entering, p.reduced_cost)
-        sc = s.lookahead_scores([0, 1], p.entering)
-        assert sc.shape == (2,)
-        assert s.select_leaving([0, 1], p.entering) in (0, 1)
+    g = Golden(name)
+    A, b, c, ck = g.arrays()
+    cfg = make_config(**g.config_kwargs())
+    _, ties = port.solve_with_ties(LP(g.m, g.n_total, A, b, c, ck), cfg, cap_ties=4096,
+                                   cap_rows=1 << 20)
+    scored = [t for t in ties if np.any(t[3] != 0)]
+    assert scored, name
+    pick = scored[:: max(1, len(scored) // 8)][:8]
+    lp = _golden_lp(g)
+    for it, q, rows, want in pick:
+        with P.SimplexSolver(lp, P.SolverConfig(max_iter=it, pivot_tol=g.pivot_tol)) as s:
+            rep = s.solve()
+            assert rep.status == P.SolveStatus.iteration_limit and rep.iterations == it
+            pr = s.price()
+            assert not pr.optimal and pr.entering == q, (name, it)
+            s.compute_direction(pr.entering, pr.reduced_cost)
+            got = s.lookahead_scores([int(r) for r in rows], q)
+            assert np.array_equal(_bits(got), _bits(want)), (name, it, got, want)
 
 
 def test_non_finite_costs_or_coefficients_are_rejected():
@@ -231,6 +299,46 @@ def test_non_finite_costs_or_coefficients_are_rejected():
             c2[1] = bad_c
         with pytest.raises(P.Error, match="inf/NaN"):
             P.two_phase_solve(P.StandardFormLP(2, 4, A2, b, c2, ck))
+
+
+def test_rejected_create_releases_device_memory():
+    """A create that fails after the device buffers exist (here: inf in A,
+    found by the upload's transpose) releases every one of them:
+    m = 2000 allocates ~100 MB per attempt."""
+    P = _P()
+    import torch
+    lp = P.generate(P.GenSpec(2000, 4000, seed=1))
+    A = lp.A.copy()
+    A[1999, 3999] = np.inf
+    bad = P.StandardFormLP(lp.m, lp.n_total, A, lp.b, lp.c, lp.col_kind)
+    with pytest.raises(P.Error, match="inf/NaN"):
+        P.SimplexSolver(bad)
+    torch.cuda.synchronize()
+    free0 = torch.cuda.mem_get_info(0)[0]
+    for _ in range(6):
+        with pytest.raises(P.Error, match="inf/NaN"):
+            P.SimplexSolver(bad)
+    torch.cuda.synchronize()
+    free1 = torch.cuda.mem_get_info(0)[0]
+    assert free0 - free1 < 64 << 20, (free0, free1)
+
+
+def test_naive_kernel_mode_changes_only_zero_signs():
+    """KernelMode::naive stores every element (tiled_engine.cpp:61-77). On
+    BOEING2 that turns 26 of x's -0.0 into +0.0; the naive golden fixtures
+    (netlib_*_naive, made by the reference with kernel=naive) pin those bits,
+    and the cached run of the same LP keeps its -0.0s."""
+    P = _P()
+    g = Golden("netlib_boeing2_naive")
+    assert g.kernel == 1
+    lp = _golden_lp(g)
+    rep_n, _ = _solve_traced(lp, kernel=1)
+    rep_c, _ = _solve_traced(lp, kernel=0)
+    assert np.array_equal(_bits(rep_n.x), _bits(g.x))
+    neg0 = lambda x: int(np.sum(np.signbit(x) & (x == 0)))  # noqa: E731
+    assert neg0(rep_n.x) == 0 and neg0(rep_c.x) == 26
+    with pytest.raises(P.Error, match="kernel"):
+        P.SimplexSolver(lp, P.SolverConfig(kernel=2))
 
 
 def test_infinite_rhs_matches_port(port):
@@ -264,3 +372,28 @@ def test_fp64_peak_probe():
     P = _P()
     v = P.fp64_peak(0)
     assert 5.0 < v < 40.0, v
+
+
+@pytest.mark.parametrize("nan_rows", [[0], [0, 4, 8, 148], [2, 150, 299]])
+def test_nan_rhs_matches_port(port, nan_rows):
+    """NaN entries of b (some at the first row of an update CTA, m = 300 gives
+    4-row CTAs) make those rows' ratios NaN. std::min(theta, NaN) keeps theta
+    (solver.cpp:147), so they must never win the fused ratio test's CTA
+    minimum. Port pinned to the reference on these inputs in
+    tests/test_oracle.py::test_port_nan_rhs_matches_reference."""
+    P = _P()
+    from oracle.oracle import LP, make_config
+    lp = P.generate(P.GenSpec(300, 400, seed=7, form=P.Form.le_max))
+    b = lp.b.copy()
+    b[nan_rows] = np.nan
+    ref = port.solve(LP(lp.m, lp.n_total, lp.A, b, lp.c, lp.col_kind), make_config(max_iter=200))
+    rep, tr = _solve_traced(P.StandardFormLP(lp.m, lp.n_total, lp.A, b, lp.c, lp.col_kind),
+                            max_iter=200)
+    assert int(rep.status) == ref.status
+    want = ref.trace[: ref.trace_len]
+    assert len(tr) == len(want)
+    for f in ("iteration", "phase", "row", "leaving", "entering"):
+        assert np.array_equal(tr[f], want[f]), f
+    x, w = rep.x, ref.x
+    assert np.array_equal(np.isnan(x), np.isnan(w))
+    assert np.array_equal(_bits(x[~np.isnan(x)]), _bits(w[~np.isnan(w)]))

@@ -59,7 +59,7 @@ def test_sharded_golden_parity(name, shards):
     if shards > g.m:
         pytest.skip("fewer rows than shards")
     lp = _golden_lp(g)
-    cfg = P.SolverConfig(max_iter=g.max_iter, pivot_tol=g.pivot_tol,
+    cfg = P.SolverConfig(max_iter=g.max_iter, pivot_tol=g.pivot_tol, kernel=g.kernel,
                          anticycle=P.Anticycle(g.anticycle))
     rep, tr = P.solve_sharded(lp, cfg, shards=shards, trace=True)
     _check(rep, tr, g, (name, shards))
@@ -84,7 +84,7 @@ def test_sharded_p2p_golden_parity(name, shards):
     if shards > g.m:
         pytest.skip("fewer rows than shards")
     lp = _golden_lp(g)
-    cfg = P.SolverConfig(max_iter=g.max_iter, pivot_tol=g.pivot_tol,
+    cfg = P.SolverConfig(max_iter=g.max_iter, pivot_tol=g.pivot_tol, kernel=g.kernel,
                          anticycle=P.Anticycle(g.anticycle))
     rep, tr = P.solve_sharded(lp, cfg, shards=shards, trace=True, p2p=True)
     _check(rep, tr, g, (name, shards, "p2p"))
@@ -100,7 +100,7 @@ def test_sharded_more_shards(name, shards):
     if shards > g.m:
         pytest.skip("fewer rows than shards")
     lp = _golden_lp(g)
-    cfg = P.SolverConfig(max_iter=g.max_iter, pivot_tol=g.pivot_tol,
+    cfg = P.SolverConfig(max_iter=g.max_iter, pivot_tol=g.pivot_tol, kernel=g.kernel,
                          anticycle=P.Anticycle(g.anticycle))
     rep, tr = P.solve_sharded(lp, cfg, shards=shards, trace=True)
     _check(rep, tr, g, (name, shards))

@@ -30,8 +30,8 @@ def test_tpi_and_speedup_rules():
     with pytest.raises(H.ZeroIterations):
         H.tpi(1.0, 0)
     assert H.speedup(10.0, 2.0) == 5.0
-    with pytest.raises(H.NonPositiveTime):
-        H.speedup(1.0, 0.0)
+    with pytest.raises(H.NonPositiveTime, match=r"^speedup: t_par must be positive, got 0\.000000$"):
+        H.speedup(1.0, 0.0)  # std::to_string formatting (bench.cpp:16-17)
     assert H.status_name(H.SolveStatus.optimal) == "Optimal"
     assert H.status_name(H.SolveStatus.iteration_limit) == "IterationLimit"
 

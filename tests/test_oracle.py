@@ -115,3 +115,24 @@ def test_spec_pivot_example_on_port(port):
     assert out.status == 0 and out.objective == -2.0
     assert out.trace_len == 1
     assert out.trace[0]["entering"] == 0
+
+
+@pytest.mark.skipif(not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "liblps_ref.so")),
+                    reason="compiled reference not present")
+@pytest.mark.parametrize("nan_rows", [[0], [0, 4, 8, 148], [2, 150, 299]])
+def test_port_nan_rhs_matches_reference(port, nan_rows):
+    """Pins the port on NaN right-hand sides (the GPU test of the same inputs
+    compares against the port: tests/test_gpu_parity.py::test_nan_rhs_matches_port)."""
+    from oracle.oracle import LP, Ref, make_config
+    ref = Ref()
+    lp = ref.generate(300, 400, 7, 1)
+    b = lp.b.copy()
+    b[nan_rows] = np.nan
+    l2 = LP(lp.m, lp.n_total, lp.A, b, lp.c, lp.col_kind)
+    a = ref.solve(l2, make_config(max_iter=200))
+    p = port.solve(l2, make_config(max_iter=200))
+    assert a.status == p.status and a.trace_len == p.trace_len
+    for f in ("iteration", "phase", "row", "leaving", "entering"):
+        assert np.array_equal(a.trace[f], p.trace[f]), f
+    assert np.array_equal(np.isnan(a.x), np.isnan(p.x))
+    assert _bits_equal(a.x[~np.isnan(a.x)], p.x[~np.isnan(p.x)])

@@ -5,10 +5,16 @@ pivots). Usage: PYTHONPATH=. python tools/dbg/price_rate_probe.py [m] [bits,bits
 import sys
 import paper_1803_04378_b200 as P
 
+
+def _xcfg(cfg, exp):
+    cfg._experiment = exp  # knobs live only in the LPSG_EXPERIMENTS_LIB=1 build
+    return cfg
+
+
 m = int(sys.argv[1]) if len(sys.argv) > 1 else 2000
 lp = P.generate(P.GenSpec(m, 2 * m, seed=1))
 for exp in [int(v) for v in (sys.argv[2].split(',') if len(sys.argv) > 2 else ['0', '1', '2', '4', '8'])]:
-    s = P.SimplexSolver(lp, P.SolverConfig(max_iter=20, experiment=exp))
+    s = P.SimplexSolver(lp, _xcfg(P.SolverConfig(max_iter=20), exp))
     s.solve()
     s.set_max_iter(220)
     s.profile(True)

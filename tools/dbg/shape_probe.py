@@ -4,10 +4,16 @@ PYTHONPATH=. python tools/dbg/shape_probe.py m n [experiment]"""
 import sys
 import paper_1803_04378_b200 as P
 
+
+def _xcfg(cfg, exp):
+    cfg._experiment = exp  # knobs live only in the LPSG_EXPERIMENTS_LIB=1 build
+    return cfg
+
+
 m, n = int(sys.argv[1]), int(sys.argv[2])
 exp = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 lp = P.generate(P.GenSpec(m, n, seed=1))
-s = P.SimplexSolver(lp, P.SolverConfig(max_iter=20, experiment=exp))
+s = P.SimplexSolver(lp, _xcfg(P.SolverConfig(max_iter=20), exp))
 s.solve()
 s.set_max_iter(220)
 s.profile(True)
