@@ -90,6 +90,15 @@ typedef struct {
      * When set, the shards exchange through device-initiated NVLink stores and
      * flags instead of NCCL (world_size/rank come from the heap). */
     struct lpsg_peer* peer;
+    /* Opt-in periodic reinversion (north_star item 5; NOT the reference's
+     * arithmetic, so results are no longer bit-identical to it): every
+     * `reinvert_every` pivots, and before accepting an optimal or unbounded
+     * phase outcome, B^-1 is rebuilt on the device from the basis columns of
+     * the original A (one Newton-Schulz step from the current inverse, DFMA
+     * GEMMs: csrc/reinvert.cu), then b_bar = B^-1 b and W = c_B^T B^-1.
+     * 0 = off (default: the reference's drifting explicit inverse, bit for
+     * bit). Single GPU only. */
+    long reinvert_every;
 } lpsg_config;
 
 /* lps::SolveReport (solver.hpp:47-57); x is fetched with lpsg_get_x. */
@@ -185,6 +194,11 @@ int lpsg_get_trace(lpsg_solver* s, lpsg_trace* out, long cap, long* len);
 int lpsg_set_view_observer(lpsg_solver* s, lpsg_view_observer cb, void* user, int with_rows);
 /* SolveReport::memory (solver.hpp:55). */
 int lpsg_get_memory(lpsg_solver* s, lpsg_memory* out);
+/* Reinversion mode (lpsg_config.reinvert_every): rebuilds done, Newton steps
+ * taken, max |I - B X| before the last rebuild's first step and after its last
+ * one, and device seconds spent rebuilding. */
+int lpsg_reinvert_stats(lpsg_solver* s, long* rebuilds, long* steps, double* residual_before,
+                        double* residual_after, double* seconds);
 
 /* ---- multi-GPU -------------------------
  * NCCL unique id for lpsg_config.nccl_id (rank 0 creates it, the caller

@@ -26,7 +26,7 @@ class Config(C.Structure):
                 ("kernel", C.c_int), ("workers", C.c_int), ("device", C.c_int),
                 ("batch", C.c_int), ("use_graphs", C.c_int), ("reserved", C.c_int * 6),
                 ("world_size", C.c_int), ("rank", C.c_int), ("nccl_id", C.c_ubyte * 128),
-                ("peer", C.c_void_p)]
+                ("peer", C.c_void_p), ("reinvert_every", C.c_long)]
 
 
 class Report(C.Structure):
@@ -83,6 +83,7 @@ SIGNATURES = [
     ("lpsg_keep_trace", C.c_int, [_P, C.c_int]),
     ("lpsg_set_view_observer", C.c_int, [_P, VIEW_OBSERVER, _P, C.c_int]),
     ("lpsg_get_memory", C.c_int, [_P, C.POINTER(Memory)]),
+    ("lpsg_reinvert_stats", C.c_int, [_P, C.POINTER(C.c_long), C.POINTER(C.c_long), _PD, _PD, _PD]),
     ("lpsg_get_trace", C.c_int, [_P, C.POINTER(Trace), C.c_long, C.POINTER(C.c_long)]),
     ("lpsg_price", C.c_int, [_P, _PI, _PI, _PD]),
     ("lpsg_compute_direction", C.c_int, [_P, C.c_int, C.c_double]),

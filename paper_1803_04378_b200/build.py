@@ -22,7 +22,7 @@ LIB = os.path.join(OUT_DIR, "liblpsg.so")
 LIB_XP = os.path.join(OUT_DIR, "liblpsg_xp.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["kernels.cu", "solver.cu", "comm.cu", "generator.cpp"]
+SOURCES = ["kernels.cu", "solver.cu", "comm.cu", "reinvert.cu", "generator.cpp"]
 HEADERS = ["device.cuh", "comm.h"]
 GENCODE = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "--fmad=false", "-Xcompiler", "-fPIC",

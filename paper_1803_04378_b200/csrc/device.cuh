@@ -275,5 +275,13 @@ void launch_la_score(const Dev& d, LookaheadDev& la, const double* tl, int nsrc,
 void launch_sum_i64(const long long* in, int nsrc, size_t n, long long* out, cudaStream_t st);
 void launch_min_i32(const int* in, int nsrc, size_t n, int* out, cudaStream_t st);
 void launch_gather_row(const Dev& d, int i, double* out, cudaStream_t st);
+// opt-in reinversion (reinvert.cu): column-major C = alpha A B + D (D == nullptr: + I)
+void launch_dgemm_nn(int M, int N, int K, const double* A, long long lda, const double* B, long long ldb, double* C,
+                     long long ldc, double alpha, const double* D, long long ldd, cudaStream_t st);
+void launch_form_basis(const Dev& d, const int* art_row, double* Bm, long long ld, cudaStream_t st);
+void launch_absmax(const double* R, int m, long long ld, unsigned long long* out, cudaStream_t st);
+void launch_gemv_bbar(const Dev& d, const double* b, cudaStream_t st);
+void launch_probe_residual(int m, const double* Bm, long long ldb, const double* X, long long ldx, double* u,
+                           double* w, unsigned long long* out, cudaStream_t st);
 
 }  // namespace lpsg

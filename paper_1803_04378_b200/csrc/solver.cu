@@ -214,6 +214,20 @@ private:
     bool dbg_trace_ = getenv("LPSG_TRACE_COMM") != nullptr;
     int world_ = 1, rank_ = 0;
     double* chain_ = nullptr;     // world > 1: rebuild_top_row partial sums (m+1)
+    // opt-in reinversion (lpsg_config.reinvert_every, csrc/reinvert.cu)
+    long long reinv_every_ = 0;
+    long long reinv_at_ = -1;       // total_iter_ of the last rebuild (-1: none yet)
+    double* b0_ = nullptr;          // the LP's b (device), for b_bar = B^-1 b
+    int* art_row_ = nullptr;        // artificial n_total + k is the unit column of row art_row_[k]
+    std::vector<int> art_row_host_;
+    int run_phase_any();
+    void reinvert();
+
+public:
+    long reinv_count = 0, reinv_steps = 0;
+    double reinv_res_before = 0.0, reinv_res_after = 0.0, reinv_seconds = 0.0;
+
+private:
 
 public:
     // ---- counters and optional per-kernel CUDA-event profile
@@ -421,6 +435,7 @@ void Solver::init(const lpsg_problem& lp) {
         for (int i = 0; i < m; ++i) {
             if (basic_[i] >= 0) continue;
             cost[next] = 1.0;  // c_phase1 of the artificial (solver.cpp:56)
+            art_row_host_.push_back(i);
             basic_[i] = next++;
         }
     }
@@ -454,6 +469,10 @@ void Solver::init(const lpsg_problem& lp) {
     d_.ratio_tie_tol = cfg_.ratio_tie_tol;
     d_.anticycle = cfg_.anticycle;
     if (cfg_.kernel != 0 && cfg_.kernel != 1) throw Error(LPSG_INVALID_ARGUMENT, "lpsg_create: kernel must be 0 (cached) or 1 (naive)");
+    if (cfg_.reinvert_every < 0) throw Error(LPSG_INVALID_ARGUMENT, "lpsg_create: reinvert_every must be >= 0");
+    if (cfg_.reinvert_every > 0 && sharded_)
+        throw Error(LPSG_INVALID_ARGUMENT, "lpsg_create: reinversion is single-GPU only");
+    reinv_every_ = cfg_.reinvert_every;
     d_.naive = cfg_.kernel == 1 ? 1 : 0;
     d_.dbg = cfg_.reserved[2] & ~kLookaheadExactBit;  // perf experiments (-DLPSG_EXPERIMENTS only)
     d_.la_exact = (cfg_.reserved[2] & kLookaheadExactBit) != 0;
@@ -547,6 +566,15 @@ void Solver::init(const lpsg_problem& lp) {
     }
     CK(cudaMemcpyAsync(scratch_, lp.b, sizeof(double) * m, cudaMemcpyHostToDevice, st_));
     launch_init_tableau(d_, scratch_, st_);
+    if (reinv_every_ > 0) {
+        b0_ = dalloc<double>(m);
+        CK(cudaMemcpyAsync(b0_, lp.b, sizeof(double) * m, cudaMemcpyHostToDevice, st_));
+        art_row_ = dalloc<int>(std::max<size_t>(1, art_row_host_.size()));
+        if (!art_row_host_.empty())
+            CK(cudaMemcpyAsync(art_row_, art_row_host_.data(), sizeof(int) * art_row_host_.size(),
+                               cudaMemcpyHostToDevice, st_));
+        CK(cudaStreamSynchronize(st_));  // art_row_host_ is host-pageable
+    }
 
     h2d_bytes += 8LL * m * n + 8LL * m + 8LL * (long long)cost.size() + 4LL * (n_scan + n + m);
     std::memset(hctl_, 0, sizeof(Ctl));
@@ -580,7 +608,7 @@ void Solver::release() {
     void* bufs[] = {d_.T, d_.top, d_.Y, d_.xrow, shared_A_cm_ ? nullptr : (void*)d_.A_cm, d_.A_nb, d_.slot2col, d_.col2slot,
                     d_.basic, d_.frozen, cost_buf_, d_.ctl, d_.cand, d_.pz, d_.pj, d_.log, scratch_, tmaps_,
                     d_.rc_theta, d_.rc_cnt, d_.rc_row, d_.rc_ratio, d_.cand_ratio, d_.pmsg, d_.rmsg,
-                    chain_};
+                    chain_, b0_, art_row_};
     for (void* p : bufs)
         if (p) cudaFree(p);
     if (hctl_) cudaFreeHost(hctl_);
@@ -595,7 +623,8 @@ void Solver::release() {
     if (pool_) cudaMemPoolDestroy(pool_);
     if (st_) cudaStreamDestroy(st_);
     d_ = Dev{};
-    cost_buf_ = scratch_ = chain_ = nullptr;
+    cost_buf_ = scratch_ = chain_ = b0_ = nullptr;
+    art_row_ = nullptr;
     tmaps_ = nullptr;
     hctl_ = nullptr;
     hlog_ = nullptr;
@@ -1045,6 +1074,99 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
         if (p) CK(cudaFreeAsync(p, st_));
 }
 
+// One phase, through the reinversion mode when it is on: the device budget
+// stops the pivot chain every reinv_every_ pivots for a rebuild, and an optimal
+// or unbounded outcome is only accepted on a freshly rebuilt inverse (the
+// drift that makes the reference call SCSD1 unbounded, or end C3 with a
+// phase-1 objective above feas_tol, is gone after the rebuild).
+int Solver::run_phase_any() {
+    if (reinv_every_ <= 0) return view_rows ? run_phase_stepwise() : run_phase();
+    for (;;) {
+        const long long since = reinv_at_ >= 0 ? reinv_at_ : 0;
+        const long long stop = std::min<long long>(max_iter_, std::max<long long>(total_iter_ + 1, since + reinv_every_));
+        hctl_->budget = stop;
+        const int st = view_rows ? run_phase_stepwise() : run_phase();
+        hctl_->budget = max_iter_;
+        push();
+        const bool fresh = reinv_at_ == total_iter_;
+        if (st == LPSG_ITERATION_LIMIT && total_iter_ < max_iter_) {
+            reinvert();
+            continue;
+        }
+        if ((st == LPSG_OPTIMAL || st == LPSG_UNBOUNDED) && !fresh) {
+            reinvert();
+            continue;
+        }
+        return st;
+    }
+}
+
+// B^-1 rebuilt from the basis columns of the original A (csrc/reinvert.cu):
+// Newton-Schulz X <- X + X (I - B X), repeated while the starting residual
+// max|I - B X| is not small (>= 1e-6; one step from a residual eps leaves
+// ~eps^2), then a probe |B X 1 - 1| of the result, b_bar = X b, and row 0 by
+// rebuild_top_row (W = c_B^T X, obj = c_B . b_bar).
+void Solver::reinvert() {
+    const int m = m_;
+    const long long ld = round_up(m, 4);
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaEventRecord(e0, st_));
+    double* Bm = talloc<double>((size_t)ld * m, st_, pool_);
+    double* R = talloc<double>((size_t)ld * m, st_, pool_);
+    double* Xn = talloc<double>((size_t)ld * m, st_, pool_);
+    double* vec = talloc<double>(2 * (size_t)ld, st_, pool_);
+    unsigned long long* amax = talloc<unsigned long long>(2, st_, pool_);
+    auto read_max = [&](int k) {
+        unsigned long long bits = 0;
+        CK(cudaMemcpyAsync(&bits, amax + k, sizeof(bits), cudaMemcpyDeviceToHost, st_));
+        CK(cudaStreamSynchronize(st_));
+        double v;
+        std::memcpy(&v, &bits, sizeof(v));
+        return v;
+    };
+    launch_form_basis(d_, art_row_, Bm, ld, st_);
+    int steps = 0;
+    double before = 0.0;
+    for (;;) {
+        // R = I - B X, its max, X' = X + X R (into Xn, then back into T)
+        launch_dgemm_nn(m, m, m, Bm, ld, d_.T, d_.ldT, R, ld, -1.0, nullptr, 0, st_);
+        CK(cudaMemsetAsync(amax, 0, sizeof(unsigned long long), st_));
+        launch_absmax(R, m, ld, amax, st_);
+        const double res = read_max(0);
+        if (steps == 0) before = res;
+        if (!(res < 0.5)) throw Error(LPSG_CUDA_ERROR, "reinversion: the inverse drifted too far to refine");
+        if (steps > 0 && res < 1e-14) break;  // converged: X is already the rebuilt inverse
+        launch_dgemm_nn(m, m, m, d_.T, d_.ldT, R, ld, Xn, ld, 1.0, d_.T, d_.ldT, st_);
+        CK(cudaMemcpy2DAsync(d_.T, sizeof(double) * d_.ldT, Xn, sizeof(double) * ld, sizeof(double) * m, m,
+                             cudaMemcpyDeviceToDevice, st_));
+        ++steps;
+        if (res < 1e-6 || steps >= 4) break;  // quadratic convergence: one more step is below rounding
+    }
+    CK(cudaMemsetAsync(amax + 1, 0, sizeof(unsigned long long), st_));
+    launch_probe_residual(m, Bm, ld, d_.T, d_.ldT, vec, vec + ld, amax + 1, st_);
+    const double after = read_max(1);
+    launch_gemv_bbar(d_, b0_, st_);
+    CK(cudaGetLastError());
+    rebuild_top_row();
+    void* tmp[] = {Bm, R, Xn, vec, amax};
+    for (void* p : tmp) CK(cudaFreeAsync(p, st_));
+    CK(cudaEventRecord(e1, st_));
+    CK(cudaStreamSynchronize(st_));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    ++reinv_count;
+    reinv_steps += steps;
+    reinv_res_before = before;
+    reinv_res_after = after;
+    reinv_seconds += ms / 1e3;
+    reinv_at_ = total_iter_;
+    last_objective_ = objective_value();
+}
+
 // drive_out_artificials (solver.cpp:295-316)
 void Solver::drive_out_artificials() {
     for (int i = 0; i < m_; ++i) {
@@ -1117,7 +1239,7 @@ void Solver::solve(lpsg_report* rep) {
         status = LPSG_OPTIMAL;
         bool finished = false;
         if (phase_ == 1) {
-            const int st = view_rows ? run_phase_stepwise() : run_phase();
+            const int st = run_phase_any();
             if (st == LPSG_ITERATION_LIMIT) {
                 status = LPSG_ITERATION_LIMIT;
                 finished = true;
@@ -1129,7 +1251,7 @@ void Solver::solve(lpsg_report* rep) {
                 enter_phase2();
             }
         }
-        if (!finished) status = view_rows ? run_phase_stepwise() : run_phase();
+        if (!finished) status = run_phase_any();
         done_ = status != LPSG_ITERATION_LIMIT;
     }
     hctl_->status = ST_HOLD;
@@ -1618,6 +1740,17 @@ int lpsg_set_view_observer(lpsg_solver* s, lpsg_view_observer cb, void* user, in
 int lpsg_get_memory(lpsg_solver* s, lpsg_memory* out) {
     if (!s || !out) return bad("lpsg_get_memory: null argument");
     *out = s->s->memory();
+    return LPSG_OK;
+}
+
+int lpsg_reinvert_stats(lpsg_solver* s, long* rebuilds, long* steps, double* residual_before,
+                        double* residual_after, double* seconds) {
+    if (!s) return bad("lpsg_reinvert_stats: null solver");
+    if (rebuilds) *rebuilds = s->s->reinv_count;
+    if (steps) *steps = s->s->reinv_steps;
+    if (residual_before) *residual_before = s->s->reinv_res_before;
+    if (residual_after) *residual_after = s->s->reinv_res_after;
+    if (seconds) *seconds = s->s->reinv_seconds;
     return LPSG_OK;
 }
 

@@ -102,6 +102,9 @@ class SolverConfig:
     # verification modes, result-identical to the default (tests/test_gpu_parity.py):
     unfused_ratio: bool = False           # standalone ratio-test kernel, not the fused epilogue
     lookahead_exact_select: bool = False  # theta' keeps the y_i == 0 select
+    # opt-in periodic reinversion on the device (NOT bit-identical to the
+    # reference; include/lpsg.h lpsg_config.reinvert_every): 0 = off
+    reinvert_every: int = 0
 
     def _c(self) -> L.Config:
         c = L.Config()
@@ -114,6 +117,7 @@ class SolverConfig:
         c.world_size, c.rank = int(self.world_size), int(self.rank)
         c.reserved[1] = 1 if self.nccl_single else 0
         c.peer = self.peer.ptr if self.peer is not None else None
+        c.reinvert_every = int(self.reinvert_every)
         # (tools/dbg set `_experiment` on an instance; it only has an effect in
         # the -DLPSG_EXPERIMENTS library, LPSG_EXPERIMENTS_LIB=1)
         c.reserved[2] = (16 if self.lookahead_exact_select else 0) | (
@@ -344,6 +348,16 @@ class SimplexSolver:
         return SolveReport(SolveStatus(rep.status), rep.objective, x, rep.iterations_phase1,
                            rep.iterations_phase2, rep.total_seconds, rep.tpi_seconds,
                            memory=self.memory())
+
+    def reinvert_stats(self) -> dict:
+        """Reinversion mode: rebuilds, Newton steps, max|I - B X| before / after
+        the last rebuild, device seconds (include/lpsg.h lpsg_reinvert_stats)."""
+        n, k = C.c_long(), C.c_long()
+        r0, r1, t = C.c_double(), C.c_double(), C.c_double()
+        _check(self.lib.lpsg_reinvert_stats(self._h, C.byref(n), C.byref(k), C.byref(r0),
+                                            C.byref(r1), C.byref(t)))
+        return dict(rebuilds=n.value, steps=k.value, residual_before=r0.value,
+                    residual_after=r1.value, seconds=t.value)
 
     def memory(self) -> dict:
         """SolveReport::memory counterpart (include/lpsg.h lpsg_memory)."""
