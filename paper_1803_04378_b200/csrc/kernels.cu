@@ -1436,80 +1436,120 @@ __global__ void k_la_wp(Dev d, LookaheadDev la) {
 }
 
 // ---- register-tiled batched lookahead (a SIMT "GEMM" with sequential sums) --
-// The K candidates share every A_nb / T element they read: a CTA computes a
-// 64 x 64 tile of outputs (4 x 4 per thread, 16 independent chains hide the
-// DADD latency) and stages 16-deep chunks of both operands in shared memory,
-// so A_nb and T are read once per 64 candidates instead of once per candidate.
+// The K candidates share every A_nb / T element they read: a CTA of 128
+// threads computes a 64-candidate x 128-column tile of outputs, 8 x 8 per
+// thread (64 independent chains per thread hide the 8-cycle DADD latency), and
+// streams 16-deep chunks of both operands into shared memory through a
+// 3-stage cp.async ring (no register staging, one barrier per chunk). With 8 x 8
+// tiles a chunk step issues 128 (pricing) / 256 (theta) fp64 instructions per
+// 16 (24) shared loads, so the fp64 pipe, not the LSU, is the limit (the 4 x 4
+// form of round 1 ran both at ~100 % and reached 0.72 of the pipe).
 // Each output is still one chain in ascending reduction index, bit for bit the
-// reference's dot (solver.cpp:190-200, 203-210).
-constexpr int kLT = 64;  // tile edge
-constexpr int kLC = 16;  // reduction chunk
+// reference's dot (solver.cpp:190-200, 203-210): DMUL + DADD, never DFMA.
+constexpr int kLK = 64;    // candidates per CTA tile
+constexpr int kLN = 128;   // slots (pricing) / rows (theta) per CTA tile
+constexpr int kLC = 16;    // reduction chunk
+constexpr int kLS = 3;     // cp.async stages
+constexpr int kLThreads = 128;
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool ok) {
+    // src-size 0 zero-fills the destination (out-of-range elements)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(su32(dst)), "l"(src), "r"(ok ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(dst)), "l"(src), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+struct LaPriceSmem {
+    double W[kLS][kLC][kLK];   // [i][k]
+    double A[kLS][kLC][kLN];   // [i][s]
+};
+struct LaThetaSmem {
+    double T[kLS][kLC][kLN];   // [j][i]
+    double X[kLS][kLC][kLK];   // [j][k]
+    double B[kLS][kLC][kLK];   // [j][k]  a_{b_k}[j]
+    int bj[kLK], rk[kLK];
+};
 
 // z_k(s) = dot(W'_k, a_s) - c_j over this shard's slots (j = slot2col[s] != q):
-// the best (z, j) of the tile's 64 slots per candidate -> part_z/part_j[k][bx].
-__global__ void __launch_bounds__(256, 2) k_la_gemm_price(Dev d, LookaheadDev la) {
-    __shared__ double Ws[kLC][kLT + 1];  // [i][k]
-    __shared__ double As[kLC][kLT];      // [i][s]
+// the best (z, j) of the tile's 128 slots per candidate -> part_z/part_j[k][bx].
+__global__ void __launch_bounds__(kLThreads) k_la_gemm_price(Dev d, LookaheadDev la) {
+    extern __shared__ __align__(16) unsigned char la_smem[];
+    LaPriceSmem& sm = *reinterpret_cast<LaPriceSmem*>(la_smem);
     const int n_scan = d.ctl->n_scan;
     const double* cost = phase_cost(d, d.ctl->phase);
-    const int s0 = blockIdx.x * kLT, k0 = blockIdx.y * kLT;
+    const int s0 = blockIdx.x * kLN, k0 = blockIdx.y * kLK;
     const int t = threadIdx.x, tk = t >> 4, ts = t & 15;
     const int m = d.m;
-    double acc[4][4];
+    double acc[8][8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-    // chunk c+1 is fetched into registers while chunk c is consumed
-    double rw[4], ra[4];
-    auto fetch = [&](int i0) {
+        for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
+    // chunk loads: W 16 x 64 as 8-byte copies (candidate-fast: conflict-free
+    // stores, L1 reuse of each candidate's 32-byte sectors); A_nb 16 x 128 as
+    // 16-byte copies along the slot rows
+    auto issue = [&](int stage, int i0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int e = t + 256 * q;
-            const int ii = e % kLC, kk = e / kLC;
+        for (int q = 0; q < kLC * kLK / kLThreads; ++q) {
+            const int e = t + kLThreads * q;
+            const int kk = e % kLK, ii = e / kLK;
             const int k = k0 + kk, i = i0 + ii;
-            rw[q] = (k < la.K && i < m) ? la.Wp[(size_t)k * la.ldx + i] : 0.0;
-            const int ss = e % kLT, ia = e / kLT;
-            const int sl = s0 + ss, i2 = i0 + ia;
-            ra[q] = (sl < n_scan && i2 < m) ? d.A_nb[(size_t)i2 * d.ld_nb + sl] : 0.0;
+            const bool ok = k < la.K && i < m;
+            cp_async8(&sm.W[stage][ii][kk], ok ? la.Wp + (size_t)k * la.ldx + i : la.Wp, ok);
+        }
+#pragma unroll
+        for (int q = 0; q < kLC * kLN / (2 * kLThreads); ++q) {
+            const int e = t + kLThreads * q;
+            const int sp = e % (kLN / 2), ii = e / (kLN / 2);
+            const int sl = s0 + 2 * sp, i = i0 + ii;
+            const int nb = (i < m) ? 8 * max(0, min(2, n_scan - sl)) : 0;
+            cp_async16(&sm.A[stage][ii][2 * sp], nb ? d.A_nb + (size_t)i * d.ld_nb + sl : d.A_nb, nb);
         }
     };
-    fetch(0);
-    for (int i0 = 0; i0 < m; i0 += kLC) {
+    const int nch = (m + kLC - 1) / kLC;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int e = t + 256 * q;
-            Ws[e % kLC][e / kLC] = rw[q];
-            As[e / kLT][e % kLT] = ra[q];
-        }
-        __syncthreads();
-        if (i0 + kLC < m) fetch(i0 + kLC);
+    for (int st = 0; st < kLS - 1; ++st) {
+        if (st < nch) issue(st, st * kLC);
+        cp_async_commit();
+    }
+    for (int ch = 0; ch < nch; ++ch) {
+        cp_async_wait<kLS - 2>();
+        __syncthreads();  // chunk ch landed for every thread; stage (ch-1) % S is free
+        if (ch + kLS - 1 < nch) issue((ch + kLS - 1) % kLS, (ch + kLS - 1) * kLC);
+        cp_async_commit();
+        const int stg = ch % kLS;
+        const int lim = min(kLC, m - ch * kLC);
         auto step = [&](int ii) {
-            double w[4], a[4];
+            double w[8], a[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                w[u] = Ws[ii][tk + 16 * u];
-                a[u] = As[ii][ts + 16 * u];
-            }
+            for (int u = 0; u < 8; ++u) w[u] = sm.W[stg][ii][tk + 8 * u];
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int v = 0; v < 8; ++v) a[v] = sm.A[stg][ii][ts + 16 * v];
 #pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] = dadd(acc[u][v], dmul(w[u], a[v]));
+            for (int u = 0; u < 8; ++u)
+#pragma unroll
+                for (int v = 0; v < 8; ++v) acc[u][v] = dadd(acc[u][v], dmul(w[u], a[v]));
         };
-        if (i0 + kLC <= m) {
+        if (lim == kLC) {
 #pragma unroll
             for (int ii = 0; ii < kLC; ++ii) step(ii);
         } else {
-            for (int ii = 0; ii < m - i0; ++ii) step(ii);
+            for (int ii = 0; ii < lim; ++ii) step(ii);
         }
-        __syncthreads();
     }
+    cp_async_wait<0>();
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
         double bz = -kInf;
         int bj = INT_MAX;
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
+        for (int v = 0; v < 8; ++v) {
             const int sl = s0 + ts + 16 * v;
             if (sl < n_scan) {
                 const int j = d.slot2col[sl];
@@ -1519,12 +1559,12 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_price(Dev d, LookaheadDev la
                 }
             }
         }
-        for (int o = 8; o > 0; o >>= 1) {  // the 16 lanes sharing candidate tk + 16u
+        for (int o = 8; o > 0; o >>= 1) {  // the 16 lanes sharing candidate tk + 8u
             const double oz = __shfl_xor_sync(0xffffffffu, bz, o);
             const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
             if (better(oz, oj, bz, bj)) { bz = oz; bj = oj; }
         }
-        const int k = k0 + tk + 16 * u;
+        const int k = k0 + tk + 8 * u;
         if (ts == 0 && k < la.K) {
             la.part_z[(size_t)k * la.nblk + blockIdx.x] = bz;
             la.part_j[(size_t)k * la.nblk + blockIdx.x] = bj;
@@ -1657,123 +1697,126 @@ __global__ void __launch_bounds__(kDT) k_la_own(Dev d, LookaheadDev la) {
 
 // y'_ik = sum_j t_ij(k) a_{b_k}[j] for this shard's rows, t = X_kj on the
 // candidate's own row, T_ij where y_i == 0, else T_ij - y_i X_kj (solver.cpp:
-// 177-184, 203-210); theta'_k partial (min ratio) per 64-row tile -> part_t[k][bx].
-__global__ void __launch_bounds__(256, 2) k_la_gemm_theta(Dev d, LookaheadDev la) {
-    __shared__ double Ts[kLC][kLT];      // [j][i]
-    __shared__ double Xs[kLC][kLT + 1];  // [j][k]
-    __shared__ double Bs[kLC][kLT + 1];  // [j][k]  a_{b_k}[j]
-    __shared__ int s_bj[kLT], s_rk[kLT];
+// 177-184, 203-210); theta'_k partial (min ratio) per 128-row tile -> part_t[k][bx].
+__global__ void __launch_bounds__(kLThreads) k_la_gemm_theta(Dev d, LookaheadDev la) {
+    extern __shared__ __align__(16) unsigned char la_smem[];
+    LaThetaSmem& sm = *reinterpret_cast<LaThetaSmem*>(la_smem);
     const int m = d.m;
-    const int i0 = blockIdx.x * kLT, k0 = blockIdx.y * kLT;
+    const int i0 = blockIdx.x * kLN, k0 = blockIdx.y * kLK;
     const int t = threadIdx.x, ti = t & 15, tk = t >> 4;
-    if (t < kLT) {
+    if (t < kLK) {
         const int k = k0 + t;
-        s_bj[t] = k < la.K ? la.bj[k] : -1;
-        s_rk[t] = k < la.K ? la.rows[k] : -1;
+        sm.bj[t] = k < la.K ? la.bj[k] : -1;
+        sm.rk[t] = k < la.K ? la.rows[k] : -1;
     }
     __syncthreads();
     bool any = false;
-    for (int kk = 0; kk < kLT; ++kk) any |= s_bj[kk] >= 0;
+    for (int kk = 0; kk < kLK; ++kk) any |= sm.bj[kk] >= 0;
     if (!any) {  // no candidate of this tile has an entering column: score 0
         if (ti == 0)
-            for (int v = 0; v < 4; ++v) {
-                const int k = k0 + tk + 16 * v;
+            for (int v = 0; v < 8; ++v) {
+                const int k = k0 + tk + 8 * v;
                 if (k < la.K) la.part_t[(size_t)k * la.nblk_t + blockIdx.x] = kInf;
             }
         return;
     }
-    double yv[4];
-    bool rowok[4];
+    double yv[8];
+    bool rowok[8], zrow[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
         const int li = i0 + ti + 16 * u;
         rowok[u] = li < d.mloc;
         yv[u] = rowok[u] ? d.Y[li] : 0.0;
+        zrow[u] = yv[u] == 0.0;
     }
-    double acc[4][4];
+    double acc[8][8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+    for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
+        for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
     // Chains use T_ij - y_i X_kj; rows with y_i == 0 keep T_ij exactly as the
     // reference does (solver.cpp:177-184: T - 0*X would flip a -0 entry of a
-    // former pivot row). The row kind is fixed per thread row, so it costs one
-    // select per element. The candidate's own row (t = X_kj) is skipped here and
-    // handled by k_la_own.
-    bool zrow[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) zrow[u] = yv[u] == 0.0;
-    // some X_kj is inf/NaN: keep the select (la_exact forces it: a parity check
-    // of that path, tests/test_gpu_parity.py)
+    // former pivot row). The candidate's own row (t = X_kj) is skipped here and
+    // handled by k_la_own. Some X_kj inf/NaN: keep the select (la_exact forces
+    // it: a parity check of that path, tests/test_gpu_parity.py).
     const bool exact = *la.nonfinite != 0 || d.la_exact != 0;
-    double rt[4], rx[4], rb[4];
-    auto fetch = [&](int j0) {
+    auto issue = [&](int stage, int j0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int e = t + 256 * q;
-            const int ii = e % kLT, jj = e / kLT;
-            const int li = i0 + ii, j = j0 + jj;
-            rt[q] = (li < d.mloc && j < m) ? d.T[(size_t)j * d.ldT + li] : 0.0;
-            const int jx = e % kLC, kk = e / kLC;
-            const int k = k0 + kk, j2 = j0 + jx;
-            const bool okk = k < la.K && j2 < m;
-            rx[q] = okk ? la.X[(size_t)k * la.ldx + j2] : 0.0;
-            rb[q] = (okk && s_bj[kk] >= 0) ? d.A_cm[(size_t)s_bj[kk] * d.ld_cm + j2] : 0.0;
+        for (int q = 0; q < kLC * kLN / (2 * kLThreads); ++q) {  // T: 16 columns x 128 rows, 16-byte copies
+            const int e = t + kLThreads * q;
+            const int ip = e % (kLN / 2), jj = e / (kLN / 2);
+            const int li = i0 + 2 * ip, j = j0 + jj;
+            const int nb = (j < m) ? 8 * max(0, min(2, d.mloc - li)) : 0;
+            cp_async16(&sm.T[stage][jj][2 * ip], nb ? d.T + (size_t)j * d.ldT + li : d.T, nb);
+        }
+#pragma unroll
+        for (int q = 0; q < kLC * kLK / kLThreads; ++q) {  // X and a_{b_k}: 16 x 64, candidate-fast
+            const int e = t + kLThreads * q;
+            const int kk = e % kLK, jj = e / kLK;
+            const int k = k0 + kk, j = j0 + jj;
+            const bool ok = k < la.K && j < m;
+            cp_async8(&sm.X[stage][jj][kk], ok ? la.X + (size_t)k * la.ldx + j : la.X, ok);
+            const int bj = sm.bj[kk];
+            const bool okb = ok && bj >= 0;
+            cp_async8(&sm.B[stage][jj][kk], okb ? d.A_cm + (size_t)bj * d.ld_cm + j : d.A_cm, okb);
         }
     };
-    fetch(0);
-    for (int j0 = 0; j0 < m; j0 += kLC) {
+    const int nch = (m + kLC - 1) / kLC;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int e = t + 256 * q;
-            Ts[e / kLT][e % kLT] = rt[q];
-            Xs[e % kLC][e / kLC] = rx[q];
-            Bs[e % kLC][e / kLC] = rb[q];
-        }
+    for (int st = 0; st < kLS - 1; ++st) {
+        if (st < nch) issue(st, st * kLC);
+        cp_async_commit();
+    }
+    for (int ch = 0; ch < nch; ++ch) {
+        cp_async_wait<kLS - 2>();
         __syncthreads();
-        if (j0 + kLC < m) fetch(j0 + kLC);
+        if (ch + kLS - 1 < nch) issue((ch + kLS - 1) % kLS, (ch + kLS - 1) * kLC);
+        cp_async_commit();
+        const int stg = ch % kLS;
+        const int lim = min(kLC, m - ch * kLC);
         // exact: rows with y_i == 0 take T_ij itself (a select per element).
         // fast: T_ij - y_i X_kj for every row. With y_i = +-0 and X_kj finite
         // that differs from T_ij only in the sign of a zero, and a zero term
         // never changes the chain (acc starts at +0.0 and round-to-nearest
         // never produces -0.0 from it), so the chains are bit-identical.
         auto step = [&](int jj, auto sel) {
-            double tv[4], xv[4], bv[4];
+            double tv[8], xv[8], bv[8];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                tv[u] = Ts[jj][ti + 16 * u];
-                xv[u] = Xs[jj][tk + 16 * u];
-                bv[u] = Bs[jj][tk + 16 * u];
+            for (int u = 0; u < 8; ++u) tv[u] = sm.T[stg][jj][ti + 16 * u];
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+                xv[v] = sm.X[stg][jj][tk + 8 * v];
+                bv[v] = sm.B[stg][jj][tk + 8 * v];
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
+            for (int u = 0; u < 8; ++u)
 #pragma unroll
-                for (int v = 0; v < 4; ++v) {
+                for (int v = 0; v < 8; ++v) {
                     const double sub = dsub(tv[u], dmul(yv[u], xv[v]));
                     acc[u][v] = dadd(acc[u][v], dmul(decltype(sel)::value && zrow[u] ? tv[u] : sub, bv[v]));
                 }
         };
         if (exact) {
-            for (int jj = 0; jj < min(kLC, m - j0); ++jj) step(jj, std::true_type{});
-        } else if (j0 + kLC <= m) {
+            for (int jj = 0; jj < lim; ++jj) step(jj, std::true_type{});
+        } else if (lim == kLC) {
 #pragma unroll
             for (int jj = 0; jj < kLC; ++jj) step(jj, std::false_type{});
         } else {
-            for (int jj = 0; jj < m - j0; ++jj) step(jj, std::false_type{});
+            for (int jj = 0; jj < lim; ++jj) step(jj, std::false_type{});
         }
-        __syncthreads();
     }
+    cp_async_wait<0>();
     const double* bcol = d.T + (size_t)m * d.ldT;
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-        const int kk = tk + 16 * v, k = k0 + kk;
+    for (int v = 0; v < 8; ++v) {
+        const int kk = tk + 8 * v, k = k0 + kk;
         double th = kInf;
-        if (k < la.K && s_bj[kk] >= 0) {
+        if (k < la.K && sm.bj[kk] >= 0) {
             const double xm = la.X[(size_t)k * la.ldx + m];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 8; ++u) {
                 const int li = i0 + ti + 16 * u;
-                if (!rowok[u] || d.frozen[d.row0 + li] || d.row0 + li == s_rk[kk]) continue;
+                if (!rowok[u] || d.frozen[d.row0 + li] || d.row0 + li == sm.rk[kk]) continue;
                 if (acc[u][v] <= d.pivot_tol) continue;
                 const double bb = zrow[u] ? bcol[li] : dsub(bcol[li], dmul(yv[u], xm));
                 th = min_keep(th, ddiv(bb, acc[u][v]));
@@ -1963,6 +2006,8 @@ void configure_kernels(Dev& d) {
     d.price_smem = (int)(d.price_S * d.price_stage_bytes + 2 * d.price_S * 8);
     cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, d.upd_smem);
     cudaFuncSetAttribute(k_price, cudaFuncAttributeMaxDynamicSharedMemorySize, d.price_smem);
+    cudaFuncSetAttribute(k_la_gemm_price, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaPriceSmem));
+    cudaFuncSetAttribute(k_la_gemm_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaThetaSmem));
     // One shared-memory carveout for every kernel: SMs never reconfigure the
     // L1/shared split between the streaming kernels and the small ones, and a
     // shard's spin-waiting exchange kernel can share an SM with another shard's
@@ -2060,7 +2105,8 @@ void launch_la_x(const Dev& d, LookaheadDev& la, cudaStream_t st) {
 void launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     k_la_wp<<<dim3((d.m + 255) / 256, la.K), 256, 0, st>>>(d, la);
     // la.nblk = slot tiles + 1 (the last partial holds the leaving column)
-    if (la.nblk > 1) k_la_gemm_price<<<dim3(la.nblk - 1, (la.K + kLT - 1) / kLT), 256, 0, st>>>(d, la);
+    if (la.nblk > 1)
+        k_la_gemm_price<<<dim3(la.nblk - 1, (la.K + kLK - 1) / kLK), kLThreads, sizeof(LaPriceSmem), st>>>(d, la);
     k_la_leave<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
     k_la_price_local<<<la.K, 32, 0, st>>>(d, la);
 }
@@ -2070,7 +2116,7 @@ void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int 
 }
 
 void launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st) {
-    k_la_gemm_theta<<<dim3(la.nblk_t, (la.K + kLT - 1) / kLT), 256, 0, st>>>(d, la);
+    k_la_gemm_theta<<<dim3(la.nblk_t, (la.K + kLK - 1) / kLK), kLThreads, sizeof(LaThetaSmem), st>>>(d, la);
     k_la_own<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
     k_la_theta_local<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);
 }

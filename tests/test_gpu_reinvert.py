@@ -109,4 +109,6 @@ def test_reinversion_c3_reaches_optimal():
     assert rep.status == P.SolveStatus.optimal, rep.status
     assert rep.iterations_phase1 == 67548
     _check_point(lp, rep)
-    assert st["residual_after"] < 1e-12, st
+    # |B X 1 - 1| after the last rebuild: the two m = 8000 GEMVs of the probe
+    # alone round at ~1e-12 (m eps |B| |X 1|)
+    assert st["residual_after"] < 1e-10, st
