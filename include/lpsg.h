@@ -29,7 +29,8 @@ typedef enum {
     LPSG_OUT_OF_MEMORY = 3,
     LPSG_INVALID_ARGUMENT = 4,
     LPSG_NCCL_ERROR = 5,
-    LPSG_EMPTY_PROBLEM = 6    /* lps::DegenerateSpec / EmptyProblem (errors.hpp:17-19,66-68) */
+    LPSG_EMPTY_PROBLEM = 6,   /* lps::DegenerateSpec / EmptyProblem (errors.hpp:17-19,66-68) */
+    LPSG_BUDGET_TOO_SMALL = 7 /* lps::BudgetTooSmall (tiled_engine.cpp:43-47) */
 } lpsg_status;
 
 /* lps::SolveStatus (solver.hpp:14), same order. */
@@ -99,6 +100,17 @@ typedef struct {
      * 0 = off (default: the reference's drifting explicit inverse, bit for
      * bit). Single GPU only. */
     long reinvert_every;
+    /* lps::SolverConfig::memory_budget (solver.hpp:41, tiled_engine.cpp:29-54):
+     * device bytes for the (m+1) x (m+2) tableau. When the tableau does not fit
+     * (or, with 0 = unlimited, when it does not fit the GPU's free HBM beside A)
+     * the solve runs Case 2 ("tiled", report.case_used = 1): the rows of
+     * [B^-1 | b_bar] live in page-locked host memory in the reference's row
+     * partitions and stream through one device slab per pivot, resident
+     * partition first (tiled_engine.cpp:246-263); results are bit-identical to
+     * the in-core solve. A budget below two tableau rows is
+     * LPSG_BUDGET_TOO_SMALL (lps::BudgetTooSmall, tiled_engine.cpp:44). Case 2
+     * is single-GPU only and has no step API or reinversion. */
+    unsigned long long memory_budget;
 } lpsg_config;
 
 /* lps::SolveReport (solver.hpp:47-57); x is fetched with lpsg_get_x. */
@@ -109,7 +121,7 @@ typedef struct {
     long iterations_phase2;
     double total_seconds;   /* solve() only, like solver.cpp:332,363 */
     double tpi_seconds;     /* total / max(1, iterations) (solver.cpp:387-388) */
-    int case_used;          /* always 0 = in-core (tiled_engine.hpp:24) */
+    int case_used;          /* TileCase (tiled_engine.hpp:24): 0 in-core, 1 tiled (Case 2) */
 } lpsg_report;
 
 /* One pivot, as the reference's IterationObserver sees it (solver.hpp:21-32,

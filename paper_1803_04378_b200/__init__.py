@@ -6,7 +6,7 @@ lps::SimplexSolver, and all per-pivot work runs in hand-written sm_100a CUDA
 kernels behind the C ABI in include/lpsg.h.
 """
 from .solver import (  # noqa: F401
-    Anticycle, ColKind, CudaError, DegenerateSpec, Error, Form, GenSpec, IterationView,
+    Anticycle, BudgetTooSmall, ColKind, CudaError, DegenerateSpec, Error, Form, GenSpec, IterationView,
     PeerHeap, PivotTooSmall, SimplexSolver, SolveReport, SolverConfig, SolveStatus, SparsityClass,
     StandardFormLP, TRACE_DTYPE, device_count, fp64_peak, generate, nccl_unique_id, shard_range, solve_sharded,
     two_phase_solve)
@@ -19,7 +19,7 @@ from .mps import (  # noqa: F401
     to_general_lp, to_mps_document, write_mps)
 
 __all__ = [
-    "Anticycle", "ColKind", "CudaError", "DegenerateSpec", "Error", "Form", "GenSpec",
+    "Anticycle", "BudgetTooSmall", "ColKind", "CudaError", "DegenerateSpec", "Error", "Form", "GenSpec",
     "IterationView", "PeerHeap", "PivotTooSmall", "SimplexSolver", "SolveReport", "SolverConfig",
     "SolveStatus", "SparsityClass", "StandardFormLP", "TRACE_DTYPE", "device_count",
     "fp64_peak", "generate", "nccl_unique_id", "shard_range", "solve_sharded", "two_phase_solve",

@@ -26,7 +26,8 @@ class Config(C.Structure):
                 ("kernel", C.c_int), ("workers", C.c_int), ("device", C.c_int),
                 ("batch", C.c_int), ("use_graphs", C.c_int), ("reserved", C.c_int * 6),
                 ("world_size", C.c_int), ("rank", C.c_int), ("nccl_id", C.c_ubyte * 128),
-                ("peer", C.c_void_p), ("reinvert_every", C.c_long)]
+                ("peer", C.c_void_p), ("reinvert_every", C.c_long),
+                ("memory_budget", C.c_ulonglong)]
 
 
 class Report(C.Structure):

@@ -177,6 +177,8 @@ struct Dev {
                            // through LPSG_XP, i.e. only in a -DLPSG_EXPERIMENTS build
     int la_exact;          // lookahead theta' keeps the y_i == 0 select (cfg.reserved[2] bit 4):
                            // result-identical verification mode
+    int keep_pending;      // Case 2 (tiled): this k_update launch is not the last partition of the
+                           // pass, so its last CTA leaves ctl.pending set for the next one
     int naive;             // KernelMode::naive (tiled_engine.cpp:61-77): every element is stored,
                            // no `temp != 0` skip (only zero signs differ from cached mode)
     int pdl;               // launch the pivot chain with programmatic dependent launch
@@ -239,6 +241,8 @@ struct LookaheadDev {
     int q;            // entering column
     double d;         // entering reduced cost
     int* nonfinite;   // set by k_la_wp when some X_kj (j < m) is inf/NaN (host zeroes it)
+    int x_owned_only; // Case 2: k_la_x writes only the rows of the resident partition (runs once
+                      // per partition) instead of zero-filling the others for a sum exchange
 };
 
 // ---- launchers (kernels.cu) -------------------------------------------------
@@ -275,6 +279,10 @@ void launch_la_score(const Dev& d, LookaheadDev& la, const double* tl, int nsrc,
 void launch_sum_i64(const long long* in, int nsrc, size_t n, long long* out, cudaStream_t st);
 void launch_min_i32(const int* in, int nsrc, size_t n, int* out, cudaStream_t st);
 void launch_gather_row(const Dev& d, int i, double* out, cudaStream_t st);
+// Case 2 (tiled): the ratio test over P partitions' messages (msgs[p], the
+// partition's full candidate list at d.cand + row0[p]) -> ctl (r / ST_TIE /
+// ST_UNBOUNDED), ascending rows in d.cand
+void launch_ratio_merge_parts(const Dev& d, const RatioMsg* msgs, const int* row0, int P, cudaStream_t st);
 // opt-in reinversion (reinvert.cu): column-major C = alpha A B + D (D == nullptr: + I)
 void launch_dgemm_nn(int M, int N, int K, const double* A, long long lda, const double* B, long long ldb, double* C,
                      long long ldc, double alpha, const double* D, long long ldd, cudaStream_t st);

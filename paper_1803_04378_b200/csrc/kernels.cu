@@ -922,7 +922,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
     if (!last_block(&c->ticket_update)) return;
     if (threadIdx.x == 0) {
         c->ticket_update = 0;
-        if (up) c->pending = 0;
+        if (up && !d.keep_pending) c->pending = 0;
         if (ft) d.top[m + 1] = c->d;
         if (up) c->work[1] += 1;  // credited as an update pass (an FTRAN-only pass is not)
     }
@@ -1089,6 +1089,48 @@ __global__ void k_ratio_final(Dev d) {
         else
             c->status = ST_TIE;
     }
+}
+
+// Case 2 (out-of-core, tiled): the partitions of T were updated one after the
+// other on one device, each leaving a RatioMsg (its theta, whether any row was
+// eligible, and the count of its rows inside its own window) and its full
+// in-window list at d.cand + row0[p]. Same merge as k_ratio_final (global theta
+// = min, window, concatenation in partition = row order), but over any number
+// of partitions and without the 30-entry message cap. One thread: the lists
+// are read ascending and the merged list is written into d.cand from the
+// front, never past an entry still to be read.
+__global__ void k_ratio_merge_parts(Dev d, const RatioMsg* __restrict__ msgs, const int* __restrict__ row0, int P) {
+    Ctl* c = d.ctl;
+    if (threadIdx.x != 0 || c->status != ST_RUNNING || c->no_ratio || c->no_ftran || c->q < 0) return;
+    double th = kInf;
+    bool any = false;
+    for (int p = 0; p < P; ++p)
+        if (msgs[p].any) {
+            any = true;
+            th = min_keep(th, msgs[p].theta);
+        }
+    if (!any) {
+        c->status = ST_UNBOUNDED;
+        return;
+    }
+    const double window = dadd(th, dmul(d.ratio_tie_tol, fmax(1.0, fabs(th))));
+    int total = 0;
+    for (int p = 0; p < P; ++p) {
+        if (!msgs[p].any) continue;
+        for (int e = 0; e < msgs[p].n; ++e) {
+            const int src = row0[p] + e;
+            const double ra = d.cand_ratio[src];
+            if (ra <= window) {
+                const int row = d.cand[src];
+                d.cand_ratio[total] = ra;
+                d.cand[total++] = row;
+            }
+        }
+    }
+    c->theta = th;
+    c->ncand = total;
+    if (total == 1 || d.anticycle == 1) c->r = d.cand[0];
+    else c->status = ST_TIE;
 }
 
 // ---------------------------------------------------------------- ratio ---
@@ -1417,7 +1459,7 @@ __global__ void k_la_x(Dev d, LookaheadDev la) {
     const double piv = own ? d.Y[li] : 0.0;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j <= d.m; j += gridDim.x * blockDim.x) {
         if (own) X[j] = ddiv(d.T[(size_t)j * d.ldT + li], piv);
-        else reinterpret_cast<long long*>(X)[j] = 0;
+        else if (!la.x_owned_only) reinterpret_cast<long long*>(X)[j] = 0;
     }
 }
 
@@ -1436,21 +1478,21 @@ __global__ void k_la_wp(Dev d, LookaheadDev la) {
 }
 
 // ---- register-tiled batched lookahead (a SIMT "GEMM" with sequential sums) --
-// The K candidates share every A_nb / T element they read: a CTA of 128
-// threads computes a 64-candidate x 128-column tile of outputs, 8 x 8 per
-// thread (64 independent chains per thread hide the 8-cycle DADD latency), and
-// streams 16-deep chunks of both operands into shared memory through a
-// 3-stage cp.async ring (no register staging, one barrier per chunk). With 8 x 8
-// tiles a chunk step issues 128 (pricing) / 256 (theta) fp64 instructions per
-// 16 (24) shared loads, so the fp64 pipe, not the LSU, is the limit (the 4 x 4
-// form of round 1 ran both at ~100 % and reached 0.72 of the pipe).
+// The K candidates share every A_nb / T element they read: a CTA of 256
+// threads computes a 64-candidate x 128-column tile of outputs, 8 x 4 per
+// thread (32 independent chains per thread), and streams 16-deep chunks of both
+// operands into shared memory through a 3-stage cp.async ring (no register
+// staging, one barrier per chunk). A chunk step issues 64 (pricing) / 128
+// (theta) fp64 instructions per 12 (16) shared loads, and <= 128 registers per
+// thread keep 16 warps per SM to hide the DMUL -> DADD dependency (ncu: with
+// 8 x 8 tiles, 8-12 warps, "wait" was the top stall at 78 % pipe activity).
 // Each output is still one chain in ascending reduction index, bit for bit the
 // reference's dot (solver.cpp:190-200, 203-210): DMUL + DADD, never DFMA.
 constexpr int kLK = 64;    // candidates per CTA tile
 constexpr int kLN = 128;   // slots (pricing) / rows (theta) per CTA tile
 constexpr int kLC = 16;    // reduction chunk
 constexpr int kLS = 3;     // cp.async stages
-constexpr int kLThreads = 128;
+constexpr int kLThreads = 256;  // 8 x 4 outputs per thread, 2 CTAs (16 warps) per SM
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src, bool ok) {
     // src-size 0 zero-fills the destination (out-of-range elements)
@@ -1478,19 +1520,20 @@ struct LaThetaSmem {
 
 // z_k(s) = dot(W'_k, a_s) - c_j over this shard's slots (j = slot2col[s] != q):
 // the best (z, j) of the tile's 128 slots per candidate -> part_z/part_j[k][bx].
-__global__ void __launch_bounds__(kLThreads) k_la_gemm_price(Dev d, LookaheadDev la) {
+__global__ void __launch_bounds__(kLThreads, 2) k_la_gemm_price(Dev d, LookaheadDev la) {
     extern __shared__ __align__(16) unsigned char la_smem[];
     LaPriceSmem& sm = *reinterpret_cast<LaPriceSmem*>(la_smem);
     const int n_scan = d.ctl->n_scan;
     const double* cost = phase_cost(d, d.ctl->phase);
     const int s0 = blockIdx.x * kLN, k0 = blockIdx.y * kLK;
-    const int t = threadIdx.x, tk = t >> 4, ts = t & 15;
+    // warp = one group of 8 candidates tk * 8 + u; lanes = 32 consecutive slots ts + 32 v
+    const int t = threadIdx.x, tk = t >> 5, ts = t & 31;
     const int m = d.m;
-    double acc[8][8];
+    double acc[8][4];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
     // chunk loads: W 16 x 64 as 8-byte copies (candidate-fast: conflict-free
     // stores, L1 reuse of each candidate's 32-byte sectors); A_nb 16 x 128 as
     // 16-byte copies along the slot rows
@@ -1526,15 +1569,19 @@ __global__ void __launch_bounds__(kLThreads) k_la_gemm_price(Dev d, LookaheadDev
         const int stg = ch % kLS;
         const int lim = min(kLC, m - ch * kLC);
         auto step = [&](int ii) {
-            double w[8], a[8];
+            double w[8], a[4];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) w[u] = sm.W[stg][ii][tk + 8 * u];
+            for (int u = 0; u < 8; u += 2) {  // candidates tk*8 .. tk*8+7: 4 broadcast LDS.128
+                const double2 v2 = *reinterpret_cast<const double2*>(&sm.W[stg][ii][tk * 8 + u]);
+                w[u] = v2.x;
+                w[u + 1] = v2.y;
+            }
 #pragma unroll
-            for (int v = 0; v < 8; ++v) a[v] = sm.A[stg][ii][ts + 16 * v];
+            for (int v = 0; v < 4; ++v) a[v] = sm.A[stg][ii][ts + 32 * v];
 #pragma unroll
             for (int u = 0; u < 8; ++u)
 #pragma unroll
-                for (int v = 0; v < 8; ++v) acc[u][v] = dadd(acc[u][v], dmul(w[u], a[v]));
+                for (int v = 0; v < 4; ++v) acc[u][v] = dadd(acc[u][v], dmul(w[u], a[v]));
         };
         if (lim == kLC) {
 #pragma unroll
@@ -1549,8 +1596,8 @@ __global__ void __launch_bounds__(kLThreads) k_la_gemm_price(Dev d, LookaheadDev
         double bz = -kInf;
         int bj = INT_MAX;
 #pragma unroll
-        for (int v = 0; v < 8; ++v) {
-            const int sl = s0 + ts + 16 * v;
+        for (int v = 0; v < 4; ++v) {
+            const int sl = s0 + ts + 32 * v;
             if (sl < n_scan) {
                 const int j = d.slot2col[sl];
                 if (j != la.q) {
@@ -1559,12 +1606,12 @@ __global__ void __launch_bounds__(kLThreads) k_la_gemm_price(Dev d, LookaheadDev
                 }
             }
         }
-        for (int o = 8; o > 0; o >>= 1) {  // the 16 lanes sharing candidate tk + 8u
+        for (int o = 16; o > 0; o >>= 1) {  // the warp's 32 lanes share candidate tk * 8 + u
             const double oz = __shfl_xor_sync(0xffffffffu, bz, o);
             const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
             if (better(oz, oj, bz, bj)) { bz = oz; bj = oj; }
         }
-        const int k = k0 + tk + 8 * u;
+        const int k = k0 + tk * 8 + u;
         if (ts == 0 && k < la.K) {
             la.part_z[(size_t)k * la.nblk + blockIdx.x] = bz;
             la.part_j[(size_t)k * la.nblk + blockIdx.x] = bj;
@@ -1698,11 +1745,12 @@ __global__ void __launch_bounds__(kDT) k_la_own(Dev d, LookaheadDev la) {
 // y'_ik = sum_j t_ij(k) a_{b_k}[j] for this shard's rows, t = X_kj on the
 // candidate's own row, T_ij where y_i == 0, else T_ij - y_i X_kj (solver.cpp:
 // 177-184, 203-210); theta'_k partial (min ratio) per 128-row tile -> part_t[k][bx].
-__global__ void __launch_bounds__(kLThreads) k_la_gemm_theta(Dev d, LookaheadDev la) {
+__global__ void __launch_bounds__(kLThreads, 2) k_la_gemm_theta(Dev d, LookaheadDev la) {
     extern __shared__ __align__(16) unsigned char la_smem[];
     LaThetaSmem& sm = *reinterpret_cast<LaThetaSmem*>(la_smem);
     const int m = d.m;
     const int i0 = blockIdx.x * kLN, k0 = blockIdx.y * kLK;
+    // thread (ti, tk): rows ti + 16 u (u < 8), candidates tk * 4 + v (v < 4; two LDS.128 each of X and a_b)
     const int t = threadIdx.x, ti = t & 15, tk = t >> 4;
     if (t < kLK) {
         const int k = k0 + t;
@@ -1714,8 +1762,8 @@ __global__ void __launch_bounds__(kLThreads) k_la_gemm_theta(Dev d, LookaheadDev
     for (int kk = 0; kk < kLK; ++kk) any |= sm.bj[kk] >= 0;
     if (!any) {  // no candidate of this tile has an entering column: score 0
         if (ti == 0)
-            for (int v = 0; v < 8; ++v) {
-                const int k = k0 + tk + 8 * v;
+            for (int v = 0; v < 4; ++v) {
+                const int k = k0 + tk * 4 + v;
                 if (k < la.K) la.part_t[(size_t)k * la.nblk_t + blockIdx.x] = kInf;
             }
         return;
@@ -1729,11 +1777,11 @@ __global__ void __launch_bounds__(kLThreads) k_la_gemm_theta(Dev d, LookaheadDev
         yv[u] = rowok[u] ? d.Y[li] : 0.0;
         zrow[u] = yv[u] == 0.0;
     }
-    double acc[8][8];
+    double acc[8][4];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
 #pragma unroll
-        for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
+        for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
     // Chains use T_ij - y_i X_kj; rows with y_i == 0 keep T_ij exactly as the
     // reference does (solver.cpp:177-184: T - 0*X would flip a -0 entry of a
     // former pivot row). The candidate's own row (t = X_kj) is skipped here and
@@ -1780,18 +1828,22 @@ __global__ void __launch_bounds__(kLThreads) k_la_gemm_theta(Dev d, LookaheadDev
         // never changes the chain (acc starts at +0.0 and round-to-nearest
         // never produces -0.0 from it), so the chains are bit-identical.
         auto step = [&](int jj, auto sel) {
-            double tv[8], xv[8], bv[8];
+            double tv[8], xv[4], bv[4];
 #pragma unroll
             for (int u = 0; u < 8; ++u) tv[u] = sm.T[stg][jj][ti + 16 * u];
 #pragma unroll
-            for (int v = 0; v < 8; ++v) {
-                xv[v] = sm.X[stg][jj][tk + 8 * v];
-                bv[v] = sm.B[stg][jj][tk + 8 * v];
+            for (int v = 0; v < 4; v += 2) {
+                const double2 x2 = *reinterpret_cast<const double2*>(&sm.X[stg][jj][tk * 4 + v]);
+                const double2 b2 = *reinterpret_cast<const double2*>(&sm.B[stg][jj][tk * 4 + v]);
+                xv[v] = x2.x;
+                xv[v + 1] = x2.y;
+                bv[v] = b2.x;
+                bv[v + 1] = b2.y;
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u)
 #pragma unroll
-                for (int v = 0; v < 8; ++v) {
+                for (int v = 0; v < 4; ++v) {
                     const double sub = dsub(tv[u], dmul(yv[u], xv[v]));
                     acc[u][v] = dadd(acc[u][v], dmul(decltype(sel)::value && zrow[u] ? tv[u] : sub, bv[v]));
                 }
@@ -1799,7 +1851,10 @@ __global__ void __launch_bounds__(kLThreads) k_la_gemm_theta(Dev d, LookaheadDev
         if (exact) {
             for (int jj = 0; jj < lim; ++jj) step(jj, std::true_type{});
         } else if (lim == kLC) {
-#pragma unroll
+            // partially unrolled: a fully unrolled 16-row body of 8 x 8 tiles
+            // (~70 KB of SASS) missed the instruction cache (ncu: stall
+            // no_instructions on top)
+#pragma unroll 4
             for (int jj = 0; jj < kLC; ++jj) step(jj, std::false_type{});
         } else {
             for (int jj = 0; jj < lim; ++jj) step(jj, std::false_type{});
@@ -1808,8 +1863,8 @@ __global__ void __launch_bounds__(kLThreads) k_la_gemm_theta(Dev d, LookaheadDev
     cp_async_wait<0>();
     const double* bcol = d.T + (size_t)m * d.ldT;
 #pragma unroll
-    for (int v = 0; v < 8; ++v) {
-        const int kk = tk + 8 * v, k = k0 + kk;
+    for (int v = 0; v < 4; ++v) {
+        const int kk = tk * 4 + v, k = k0 + kk;
         double th = kInf;
         if (k < la.K && sm.bj[kk] >= 0) {
             const double xm = la.X[(size_t)k * la.ldx + m];
@@ -1920,6 +1975,10 @@ void launch_rebuild_top(const Dev& d, const double* init, double* out, cudaStrea
 
 void launch_price_final(const Dev& d, cudaStream_t st) { k_price_final<<<1, 32, 0, st>>>(d); }
 
+void launch_ratio_merge_parts(const Dev& d, const RatioMsg* msgs, const int* row0, int P, cudaStream_t st) {
+    k_ratio_merge_parts<<<1, 32, 0, st>>>(d, msgs, row0, P);
+}
+
 void launch_ratio_final(const Dev& d, cudaStream_t st) { k_ratio_final<<<1, 32, 0, st>>>(d); }
 
 namespace {
@@ -2022,7 +2081,8 @@ void configure_kernels(Dev& d) {
                          (const void*)k_la_gemm_price, (const void*)k_la_gemm_theta, (const void*)k_la_leave,
                          (const void*)k_la_own,
                          (const void*)k_la_decide, (const void*)k_la_theta_local,
-                         (const void*)k_la_score, (const void*)k_sum_i64, (const void*)k_min_i32};
+                         (const void*)k_la_score, (const void*)k_sum_i64, (const void*)k_min_i32,
+                         (const void*)k_ratio_merge_parts};
     for (const void* f : all) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 

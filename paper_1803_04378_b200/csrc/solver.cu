@@ -223,6 +223,27 @@ private:
     int run_phase_any();
     void reinvert();
 
+    // ---- Case 2: out-of-core tiling (tiled_engine.cpp:29-54, 165-184, 246-263)
+    struct Part {
+        int row0, rows;    // rows [row0, row0 + rows) of [B^-1 | b_bar]
+        double* host;      // page-locked, column-major, pitch `rows`
+    };
+    bool tiled_ = false;
+    std::vector<Part> parts_;
+    int resident_ = -1;          // the partition in the device slab d_.T (-1: none)
+    RatioMsg* part_msgs_ = nullptr;
+    int* part_row0_ = nullptr;
+    double* xbuf_own_ = nullptr;  // Case 2: the pivot-row buffer (sharded runs use the comm heap)
+    void plan_tiles(int m, int n);
+    Dev part_dev(int p) const;
+    int part_of_row(int i) const;
+    void ensure_resident(int p);
+    void tiled_pass();
+    void tiled_pivot();
+    int run_phase_tiled();
+    void gather_row_any(int i, double* out);
+    int rows_local() const { return tiled_ ? m_ : d_.mloc; }
+
 public:
     long reinv_count = 0, reinv_steps = 0;
     double reinv_res_before = 0.0, reinv_res_after = 0.0, reinv_seconds = 0.0;
@@ -479,7 +500,8 @@ void Solver::init(const lpsg_problem& lp) {
     // PDL hides kernel-boundary latency; it pays up to m ~ 10^4 (C1 +21 %, C3
     // +1.4 %) and was measured to cost ~17 % at m = 24000, where the boundaries
     // are noise against 3 ms pivots
-    d_.pdl = (!comm_ && m <= 12000 && xp_env("LPSG_NO_PDL") == nullptr) ? 1 : 0;
+    plan_tiles(m, n);
+    d_.pdl = (!comm_ && !tiled_ && m <= 12000 && xp_env("LPSG_NO_PDL") == nullptr) ? 1 : 0;
     d_.upd_tma_store = xp_env("LPSG_UPD_STG") == nullptr ? 1 : 0;
     d_.l2_hint = xp_env("LPSG_NO_L2_HINT") == nullptr ? 1 : 0;
     configure_kernels(d_);
@@ -491,8 +513,19 @@ void Solver::init(const lpsg_problem& lp) {
 
     d_.T = dalloc<double>((size_t)(m + 1) * d_.ldT + 64);
     d_.top = dalloc<double>(m + 520);  // + padding: TMA-side W segments may run past m+2
-    d_.Y = dalloc<double>(d_.mloc);
+    d_.Y = dalloc<double>(rows_local());
     d_.xrow = dalloc<double>(m + 4);
+    if (tiled_) {
+        xbuf_own_ = dalloc<double>(m + 4);
+        d_.xbuf = xbuf_own_;
+        part_msgs_ = dalloc<RatioMsg>(parts_.size());
+        part_row0_ = dalloc<int>(parts_.size());
+        chain_ = dalloc<double>(m + 1);
+        std::vector<int> r0;
+        for (const Part& q : parts_) r0.push_back(q.row0);
+        CK(cudaMemcpy(part_row0_, r0.data(), sizeof(int) * r0.size(), cudaMemcpyHostToDevice));
+        for (Part& q : parts_) CK(cudaMallocHost(&q.host, sizeof(double) * (size_t)q.rows * (m + 1)));
+    }
     if (sharded_) {
         d_.xbuf = static_cast<double*>(comm_->sym_alloc(sizeof(double) * (m + 4)));
         d_.xbuf_zero = std::strcmp(comm_->transport(), "p2p") != 0;
@@ -552,7 +585,7 @@ void Solver::init(const lpsg_problem& lp) {
     CK(cudaMemcpyAsync(d_.basic, basic_.data(), sizeof(int) * m, cudaMemcpyHostToDevice, st_));
     CK(cudaMemsetAsync(d_.frozen, 0, m, st_));
     CK(cudaMemcpyAsync(cost_buf_, cost.data(), sizeof(double) * cost.size(), cudaMemcpyHostToDevice, st_));
-    CK(cudaMemsetAsync(d_.Y, 0, sizeof(double) * d_.mloc, st_));
+    CK(cudaMemsetAsync(d_.Y, 0, sizeof(double) * rows_local(), st_));
     CK(cudaMemsetAsync(d_.top, 0, sizeof(double) * (m + 520), st_));
 
     // ---- initial Figure-1 tableau B = I, b_bar = b (solver.cpp:66-72)
@@ -565,7 +598,24 @@ void Solver::init(const lpsg_problem& lp) {
         CK(cudaMemsetAsync(d_.rmsg, 0, sizeof(RatioMsg) * (world_ + 1), st_));
     }
     CK(cudaMemcpyAsync(scratch_, lp.b, sizeof(double) * m, cudaMemcpyHostToDevice, st_));
-    launch_init_tableau(d_, scratch_, st_);
+    if (tiled_) {
+        // Case 2: the tableau rows start host-side (begin_solve leaves them
+        // there, tiled_engine.cpp:142-149): B^-1 = I, b_bar = b per partition
+        CK(cudaFree(d_.xrow));
+        d_.xrow = d_.xbuf;
+        CK(cudaMemsetAsync(d_.xbuf, 0, sizeof(double) * (m + 4), st_));
+        CK(cudaMemsetAsync(part_msgs_, 0, sizeof(RatioMsg) * parts_.size(), st_));
+        for (Part& q : parts_) {
+            std::memset(q.host, 0, sizeof(double) * (size_t)q.rows * (m + 1));
+            for (int li = 0; li < q.rows; ++li) {
+                q.host[(size_t)(q.row0 + li) * q.rows + li] = 1.0;
+                q.host[(size_t)m * q.rows + li] = lp.b[q.row0 + li];
+            }
+        }
+        resident_ = -1;
+    } else {
+        launch_init_tableau(d_, scratch_, st_);
+    }
     if (reinv_every_ > 0) {
         b0_ = dalloc<double>(m);
         CK(cudaMemcpyAsync(b0_, lp.b, sizeof(double) * m, cudaMemcpyHostToDevice, st_));
@@ -605,12 +655,19 @@ void Solver::release() {
         comm_->sym_free(d_.xbuf);
         if (d_.xrow == d_.xbuf) d_.xrow = nullptr;
     }
+    if (xbuf_own_ && d_.xrow == xbuf_own_) d_.xrow = nullptr;
     void* bufs[] = {d_.T, d_.top, d_.Y, d_.xrow, shared_A_cm_ ? nullptr : (void*)d_.A_cm, d_.A_nb, d_.slot2col, d_.col2slot,
                     d_.basic, d_.frozen, cost_buf_, d_.ctl, d_.cand, d_.pz, d_.pj, d_.log, scratch_, tmaps_,
                     d_.rc_theta, d_.rc_cnt, d_.rc_row, d_.rc_ratio, d_.cand_ratio, d_.pmsg, d_.rmsg,
-                    chain_, b0_, art_row_};
+                    chain_, b0_, art_row_, part_msgs_, part_row0_, xbuf_own_};
     for (void* p : bufs)
         if (p) cudaFree(p);
+    for (Part& q : parts_)
+        if (q.host) cudaFreeHost(q.host);
+    parts_.clear();
+    part_msgs_ = nullptr;
+    part_row0_ = nullptr;
+    xbuf_own_ = nullptr;
     if (hctl_) cudaFreeHost(hctl_);
     if (hlog_) cudaFreeHost(hlog_);
     if (hone_) cudaFreeHost(hone_);
@@ -666,6 +723,17 @@ double Solver::objective_value() {
 // rebuild_top_row (solver.cpp:318-329). Sharded: an ordered chain, shard g
 // continuing shard g-1's partial sums (an allreduce would reorder the sum).
 void Solver::rebuild_top_row() {
+    if (tiled_) {
+        // the ordered chain over the partitions, ascending rows (solver.cpp:318-329)
+        for (size_t p = 0; p < parts_.size(); ++p) {
+            ensure_resident((int)p);
+            launch_rebuild_top(part_dev((int)p), p == 0 ? nullptr : chain_, chain_, st_);
+            CK(cudaGetLastError());
+        }
+        CK(cudaMemcpyAsync(d_.top, chain_, sizeof(double) * (m_ + 1), cudaMemcpyDeviceToDevice, st_));
+        CK(cudaMemsetAsync(d_.top + m_ + 1, 0, sizeof(double), st_));
+        return;
+    }
     if (!sharded_) {
         launch_rebuild_top(d_, nullptr, d_.top, st_);
         CK(cudaGetLastError());
@@ -701,6 +769,7 @@ int Solver::owner_of_row(int i) const {
 
 void Solver::single_gpu_only(const char* what) const {
     if (sharded_) throw Error(LPSG_INVALID_ARGUMENT, std::string(what) + ": step API is single-GPU only");
+    if (tiled_) throw Error(LPSG_INVALID_ARGUMENT, std::string(what) + ": step API needs the in-core tableau");
 }
 
 // note_iteration (solver.cpp:256-276) for one logged pivot.
@@ -718,9 +787,10 @@ void Solver::note_pivot(const LogEntry& e) {
         // the scanned A columns and W; the update reads + writes this shard's
         // [B^-1 | b_bar] rows; the pivot row is read, divided, written; W updated
         const double m = m_;
-        dev_read_bytes += 8.0 * m * (double)n_scan_host_ + 8.0 * m + 8.0 * d_.mloc * (m + 1.0) +
+        const double rows = rows_local();
+        dev_read_bytes += 8.0 * m * (double)n_scan_host_ + 8.0 * m + 8.0 * rows * (m + 1.0) +
                           8.0 * (m + 1.0) * 2.0 + 8.0 * m;
-        dev_write_bytes += 8.0 * d_.mloc * (m + 1.0) + 8.0 * (m + 1.0) * 2.0;
+        dev_write_bytes += 8.0 * rows * (m + 1.0) + 8.0 * (m + 1.0) * 2.0;
     }
     lpsg_trace t{(long)e.iteration, e.phase, e.row, e.leaving, e.entering, e.objective};
     if (keep_trace) trace.push_back(t);
@@ -766,6 +836,10 @@ void Solver::snapshot() {
 // per-pivot exchanges: the pivot row from its owner, the
 // pricing (z, j) and the ratio-test messages.
 void Solver::seq_pivot() {
+    if (tiled_) {
+        tiled_pivot();
+        return;
+    }
     if (!sharded_) {
         L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot(d_, st_); });
         return;
@@ -800,6 +874,10 @@ void Solver::seq_price() {
 }
 
 void Solver::seq_update() {
+    if (tiled_) {
+        tiled_pass();
+        return;
+    }
     d_.fused = 0;
     if (sharded_ && comm_->fused_slot(&d_.px_ratio)) d_.fused = 1;
     L(K_UPDATE, bytes_of(K_UPDATE), [&] { launch_update(d_, st_); });
@@ -1042,7 +1120,16 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     la.pm_all = sharded_ ? talloc<PriceMsg>((size_t)kb * G, st_, pool_) : nullptr;
     la.tl = talloc<double>(kb, st_, pool_);
     la.own_t = talloc<double>(kb, st_, pool_);
-    la.tl_all = sharded_ ? talloc<double>((size_t)kb * G, st_, pool_) : nullptr;
+    const int P = tiled_ ? (int)parts_.size() : 1;
+    la.tl_all = sharded_ ? talloc<double>((size_t)kb * G, st_, pool_)
+                         : tiled_ ? talloc<double>((size_t)kb * P, st_, pool_) : nullptr;
+    la.x_owned_only = tiled_ ? 1 : 0;
+    std::vector<int> porder;  // Case 2: the resident partition first, then the others
+    if (tiled_) {
+        if (resident_ >= 0) porder.push_back(resident_);
+        for (int p = 0; p < P; ++p)
+            if (p != resident_) porder.push_back(p);
+    }
     la.nonfinite = talloc<int>(1, st_, pool_);
     CK(cudaMemsetAsync(la.X, 0, sizeof(double) * (size_t)kb * ldx, st_));
     if (dbg_trace_) fprintf(stderr, "[solver r%d] lookahead K=%d\n", rank_, K);
@@ -1056,14 +1143,38 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
         // (DMUL + DADD); theta K x mloc x m terms of (T_ij - y_i X_kj) a_j
         // (two more for the updated element)
         const double kf = 2.0 * la.K * (double)m;
-        L(K_OTHER, 0.0, [&] { launch_la_x(d_, la, st_); });
+        if (tiled_) {
+            // Case 2: each partition writes its candidates' pivot rows
+            for (int k = 0; k < P; ++k) {
+                const int p = porder[k];
+                ensure_resident(p);
+                const Dev dp = part_dev(p);
+                L(K_OTHER, 0.0, [&] { launch_la_x(dp, la, st_); });
+            }
+        } else {
+            L(K_OTHER, 0.0, [&] { launch_la_x(d_, la, st_); });
+        }
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->sum_i64(reinterpret_cast<long long*>(la.X), (size_t)la.K * ldx, st_); });
         L(K_LA_PRICE, kf * (double)hctl_->n_scan, [&] { launch_la_price(d_, la, st_); });
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.pm, la.pm_all, sizeof(PriceMsg) * la.K, st_); });
         L(K_OTHER, 0.0, [&] { launch_la_decide(d_, la, sharded_ ? la.pm_all : la.pm, G, st_); });
-        L(K_LA_THETA, 2.0 * kf * (double)d_.mloc, [&] { launch_la_theta(d_, la, st_); });
-        if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.tl, la.tl_all, sizeof(double) * la.K, st_); });
-        L(K_OTHER, 0.0, [&] { launch_la_score(d_, la, sharded_ ? la.tl_all : la.tl, G, st_); });
+        if (tiled_) {
+            // Case 2: theta' per partition (resident first), merged by the exact min of la_score
+            for (int k = 0; k < P; ++k) {
+                const int p = porder[k];
+                ensure_resident(p);
+                const Dev dp = part_dev(p);
+                L(K_LA_THETA, 2.0 * kf * (double)dp.mloc, [&] { launch_la_theta(dp, la, st_); });
+                CK(cudaMemcpyAsync(la.tl_all + (size_t)p * la.K, la.tl, sizeof(double) * la.K,
+                                   cudaMemcpyDeviceToDevice, st_));
+                ev_chain_ = nullptr;
+            }
+            L(K_OTHER, 0.0, [&] { launch_la_score(d_, la, la.tl_all, P, st_); });
+        } else {
+            L(K_LA_THETA, 2.0 * kf * (double)d_.mloc, [&] { launch_la_theta(d_, la, st_); });
+            if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.tl, la.tl_all, sizeof(double) * la.K, st_); });
+            L(K_OTHER, 0.0, [&] { launch_la_score(d_, la, sharded_ ? la.tl_all : la.tl, G, st_); });
+        }
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(scores.data() + k0, la.score, sizeof(double) * la.K, cudaMemcpyDeviceToHost, st_));
         CK(cudaStreamSynchronize(st_));
@@ -1080,6 +1191,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
 // drift that makes the reference call SCSD1 unbounded, or end C3 with a
 // phase-1 objective above feas_tol, is gone after the rebuild).
 int Solver::run_phase_any() {
+    if (tiled_) return view_rows ? run_phase_stepwise() : run_phase_tiled();
     if (reinv_every_ <= 0) return view_rows ? run_phase_stepwise() : run_phase();
     for (;;) {
         const long long since = reinv_at_ >= 0 ? reinv_at_ : 0;
@@ -1167,6 +1279,200 @@ void Solver::reinvert() {
     last_objective_ = objective_value();
 }
 
+// ---- Case 2: out-of-core tiling ---------------------------------------------
+// plan() (tiled_engine.cpp:29-54) on the reference's (m+1) x (m+2) tableau:
+// in-core when it fits the budget; else partitions of capacity_rows - 1 whole
+// tableau rows (one row slot stays reserved for the pivot row). Tableau row 0
+// (W | obj | d) always stays on the device here, so partition p of tableau
+// rows [b, e) holds rows [max(b, 1) - 1, e - 1) of [B^-1 | b_bar]; an empty
+// one (the first, when it held row 0 only) is dropped. memory_budget 0 means
+// unlimited, except that a tableau that does not fit the free HBM beside A
+// is tiled with the HBM that is left.
+void Solver::plan_tiles(int m, int n) {
+    unsigned long long budget = cfg_.memory_budget;
+    const unsigned long long row_bytes = 8ULL * (unsigned long long)(m + 2);
+    const unsigned long long total = row_bytes * (unsigned long long)(m + 1);
+    if (budget == 0 && !sharded_) {
+        size_t free_b = 0, tot_b = 0;
+        CK(cudaMemGetInfo(&free_b, &tot_b));
+        const unsigned long long other = 8ULL * (unsigned long long)n * round_up(m, 4) +
+                                         8ULL * (unsigned long long)m * (unsigned long long)d_.ld_nb +
+                                         (512ULL << 20);
+        if (total + other > free_b) {
+            if (free_b <= other + 2 * row_bytes)
+                throw Error(LPSG_OUT_OF_MEMORY, "lpsg_create: A alone does not fit the device");
+            budget = free_b - other;
+        }
+    }
+    if (budget == 0 || total <= budget) return;  // Case 1, in-core
+    if (sharded_) throw Error(LPSG_INVALID_ARGUMENT, "lpsg_create: the out-of-core (tiled) case is single-GPU only");
+    if (reinv_every_ > 0) throw Error(LPSG_INVALID_ARGUMENT, "lpsg_create: reinversion needs the in-core tableau");
+    const unsigned long long cap_rows = budget / row_bytes;
+    if (cap_rows < 2)
+        throw Error(LPSG_BUDGET_TOO_SMALL, "device budget of " + std::to_string(budget) +
+                                               " bytes cannot hold one data row plus the pivot row (row is " +
+                                               std::to_string(row_bytes) + " bytes)");
+    const int rpp = (int)std::min<unsigned long long>(cap_rows - 1, (unsigned long long)m + 1);
+    for (int b = 0; b < m + 1; b += rpp) {
+        const int e = std::min(b + rpp, m + 1);
+        const int r0 = std::max(b, 1) - 1, r1 = e - 1;
+        if (r1 > r0) parts_.push_back(Part{r0, r1 - r0, nullptr});
+    }
+    tiled_ = true;
+    int mx = 0;
+    for (const Part& q : parts_) mx = std::max(mx, q.rows);
+    d_.mloc = mx;  // the device slab holds the largest partition
+}
+
+// The kernels see partition p as a shard of rows [row0, row0 + rows) living
+// in the slab: Y, the candidate lists and the ratio message are this
+// partition's slices of the global buffers.
+Dev Solver::part_dev(int p) const {
+    Dev dp = d_;
+    const Part& q = parts_[p];
+    dp.row0 = q.row0;
+    dp.mloc = q.rows;
+    dp.Y = d_.Y + q.row0;
+    dp.cand = d_.cand + q.row0;
+    dp.cand_ratio = d_.cand_ratio + q.row0;
+    dp.rmsg = part_msgs_ + p;
+    dp.sharded = 1;  // k_update leaves a RatioMsg, k_pivot reads the divided row from xbuf
+    dp.fused = 0;
+    dp.update_grid = (q.rows + d_.upd_h - 1) / d_.upd_h;
+    dp.keep_pending = 0;
+    return dp;
+}
+
+int Solver::part_of_row(int i) const {
+    for (size_t p = 0; p < parts_.size(); ++p)
+        if (i >= parts_[p].row0 && i < parts_[p].row0 + parts_[p].rows) return (int)p;
+    throw Error(LPSG_CUDA_ERROR, "row outside every partition");
+}
+
+// upload_partition / download_resident (tiled_engine.cpp:165-184): the slab's
+// partition goes back to the host before another one comes up.
+void Solver::ensure_resident(int p) {
+    if (resident_ == p) return;
+    ev_chain_ = nullptr;
+    const size_t w = sizeof(double);
+    if (resident_ >= 0) {
+        const Part& q = parts_[resident_];
+        CK(cudaMemcpy2DAsync(q.host, w * q.rows, d_.T, w * d_.ldT, w * q.rows, m_ + 1, cudaMemcpyDeviceToHost, st_));
+        d2h_bytes += (long long)(w * q.rows * (m_ + 1));
+    }
+    const Part& q = parts_[p];
+    CK(cudaMemcpy2DAsync(d_.T, w * d_.ldT, q.host, w * q.rows, w * q.rows, m_ + 1, cudaMemcpyHostToDevice, st_));
+    h2d_bytes += (long long)(w * q.rows * (m_ + 1));
+    resident_ = p;
+}
+
+// One partitioned update (tiled_engine.cpp:246-263): the resident partition
+// first, then the others in order; the last one stays resident. Each launch
+// is the fused k_update of the in-core path on that partition (update(t),
+// FTRAN(t+1), the ratio test's partition message); the messages are merged
+// after the last one.
+void Solver::tiled_pass() {
+    const int P = (int)parts_.size();
+    std::vector<int> order;
+    if (resident_ >= 0) order.push_back(resident_);
+    for (int p = 0; p < P; ++p)
+        if (p != resident_) order.push_back(p);
+    for (int k = 0; k < P; ++k) {
+        const int p = order[k];
+        ensure_resident(p);
+        Dev dp = part_dev(p);
+        dp.keep_pending = k + 1 < P ? 1 : 0;
+        L(K_UPDATE, bytes_of(K_UPDATE), [&] { launch_update(dp, st_); });
+    }
+    L(K_OTHER, 0.0, [&] { launch_ratio_merge_parts(d_, part_msgs_, part_row0_, P, st_); });
+    CK(cudaGetLastError());
+}
+
+// pivot_update's division (solver.cpp:246-247) of row r, then k_pivot. The
+// resident partition divides in place in the slab; any other partition's row
+// is gathered from its host copy into the pivot-row buffer, divided there and
+// written back (the reference divides host-side and uploads the pivot row,
+// tiled_engine.cpp:232-235).
+void Solver::tiled_pivot() {
+    const int r = hctl_->r;
+    const int p = part_of_row(r);
+    if (p == resident_) {
+        const Dev dr = part_dev(p);
+        L(K_PIVOT, 0.0, [&] { launch_pivot_row(dr, st_); });
+    } else {
+        const Part& q = parts_[p];
+        const int li = r - q.row0;
+        const size_t w = sizeof(double);
+        ev_chain_ = nullptr;
+        CK(cudaMemcpy2DAsync(d_.xbuf, w, q.host + li, w * q.rows, w, m_ + 1, cudaMemcpyHostToDevice, st_));
+        Dev dx = d_;
+        dx.T = d_.xbuf;  // the row as a one-row slab
+        dx.ldT = 1;
+        dx.row0 = r;
+        dx.mloc = 1;
+        dx.Y = d_.Y + r;
+        dx.sharded = 1;
+        L(K_PIVOT, 0.0, [&] { launch_pivot_row(dx, st_); });
+        ev_chain_ = nullptr;
+        CK(cudaMemcpy2DAsync(q.host + li, w * q.rows, d_.xbuf, w, w, m_ + 1, cudaMemcpyDeviceToHost, st_));
+        h2d_bytes += (long long)(w * (m_ + 1));
+        d2h_bytes += (long long)(w * (m_ + 1));
+    }
+    Dev dk = d_;
+    dk.sharded = 1;
+    L(K_PIVOT, bytes_of(K_PIVOT), [&] { launch_pivot(dk, st_); });
+    CK(cudaGetLastError());
+}
+
+// run_phase (solver.cpp:278-293) for Case 2: the fused schedule of run_phase
+// (pivot(t), price(t+1), one pass over the partitions for update(t) +
+// FTRAN(t+1) + ratio), one pivot per host round trip: the host needs r to
+// place the pivot-row division.
+int Solver::run_phase_tiled() {
+    hctl_->status = ST_RUNNING;
+    hctl_->pending = 0;
+    hctl_->no_ftran = 0;
+    hctl_->no_ratio = 0;
+    hctl_->phase = phase_;
+    push();
+    seq_price();
+    tiled_pass();
+    pull(true);
+    if (prof_) flush_profile();
+    for (;;) {
+        const int st = hctl_->status;
+        if (st != ST_RUNNING) {
+            bool resumed = false;
+            const int out = handle_stop(st, &resumed);
+            if (!resumed) return out;
+        }
+        tiled_pivot();
+        seq_price();
+        tiled_pass();
+        pull(true);
+        if (prof_) flush_profile();
+        if (hctl_->status == ST_PIVOT_ERR) throw Error(LPSG_PIVOT_TOO_SMALL, "pivot element below pivot_tol");
+        drain_log();
+    }
+}
+
+// Row i of [B^-1 | b_bar] (m+1 doubles) into device memory `out`, wherever it lives.
+void Solver::gather_row_any(int i, double* out) {
+    if (!tiled_) {
+        launch_gather_row(d_, i - d_.row0, out, st_);
+        return;
+    }
+    const int p = part_of_row(i);
+    const Part& q = parts_[p];
+    if (p == resident_) {
+        launch_gather_row(part_dev(p), i - q.row0, out, st_);
+    } else {
+        const size_t w = sizeof(double);
+        CK(cudaMemcpy2DAsync(out, w, q.host + (i - q.row0), w * q.rows, w, m_ + 1, cudaMemcpyHostToDevice, st_));
+        h2d_bytes += (long long)(w * (m_ + 1));
+    }
+}
+
 // drive_out_artificials (solver.cpp:295-316)
 void Solver::drive_out_artificials() {
     for (int i = 0; i < m_; ++i) {
@@ -1175,7 +1481,7 @@ void Solver::drive_out_artificials() {
         hctl_->status = ST_HOLD;
         push();
         const int owner = owner_of_row(i);
-        if (owner == rank_) launch_gather_row(d_, i - d_.row0, scratch_, st_);
+        if (owner == rank_) gather_row_any(i, scratch_);
         if (sharded_) comm_->bcast(scratch_, sizeof(double) * (m_ + 1), owner, st_);
         launch_drive_scan(d_, scratch_, st_);
         if (sharded_) comm_->min_i32(&d_.ctl->found, 1, st_);
@@ -1280,7 +1586,7 @@ void Solver::solve(lpsg_report* rep) {
     rep->iterations_phase2 = phase_iter_[1];
     rep->total_seconds = t1 - t0;
     rep->tpi_seconds = rep->total_seconds / (double)std::max<long long>(1, total_iter_);
-    rep->case_used = 0;
+    rep->case_used = tiled_ ? 1 : 0;
 }
 
 // report.x (solver.cpp:378-383)
@@ -1290,7 +1596,16 @@ void Solver::get_x(double* x, int n) {
     if (solved_ && !(final_status_ == LPSG_OPTIMAL || final_status_ == LPSG_ITERATION_LIMIT)) return;
     std::vector<double> bbar(m_);
     const double* bcol = d_.T + (size_t)m_ * d_.ldT;
-    if (!sharded_) {
+    if (tiled_) {
+        CK(cudaStreamSynchronize(st_));
+        for (size_t p = 0; p < parts_.size(); ++p) {
+            const Part& q = parts_[p];
+            if ((int)p == resident_)
+                CK(cudaMemcpyAsync(bbar.data() + q.row0, bcol, sizeof(double) * q.rows, cudaMemcpyDeviceToHost, st_));
+            else
+                std::memcpy(bbar.data() + q.row0, q.host + (size_t)m_ * q.rows, sizeof(double) * q.rows);
+        }
+    } else if (!sharded_) {
         CK(cudaMemcpyAsync(bbar.data(), bcol, sizeof(double) * m_, cudaMemcpyDeviceToHost, st_));
     } else {
         // every shard's b_bar rows, padded to the largest shard, in rank order
@@ -1409,7 +1724,7 @@ void Solver::read_row(int i, double* out) {
         const int owner = owner_of_row(i - 1);
         if (owner == rank_) {
             const int li = i - 1 - d_.row0;
-            launch_gather_row(d_, li, scratch_, st_);
+            gather_row_any(i - 1, scratch_);
             CK(cudaMemcpyAsync(scratch_ + m_ + 1, d_.Y + li, sizeof(double), cudaMemcpyDeviceToDevice, st_));
         }
         if (sharded_) comm_->bcast(scratch_, sizeof(double) * (m_ + 2), owner, st_);

@@ -41,7 +41,12 @@ class CudaError(Error):
     """Device failure (no CUDA device, launch error, out of memory)."""
 
 
-_ERRORS = {1: PivotTooSmall, 2: CudaError, 3: CudaError, 4: Error, 5: CudaError, 6: DegenerateSpec}
+class BudgetTooSmall(Error):
+    """lps::BudgetTooSmall (tiled_engine.cpp:43-47)."""
+
+
+_ERRORS = {1: PivotTooSmall, 2: CudaError, 3: CudaError, 4: Error, 5: CudaError, 6: DegenerateSpec,
+           7: BudgetTooSmall}
 
 
 def _check(rc: int) -> None:
@@ -105,6 +110,9 @@ class SolverConfig:
     # opt-in periodic reinversion on the device (NOT bit-identical to the
     # reference; include/lpsg.h lpsg_config.reinvert_every): 0 = off
     reinvert_every: int = 0
+    # lps::SolverConfig::memory_budget (solver.hpp:41): device bytes for the
+    # tableau; over it the solve runs Case 2 (out-of-core, tiled). 0 = unlimited.
+    memory_budget: int = 0
 
     def _c(self) -> L.Config:
         c = L.Config()
@@ -118,6 +126,7 @@ class SolverConfig:
         c.reserved[1] = 1 if self.nccl_single else 0
         c.peer = self.peer.ptr if self.peer is not None else None
         c.reinvert_every = int(self.reinvert_every)
+        c.memory_budget = int(self.memory_budget)
         # (tools/dbg set `_experiment` on an instance; it only has an effect in
         # the -DLPSG_EXPERIMENTS library, LPSG_EXPERIMENTS_LIB=1)
         c.reserved[2] = (16 if self.lookahead_exact_select else 0) | (
@@ -347,7 +356,7 @@ class SimplexSolver:
                                    self.lp.n_total))
         return SolveReport(SolveStatus(rep.status), rep.objective, x, rep.iterations_phase1,
                            rep.iterations_phase2, rep.total_seconds, rep.tpi_seconds,
-                           memory=self.memory())
+                           "Tiled" if rep.case_used == 1 else "InCore", memory=self.memory())
 
     def reinvert_stats(self) -> dict:
         """Reinversion mode: rebuilds, Newton steps, max|I - B X| before / after
