@@ -1511,12 +1511,6 @@ struct LaPriceSmem {
     double W[kLS][kLC][kLK];   // [i][k]
     double A[kLS][kLC][kLN];   // [i][s]
 };
-struct LaThetaSmem {
-    double T[kLS][kLC][kLN];   // [j][i]
-    double X[kLS][kLC][kLK];   // [j][k]
-    double B[kLS][kLC][kLK];   // [j][k]  a_{b_k}[j]
-    int bj[kLK], rk[kLK];
-};
 
 // z_k(s) = dot(W'_k, a_s) - c_j over this shard's slots (j = slot2col[s] != q):
 // the best (z, j) of the tile's 128 slots per candidate -> part_z/part_j[k][bx].
@@ -1742,106 +1736,104 @@ __global__ void __launch_bounds__(kDT) k_la_own(Dev d, LookaheadDev la) {
     la.own_t[k] = th;
 }
 
+constexpr int kLT = 64;  // theta tile edge
+
 // y'_ik = sum_j t_ij(k) a_{b_k}[j] for this shard's rows, t = X_kj on the
 // candidate's own row, T_ij where y_i == 0, else T_ij - y_i X_kj (solver.cpp:
-// 177-184, 203-210); theta'_k partial (min ratio) per 128-row tile -> part_t[k][bx].
-__global__ void __launch_bounds__(kLThreads, 2) k_la_gemm_theta(Dev d, LookaheadDev la) {
-    extern __shared__ __align__(16) unsigned char la_smem[];
-    LaThetaSmem& sm = *reinterpret_cast<LaThetaSmem*>(la_smem);
+// 177-184, 203-210); theta'_k partial (min ratio) per 64-row tile -> part_t[k][bx].
+// 64 x 64 tiles, 4 x 4 outputs per thread over 256 threads, register-staged
+// 16-deep chunks: at C4 this measured 13.6 TFLOP/s against 11.4-12.1 for 8 x 4
+// / 8 x 8 tiles fed by a cp.async ring (those have half the CTAs per round, so
+// a larger wave tail, and more long-scoreboard stalls; profiles/r02_c4_*).
+__global__ void __launch_bounds__(256, 2) k_la_gemm_theta(Dev d, LookaheadDev la) {
+    __shared__ double Ts[kLC][kLT];      // [j][i]
+    __shared__ double Xs[kLC][kLT + 1];  // [j][k]
+    __shared__ double Bs[kLC][kLT + 1];  // [j][k]  a_{b_k}[j]
+    __shared__ int s_bj[kLT], s_rk[kLT];
     const int m = d.m;
-    const int i0 = blockIdx.x * kLN, k0 = blockIdx.y * kLK;
-    // thread (ti, tk): rows ti + 16 u (u < 8), candidates tk * 4 + v (v < 4; two LDS.128 each of X and a_b)
+    const int i0 = blockIdx.x * kLT, k0 = blockIdx.y * kLT;
     const int t = threadIdx.x, ti = t & 15, tk = t >> 4;
-    if (t < kLK) {
+    if (t < kLT) {
         const int k = k0 + t;
-        sm.bj[t] = k < la.K ? la.bj[k] : -1;
-        sm.rk[t] = k < la.K ? la.rows[k] : -1;
+        s_bj[t] = k < la.K ? la.bj[k] : -1;
+        s_rk[t] = k < la.K ? la.rows[k] : -1;
     }
     __syncthreads();
     bool any = false;
-    for (int kk = 0; kk < kLK; ++kk) any |= sm.bj[kk] >= 0;
+    for (int kk = 0; kk < kLT; ++kk) any |= s_bj[kk] >= 0;
     if (!any) {  // no candidate of this tile has an entering column: score 0
         if (ti == 0)
             for (int v = 0; v < 4; ++v) {
-                const int k = k0 + tk * 4 + v;
+                const int k = k0 + tk + 16 * v;
                 if (k < la.K) la.part_t[(size_t)k * la.nblk_t + blockIdx.x] = kInf;
             }
         return;
     }
-    double yv[8];
-    bool rowok[8], zrow[8];
+    double yv[4];
+    bool rowok[4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < 4; ++u) {
         const int li = i0 + ti + 16 * u;
         rowok[u] = li < d.mloc;
         yv[u] = rowok[u] ? d.Y[li] : 0.0;
-        zrow[u] = yv[u] == 0.0;
     }
-    double acc[8][4];
+    double acc[4][4];
 #pragma unroll
-    for (int u = 0; u < 8; ++u)
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
     // Chains use T_ij - y_i X_kj; rows with y_i == 0 keep T_ij exactly as the
     // reference does (solver.cpp:177-184: T - 0*X would flip a -0 entry of a
-    // former pivot row). The candidate's own row (t = X_kj) is skipped here and
-    // handled by k_la_own. Some X_kj inf/NaN: keep the select (la_exact forces
-    // it: a parity check of that path, tests/test_gpu_parity.py).
+    // former pivot row). The row kind is fixed per thread row, so it costs one
+    // select per element. The candidate's own row (t = X_kj) is skipped here and
+    // handled by k_la_own.
+    bool zrow[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) zrow[u] = yv[u] == 0.0;
+    // some X_kj is inf/NaN: keep the select (la_exact forces it: a parity check
+    // of that path, tests/test_gpu_parity.py)
     const bool exact = *la.nonfinite != 0 || d.la_exact != 0;
-    auto issue = [&](int stage, int j0) {
+    double rt[4], rx[4], rb[4];
+    auto fetch = [&](int j0) {
 #pragma unroll
-        for (int q = 0; q < kLC * kLN / (2 * kLThreads); ++q) {  // T: 16 columns x 128 rows, 16-byte copies
-            const int e = t + kLThreads * q;
-            const int ip = e % (kLN / 2), jj = e / (kLN / 2);
-            const int li = i0 + 2 * ip, j = j0 + jj;
-            const int nb = (j < m) ? 8 * max(0, min(2, d.mloc - li)) : 0;
-            cp_async16(&sm.T[stage][jj][2 * ip], nb ? d.T + (size_t)j * d.ldT + li : d.T, nb);
-        }
-#pragma unroll
-        for (int q = 0; q < kLC * kLK / kLThreads; ++q) {  // X and a_{b_k}: 16 x 64, candidate-fast
-            const int e = t + kLThreads * q;
-            const int kk = e % kLK, jj = e / kLK;
-            const int k = k0 + kk, j = j0 + jj;
-            const bool ok = k < la.K && j < m;
-            cp_async8(&sm.X[stage][jj][kk], ok ? la.X + (size_t)k * la.ldx + j : la.X, ok);
-            const int bj = sm.bj[kk];
-            const bool okb = ok && bj >= 0;
-            cp_async8(&sm.B[stage][jj][kk], okb ? d.A_cm + (size_t)bj * d.ld_cm + j : d.A_cm, okb);
+        for (int q = 0; q < 4; ++q) {
+            const int e = t + 256 * q;
+            const int ii = e % kLT, jj = e / kLT;
+            const int li = i0 + ii, j = j0 + jj;
+            rt[q] = (li < d.mloc && j < m) ? d.T[(size_t)j * d.ldT + li] : 0.0;
+            const int jx = e % kLC, kk = e / kLC;
+            const int k = k0 + kk, j2 = j0 + jx;
+            const bool okk = k < la.K && j2 < m;
+            rx[q] = okk ? la.X[(size_t)k * la.ldx + j2] : 0.0;
+            rb[q] = (okk && s_bj[kk] >= 0) ? d.A_cm[(size_t)s_bj[kk] * d.ld_cm + j2] : 0.0;
         }
     };
-    const int nch = (m + kLC - 1) / kLC;
+    fetch(0);
+    for (int j0 = 0; j0 < m; j0 += kLC) {
 #pragma unroll
-    for (int st = 0; st < kLS - 1; ++st) {
-        if (st < nch) issue(st, st * kLC);
-        cp_async_commit();
-    }
-    for (int ch = 0; ch < nch; ++ch) {
-        cp_async_wait<kLS - 2>();
+        for (int q = 0; q < 4; ++q) {
+            const int e = t + 256 * q;
+            Ts[e / kLT][e % kLT] = rt[q];
+            Xs[e % kLC][e / kLC] = rx[q];
+            Bs[e % kLC][e / kLC] = rb[q];
+        }
         __syncthreads();
-        if (ch + kLS - 1 < nch) issue((ch + kLS - 1) % kLS, (ch + kLS - 1) * kLC);
-        cp_async_commit();
-        const int stg = ch % kLS;
-        const int lim = min(kLC, m - ch * kLC);
+        if (j0 + kLC < m) fetch(j0 + kLC);
         // exact: rows with y_i == 0 take T_ij itself (a select per element).
         // fast: T_ij - y_i X_kj for every row. With y_i = +-0 and X_kj finite
         // that differs from T_ij only in the sign of a zero, and a zero term
         // never changes the chain (acc starts at +0.0 and round-to-nearest
         // never produces -0.0 from it), so the chains are bit-identical.
         auto step = [&](int jj, auto sel) {
-            double tv[8], xv[4], bv[4];
+            double tv[4], xv[4], bv[4];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) tv[u] = sm.T[stg][jj][ti + 16 * u];
-#pragma unroll
-            for (int v = 0; v < 4; v += 2) {
-                const double2 x2 = *reinterpret_cast<const double2*>(&sm.X[stg][jj][tk * 4 + v]);
-                const double2 b2 = *reinterpret_cast<const double2*>(&sm.B[stg][jj][tk * 4 + v]);
-                xv[v] = x2.x;
-                xv[v + 1] = x2.y;
-                bv[v] = b2.x;
-                bv[v + 1] = b2.y;
+            for (int u = 0; u < 4; ++u) {
+                tv[u] = Ts[jj][ti + 16 * u];
+                xv[u] = Xs[jj][tk + 16 * u];
+                bv[u] = Bs[jj][tk + 16 * u];
             }
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
+            for (int u = 0; u < 4; ++u)
 #pragma unroll
                 for (int v = 0; v < 4; ++v) {
                     const double sub = dsub(tv[u], dmul(yv[u], xv[v]));
@@ -1849,29 +1841,26 @@ __global__ void __launch_bounds__(kLThreads, 2) k_la_gemm_theta(Dev d, Lookahead
                 }
         };
         if (exact) {
-            for (int jj = 0; jj < lim; ++jj) step(jj, std::true_type{});
-        } else if (lim == kLC) {
-            // partially unrolled: a fully unrolled 16-row body of 8 x 8 tiles
-            // (~70 KB of SASS) missed the instruction cache (ncu: stall
-            // no_instructions on top)
-#pragma unroll 4
+            for (int jj = 0; jj < min(kLC, m - j0); ++jj) step(jj, std::true_type{});
+        } else if (j0 + kLC <= m) {
+#pragma unroll
             for (int jj = 0; jj < kLC; ++jj) step(jj, std::false_type{});
         } else {
-            for (int jj = 0; jj < lim; ++jj) step(jj, std::false_type{});
+            for (int jj = 0; jj < m - j0; ++jj) step(jj, std::false_type{});
         }
+        __syncthreads();
     }
-    cp_async_wait<0>();
     const double* bcol = d.T + (size_t)m * d.ldT;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-        const int kk = tk * 4 + v, k = k0 + kk;
+        const int kk = tk + 16 * v, k = k0 + kk;
         double th = kInf;
-        if (k < la.K && sm.bj[kk] >= 0) {
+        if (k < la.K && s_bj[kk] >= 0) {
             const double xm = la.X[(size_t)k * la.ldx + m];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 4; ++u) {
                 const int li = i0 + ti + 16 * u;
-                if (!rowok[u] || d.frozen[d.row0 + li] || d.row0 + li == sm.rk[kk]) continue;
+                if (!rowok[u] || d.frozen[d.row0 + li] || d.row0 + li == s_rk[kk]) continue;
                 if (acc[u][v] <= d.pivot_tol) continue;
                 const double bb = zrow[u] ? bcol[li] : dsub(bcol[li], dmul(yv[u], xm));
                 th = min_keep(th, ddiv(bb, acc[u][v]));
@@ -2066,7 +2055,6 @@ void configure_kernels(Dev& d) {
     cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, d.upd_smem);
     cudaFuncSetAttribute(k_price, cudaFuncAttributeMaxDynamicSharedMemorySize, d.price_smem);
     cudaFuncSetAttribute(k_la_gemm_price, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaPriceSmem));
-    cudaFuncSetAttribute(k_la_gemm_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaThetaSmem));
     // One shared-memory carveout for every kernel: SMs never reconfigure the
     // L1/shared split between the streaming kernels and the small ones, and a
     // shard's spin-waiting exchange kernel can share an SM with another shard's
@@ -2176,7 +2164,7 @@ void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int 
 }
 
 void launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st) {
-    k_la_gemm_theta<<<dim3(la.nblk_t, (la.K + kLK - 1) / kLK), kLThreads, sizeof(LaThetaSmem), st>>>(d, la);
+    k_la_gemm_theta<<<dim3(la.nblk_t, (la.K + kLT - 1) / kLT), 256, 0, st>>>(d, la);
     k_la_own<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
     k_la_theta_local<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);
 }

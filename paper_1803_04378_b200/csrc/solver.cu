@@ -1104,7 +1104,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     la.ldx = ldx;
     la.q = entering;
     la.nblk = (hctl_->n_scan + 127) / 128 + 1;  // 128-slot tiles + the leaving column
-    la.nblk_t = std::max(1, (d_.mloc + 127) / 128);  // 128-row tiles
+    la.nblk_t = std::max(1, (d_.mloc + 63) / 64);  // 64-row theta tiles
     int* rows_d = talloc<int>(kb, st_, pool_);
     la.rows = rows_d;
     la.X = talloc<double>((size_t)kb * ldx, st_, pool_);
