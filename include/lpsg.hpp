@@ -85,6 +85,8 @@ struct SolverConfig {  // solver.hpp:34-45
     int workers = 1;  // accepted, ignored (results are worker-independent)
     IterationObserver observer;
     bool observer_rows = false;  // IterationView::row readable (unfused, one pivot per round trip)
+    unsigned long long memory_budget = 0;  // MemoryBudget (solver.hpp:41): tableau bytes; 0 = unlimited
+    long reinvert_every = 0;  // opt-in device reinversion (NOT bit-identical to the reference)
     int device = 0;
 };
 
@@ -163,6 +165,8 @@ inline lpsg_config to_c(const SolverConfig& cfg) {
     c.anticycle = cfg.anticycle == Anticycle::none ? 1 : 0;
     c.kernel = cfg.kernel == KernelMode::naive ? 1 : 0;
     c.workers = cfg.workers;
+    c.memory_budget = cfg.memory_budget;
+    c.reinvert_every = cfg.reinvert_every;
     c.device = cfg.device;
     return c;
 }
@@ -183,7 +187,12 @@ public:
             ctx_.obs = &cfg_.observer;
             ctx_.rows = cfg_.observer_rows;
             ctx_.buf.assign(static_cast<std::size_t>(m_) + 2, 0.0);
-            check(lpsg_set_view_observer(h_, &detail::view_trampoline, &ctx_, cfg_.observer_rows ? 1 : 0));
+            const int rc = lpsg_set_view_observer(h_, &detail::view_trampoline, &ctx_, cfg_.observer_rows ? 1 : 0);
+            if (rc != LPSG_OK) {
+                const std::string msg = lpsg_last_error();
+                lpsg_destroy(h_);  // the destructor does not run for a throwing constructor
+                throw OtherErr(msg);
+            }
         }
     }
     ~BasicSimplexSolver() { lpsg_destroy(h_); }
