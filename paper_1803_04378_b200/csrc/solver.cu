@@ -888,13 +888,10 @@ void Solver::seq_update() {
     d_.fused = 0;
 }
 
-// One pivot per iteration. With the fused pivot (d_.fuse_pivot) the previous
-// k_update's last CTA already ran pivot_update, so a pivot is k_price +
-// k_update; otherwise k_pivot (or the sharded pivot-row exchange) leads.
 void Solver::enqueue_pivots(int n) {
     for (int k = 0; k < n; ++k) {
         if (unfused_ratio_) L(K_RATIO, bytes_of(K_RATIO), [&] { launch_ratio(d_, st_); });
-        if (!d_.fuse_pivot) seq_pivot();
+        seq_pivot();
         seq_price();
         seq_update();
     }
@@ -936,11 +933,6 @@ std::vector<int> Solver::gather_overflow_candidates() {
 
 // run_phase (solver.cpp:278-293) in the fused schedule.
 int Solver::run_phase() {
-    d_.fuse_pivot = (!sharded_ && !unfused_ratio_ && !tiled_ && xp_env("LPSG_NO_FUSED_PIVOT") == nullptr) ? 1 : 0;
-    struct Unfuse {
-        Dev& d;
-        ~Unfuse() { d.fuse_pivot = 0; }  // every other schedule pivots with k_pivot
-    } unfuse{d_};
     hctl_->status = ST_RUNNING;
     hctl_->pending = 0;
     hctl_->no_ftran = 0;

@@ -58,6 +58,11 @@ KEYS = {
     "sm__throughput.avg.pct_of_peak_sustained_elapsed": "sm_pct",
     "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum": "smem_bank_conflicts",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active": "fp64_pipe_pct",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active": "issue_pct",
+    "sm__warps_active.avg.per_cycle_active": "warps_per_sm",
+    "sm__cycles_active.avg": "sm_cycles_active",
+    "gpc__cycles_elapsed.max": "cycles_elapsed",
 }
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
         "ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3,
@@ -82,6 +87,12 @@ def capture(path):
             for k, v in d.items() if k.startswith("smsp__average_warps_issue_stalled_")
             and k.endswith("_per_issue_active.ratio")}
         e["top_stalls_cycles_per_issue"] = dict(sorted(stalls.items(), key=lambda kv: -kv[1])[:5])
+        samp = {k.replace("smsp__pcsamp_warps_issue_stalled_", ""): float(v.replace(",", "") or 0)
+                for k, v in d.items() if k.startswith("smsp__pcsamp_warps_issue_stalled_")
+                and not k.endswith("_not_issued")}
+        tot = sum(samp.values()) or 1.0
+        e["top_stalls_pc_samples_share"] = {k: round(v / tot, 3) for k, v in
+                                            sorted(samp.items(), key=lambda kv: -kv[1])[:8]}
         if "dram_read" in e and "dram_write" in e:
             e["traffic_bytes"] = e["dram_read"] + e["dram_write"]
         if "duration" in e and "traffic_bytes" in e:
@@ -105,7 +116,9 @@ def main():
     caps = []
     for r in a.rep:
         caps += capture(r)
-    out["captures"] = {c["kernel"]: c for c in caps}
+    names = [c["kernel"] for c in caps]
+    out["captures"] = {(c["kernel"] if names.count(c["kernel"]) == 1 else f'{c["kernel"]}@{c["source"]}'): c
+                       for c in caps}
     path = os.path.join(ROOT, "profiles", f"{a.tag}_ncu_summary.json")
     with open(path, "w") as f:
         json.dump(out, f, indent=1)
