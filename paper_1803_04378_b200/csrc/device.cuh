@@ -177,6 +177,8 @@ struct Dev {
                            // through LPSG_XP, i.e. only in a -DLPSG_EXPERIMENTS build
     int la_exact;          // lookahead theta' keeps the y_i == 0 select (cfg.reserved[2] bit 4):
                            // result-identical verification mode
+    int fuse_pivot;        // single GPU, fused schedule: k_update's last CTA also runs pivot_update
+                           // of the row its ratio test chose (no k_pivot launch on that path)
     int keep_pending;      // Case 2 (tiled): this k_update launch is not the last partition of the
                            // pass, so its last CTA leaves ctl.pending set for the next one
     int naive;             // KernelMode::naive (tiled_engine.cpp:61-77): every element is stored,

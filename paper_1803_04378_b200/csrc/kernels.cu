@@ -716,6 +716,99 @@ __device__ __forceinline__ void ratio_put(const Dev& d) {
     peer_signal(a);
 }
 
+// pivot_update (solver.cpp:240-254) of row r = ctl.r, run by ONE CTA: the
+// tail of k_update once its last CTA has decided r (single GPU, no tie,
+// m + 1 <= kPivotPF * blockDim.x). Same arithmetic and bookkeeping as k_pivot,
+// which it replaces on that path: one kernel boundary per pivot less.
+constexpr int kPivotPF = 16;
+__device__ void pivot_cta(const Dev& d, Ctl* c) {
+    const int m = d.m;
+    const int r = ((volatile int*)&c->r)[0], q = c->q, n_scan = c->n_scan;
+    const size_t ldT = (size_t)d.ldT;
+    const double yr = __ldcg(d.Y + r);
+    if (fabs(yr) <= d.pivot_tol) {
+        if (threadIdx.x == 0) c->status = ST_PIVOT_ERR;
+        return;
+    }
+    const double dk = ((volatile double*)d.top)[m + 1];
+    const double ndk = -dk;
+    const int p_leave = d.basic[r];
+    const int s_q = q < d.n_total ? d.col2slot[q] : -1;
+    const int last_col = n_scan > 0 ? d.slot2col[n_scan - 1] : -1;
+    const bool p_local = p_leave < d.n_total && p_leave >= d.col0 && p_leave < d.col1;
+    const bool q_local = s_q >= 0;
+    int dst = -1, src_col = -1;
+    if (p_local) {
+        dst = q_local ? s_q : n_scan;
+        src_col = p_leave;
+    } else if (q_local && s_q != n_scan - 1) {
+        dst = s_q;
+        src_col = last_col;
+    }
+    const double xl = ddiv(yr, yr);
+    const int li = c->log_len;
+    LogEntry* const ent = d.log + li % d.log_cap;
+    // every load first (kPivotPF per thread, all in flight together), then the
+    // arithmetic and the stores: row r of T is m+1 strided elements, and a
+    // load-divide-store loop would serialise one memory round trip per element
+    double tv[kPivotPF], wv[kPivotPF], av[kPivotPF];
+    const double* __restrict__ src = d.A_cm + (size_t)(dst >= 0 ? src_col : 0) * d.ld_cm;
+#pragma unroll
+    for (int u = 0; u < kPivotPF; ++u) {
+        const int j = threadIdx.x + u * blockDim.x;
+        tv[u] = j <= m ? __ldcg(d.T + (size_t)j * ldT + r) : 0.0;
+        wv[u] = j <= m ? d.top[j] : 0.0;
+        av[u] = (dst >= 0 && j < m) ? src[j] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPivotPF; ++u) {
+        const int j = threadIdx.x + u * blockDim.x;
+        if (j > m) break;
+        const double x = ddiv(tv[u], yr);
+        d.xrow[j] = x;
+        d.T[(size_t)j * ldT + r] = x;  // in place, like pr[j] /= y_rk (solver.cpp:246-247)
+        const double p = dmul(ndk, x);
+        const bool wr = d.naive || p != 0.0;
+        const double nt = wr ? dadd(wv[u], p) : wv[u];
+        if (wr) d.top[j] = nt;
+        if (j == m) ent->objective = nt;
+        if (dst >= 0 && j < m) d.A_nb[(size_t)j * d.ld_nb + dst] = av[u];
+    }
+    __syncthreads();  // every read of the d slot and the slot maps precedes their rewrite
+    if (threadIdx.x != 0) return;
+    d.xrow[m + 1] = xl;
+    c->work[2] += 1;
+    {
+        const double p = dmul(ndk, xl);
+        if (d.naive || p != 0.0) d.top[m + 1] = dadd(dk, p);
+    }
+    int ns = n_scan;
+    if (p_local) {
+        if (!q_local) ++ns;
+        d.slot2col[dst] = p_leave;
+        d.col2slot[p_leave] = dst;
+    } else if (q_local) {
+        if (dst >= 0) {
+            d.slot2col[dst] = src_col;
+            d.col2slot[src_col] = dst;
+        }
+        --ns;
+    }
+    if (q < d.n_total) d.col2slot[q] = -1;
+    c->n_scan = ns;
+    d.basic[r] = q;
+    c->total_iter += 1;
+    ent->iteration = c->total_iter;
+    ent->phase = c->phase;
+    ent->row = r;
+    ent->leaving = p_leave;
+    ent->entering = q;
+    c->log_len = li + 1;
+    c->pending = 1;
+    c->upd_r = r;
+    c->upd_q = q;
+}
+
 // --------------------------------------------------------- update+FTRAN ---
 // tiled_engine.cpp:230-266 with tile_kernel's cached mode (79-106) fused with the
 // NEXT pivot's compute_direction (solver.cpp:131-136), SURVEY.md Appendix B.
@@ -811,6 +904,9 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                 if (++rel == S) rel = 0;
             }
             bulk_wait_all();
+            // the fused pivot in the last CTA reads row r of T with generic
+            // loads: order these async-proxy writes before them
+            asm volatile("fence.proxy.async.global;" ::: "memory");
         }
     } else if (warp < U) {
         // ---- update warps: warp-per-column, lane-per-row-pair (double2), rows
@@ -1025,6 +1121,9 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         else
             c->status = ST_TIE;
     }
+    if (!d.fuse_pivot) return;
+    __syncthreads();
+    if (((volatile int*)&c->status)[0] == ST_RUNNING) pivot_cta(d, c);
 }
 
 // world > 1: global ratio test over the gathered shard messages

@@ -888,10 +888,13 @@ void Solver::seq_update() {
     d_.fused = 0;
 }
 
+// One pivot per iteration. With the fused pivot (d_.fuse_pivot) the previous
+// k_update's last CTA already ran pivot_update, so a pivot is k_price +
+// k_update; otherwise k_pivot (or the sharded pivot-row exchange) leads.
 void Solver::enqueue_pivots(int n) {
     for (int k = 0; k < n; ++k) {
         if (unfused_ratio_) L(K_RATIO, bytes_of(K_RATIO), [&] { launch_ratio(d_, st_); });
-        seq_pivot();
+        if (!d_.fuse_pivot) seq_pivot();
         seq_price();
         seq_update();
     }
@@ -933,6 +936,14 @@ std::vector<int> Solver::gather_overflow_candidates() {
 
 // run_phase (solver.cpp:278-293) in the fused schedule.
 int Solver::run_phase() {
+    // the fused pivot needs the whole pivot row in one CTA's registers
+    // (kernels.cu pivot_cta: 16 elements per thread)
+    d_.fuse_pivot = (!sharded_ && !unfused_ratio_ && !tiled_ && (long long)m_ + 1 <= 16LL * d_.upd_threads &&
+                     xp_env("LPSG_NO_FUSED_PIVOT") == nullptr) ? 1 : 0;
+    struct Unfuse {
+        Dev& d;
+        ~Unfuse() { d.fuse_pivot = 0; }  // every other schedule pivots with k_pivot
+    } unfuse{d_};
     hctl_->status = ST_RUNNING;
     hctl_->pending = 0;
     hctl_->no_ftran = 0;

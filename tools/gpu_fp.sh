@@ -6,7 +6,7 @@ timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_mps.py tes
 echo "pytest rc=$?" >> gpurun_out/pt_fp_$TAG.log
 timeout 1500 python -m pytest tests/test_gpu_large.py -q -x --timeout 900 -p no:cacheprovider -k "single" > gpurun_out/pt_fp_large_$TAG.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pt_fp_large_$TAG.log
-for c in c1 c2 c3; do timeout 600 python bench.py --config $c --steps 1000 --warmup 20 --no-cpu-baseline --e2e-max-iter 2000 --no-reinversion > gpurun_out/bench_${c}_$TAG.log 2>&1; done
+for c in c1 c2 c3; do timeout 600 python bench.py --config $c --steps 400 --warmup 20 --no-cpu-baseline --e2e-max-iter 2000 --no-reinversion > gpurun_out/bench_${c}_$TAG.log 2>&1; done
 tail -n 3 gpurun_out/pt_fp_$TAG.log; tail -n 3 gpurun_out/pt_fp_large_$TAG.log
 python - <<PY
 import json
