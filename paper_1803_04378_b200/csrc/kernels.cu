@@ -720,7 +720,7 @@ __device__ __forceinline__ void ratio_put(const Dev& d) {
 // tail of k_update once its last CTA has decided r (single GPU, no tie,
 // m + 1 <= kPivotPF * blockDim.x). Same arithmetic and bookkeeping as k_pivot,
 // which it replaces on that path: one kernel boundary per pivot less.
-constexpr int kPivotPF = 16;
+constexpr int kPivotPF = 4;
 __device__ void pivot_cta(const Dev& d, Ctl* c) {
     const int m = d.m;
     const int r = ((volatile int*)&c->r)[0], q = c->q, n_scan = c->n_scan;
