@@ -71,7 +71,6 @@ typedef struct {
     int workers;           /* ignored */
     int device;            /* CUDA device ordinal, default 0 */
     int batch;             /* pivots enqueued per host check (0 = auto) */
-    int use_graphs;        /* reserved (CUDA-graph capture of pivot batches) */
     int reserved[6];       /* verification switches, result-identical to 0:
                               [0] bit 0: standalone ratio kernel instead of the
                                   fused epilogue;

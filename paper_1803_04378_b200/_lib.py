@@ -24,7 +24,7 @@ class Config(C.Structure):
     _fields_ = [("opt_tol", C.c_double), ("pivot_tol", C.c_double), ("feas_tol", C.c_double),
                 ("ratio_tie_tol", C.c_double), ("max_iter", C.c_long), ("anticycle", C.c_int),
                 ("kernel", C.c_int), ("workers", C.c_int), ("device", C.c_int),
-                ("batch", C.c_int), ("use_graphs", C.c_int), ("reserved", C.c_int * 6),
+                ("batch", C.c_int), ("reserved", C.c_int * 6),
                 ("world_size", C.c_int), ("rank", C.c_int), ("nccl_id", C.c_ubyte * 128),
                 ("peer", C.c_void_p), ("reinvert_every", C.c_long),
                 ("memory_budget", C.c_ulonglong)]

@@ -1805,7 +1805,6 @@ void lpsg_config_default(lpsg_config* cfg) {
     cfg->pivot_tol = 1e-9;
     cfg->feas_tol = 1e-7;
     cfg->ratio_tie_tol = 1e-9;
-    cfg->use_graphs = 1;
 }
 
 int lpsg_create(const lpsg_problem* lp, const lpsg_config* cfg, lpsg_solver** out) {

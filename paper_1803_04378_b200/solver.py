@@ -94,7 +94,6 @@ class SolverConfig:
     workers: int = 1         # accepted, ignored (solver.hpp:43)
     device: int = 0
     batch: int = 0
-    use_graphs: bool = True
     observer: Optional[Callable[["IterationView"], None]] = None
     observer_rows: bool = False  # view.row(i) readable in the observer (unfused, one pivot per round trip)
     # sharded solve over NCCL: one process per GPU, same problem
@@ -120,7 +119,7 @@ class SolverConfig:
         c.opt_tol, c.pivot_tol, c.feas_tol = self.opt_tol, self.pivot_tol, self.feas_tol
         c.ratio_tie_tol, c.max_iter = self.ratio_tie_tol, int(self.max_iter)
         c.anticycle, c.kernel, c.workers = int(self.anticycle), int(self.kernel), int(self.workers)
-        c.device, c.batch, c.use_graphs = int(self.device), int(self.batch), int(self.use_graphs)
+        c.device, c.batch = int(self.device), int(self.batch)
         c.reserved[0] = 1 if self.unfused_ratio else 0
         c.world_size, c.rank = int(self.world_size), int(self.rank)
         c.reserved[1] = 1 if self.nccl_single else 0
