@@ -169,12 +169,10 @@ struct Dev {
     long long ld_cm;       // column pitch of A_cm (even, 16-byte aligned columns)
     // launch geometry of the streaming kernels (configure_kernels)
     int upd_h, upd_C, upd_S, upd_U, upd_smem, upd_threads;
-    int upd_prod;              // h <= 32: update lanes form the FTRAN products (k_update stage holds a product tile)
     const CUtensorMap* tm_T;   // 2D TMA descriptor of T, box {h rows, C columns}
     const CUtensorMap* tm_nb;  // 2D TMA descriptors of A_nb, box {wbx slots, price_rows(wbx) rows}
     int price_nwc, price_S, price_smem, price_threads;
     int price_spt;             // slots per consumer thread: 1 (one chain per lane) or 2 (pairs)
-    int price_nwm;             // multiplier warps forming the pricing products (narrow ranges), else 0
     int dbg;               // perf-experiment knobs (cfg.reserved[2] minus bit 4); read only
                            // through LPSG_XP, i.e. only in a -DLPSG_EXPERIMENTS build
     int la_exact;          // lookahead theta' keeps the y_i == 0 select (cfg.reserved[2] bit 4):

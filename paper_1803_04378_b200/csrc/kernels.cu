@@ -377,13 +377,10 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
         const size_t stage_stride = (stage_el * 8 + 1023) / 1024 * 1024;
         uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * d.price_stage_bytes);
         uint64_t* empty = full + S;
-        uint64_t* prodb = empty + S;  // products formed (nwm multiplier warps; narrow ranges only)
-        const int nwm = d.price_nwm;
         if (threadIdx.x == 0) {
             for (int k = 0; k < S; ++k) {
                 mbar_init(&full[k], 1);
                 mbar_init(&empty[k], nwc);
-                mbar_init(&prodb[k], nwm > 0 ? nwm : 1);
             }
             mbar_fence_init();
         }
@@ -414,34 +411,6 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
                     if (++st == S) { st = 0; ph ^= 1; }
                 }
             }
-        } else if (warp > nwc && warp <= nwc + nwm) {
-            // multiplier warps (narrow ranges, where the chains bound the
-            // kernel): W_i * a_is for the whole stage, written over the tile,
-            // so the chain lanes run a pure LDS + DADD chain (one fp64
-            // instruction per row instead of two). Same product, same bits.
-            const int mw = warp - nwc - 1;
-            const int wbx = g.wbx;
-            const int pairs = R * w / 2;  // wbx is even: a pair never straddles a row
-            int st = 0;
-            uint32_t ph = 0;
-            for (int k = 0; k < nst; ++k) {
-                mbar_wait(&full[st], ph);
-                double* sb = reinterpret_cast<double*>(smem + (size_t)st * stage_stride);
-                const double* ws = sb + (size_t)R * w;
-                double2* t2 = reinterpret_cast<double2*>(sb);
-                for (int e = mw * 32 + lane; e < pairs; e += nwm * 32) {
-                    const int f = 2 * e;
-                    const int q = f / (wbx * R);
-                    const int rr = (f - q * wbx * R) / wbx;
-                    const double wi = ws[rr];
-                    const double2 v = t2[e];
-                    t2[e] = make_double2(dmul(wi, v.x), dmul(wi, v.y));
-                }
-                fence_proxy_async_smem();  // generic writes before the stage's next TMA fill
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&prodb[st]);
-                if (++st == S) { st = 0; ph ^= 1; }
-            }
         } else if (warp < nwc && d.price_spt == 1) {
             // one slot per consumer lane, the CTA's slots split evenly over the
             // nwc consumer warps: a warp then issues 2 fp64 instructions per row
@@ -458,23 +427,11 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
             int st = 0;
             uint32_t ph = 0;
             for (int k = 0; k < nst; ++k) {
-                mbar_wait(nwm > 0 ? &prodb[st] : &full[st], ph);
+                mbar_wait(&full[st], ph);
                 const int nr = min(R, m - k * R);
                 const double* sb = reinterpret_cast<const double*>(smem + (size_t)st * stage_stride);
                 const double* ws = sb + (size_t)R * w;
-                if (act && nwm > 0 && !LPSG_XP(d, 1)) {
-                    // the tile holds the products already: LDS + DADD per row
-                    const double* col = sb + q * wbx * R + tq;
-                    int rr = 0;
-                    for (; rr + kNG <= nr; rr += kNG) {
-                        double v[kNG];
-#pragma unroll
-                        for (int u = 0; u < kNG; ++u) v[u] = col[(rr + u) * wbx];
-#pragma unroll
-                        for (int u = 0; u < kNG; ++u) acc = dadd(acc, v[u]);
-                    }
-                    for (; rr < nr; ++rr) acc = dadd(acc, col[rr * wbx]);
-                } else if (act && !LPSG_XP(d, 1)) {
+                if (act && !LPSG_XP(d, 1)) {
                     // plain loads, scheduled by the compiler: 14-15 cycles a row,
                     // against 17-20 for volatile software-pipelined loads
                     // (tools/microbench/chain_rate.cu)
@@ -691,15 +648,10 @@ __device__ __forceinline__ void update_role(const Dev& d, unsigned char* smem, u
 // covers 32 / (h/2) columns per iteration (lane = column offset x row pair)
 // instead of leaving most lanes idle on one column. Same per-element
 // arithmetic as update_role.
-// With `prod` (small row blocks, update + FTRAN in the same pass) the update
-// lanes also form the FTRAN products T_new[i][j] * a_q[j] (the same DMUL the
-// FTRAN chain would issue) into the stage's product tile, so the FTRAN lanes
-// run a pure LDS + DADD chain: one fp64 instruction per column instead of two
-// on the latency-bound path.
 __device__ __forceinline__ void update_role_small(const Dev& d, unsigned char* smem, uint64_t* full,
                                                   uint64_t* upd, size_t stage_stride, size_t tile_el,
                                                   int nst, int S, int C, int h, int i0, int r, int U,
-                                                  bool up, bool prod, int warp, int lane) {
+                                                  bool up, int warp, int lane) {
     const int m = d.m, mloc = d.mloc;
     const int hp = h >> 1;                 // row pairs per column (h is even)
     const int cpw = 32 / hp;               // columns per warp iteration
@@ -724,8 +676,6 @@ __device__ __forceinline__ void update_role_small(const Dev& d, unsigned char* s
             const int j0 = k * C, nc = min(C, ncols - j0);
             double* tile = reinterpret_cast<double*>(smem + (size_t)st * stage_stride);
             const double* xs = tile + tile_el;
-            const double* as = xs + C;
-            double* pt = tile + tile_el + 2 * (size_t)C;  // product tile, same layout as the tile
             for (int jj = warp * cpw + lc; jj < nc; jj += step) {
                 double2* tp = reinterpret_cast<double2*>(tile + (size_t)jj * h) + lr;
                 double2 tv = *tp;
@@ -738,10 +688,6 @@ __device__ __forceinline__ void update_role_small(const Dev& d, unsigned char* s
                     tv.x = (naive || p0 != 0.0) ? s0v : tv.x;
                     tv.y = (naive || p1 != 0.0) ? s1v : tv.y;
                     *tp = tv;
-                }
-                if (prod) {
-                    const double aj = as[jj];
-                    *(reinterpret_cast<double2*>(pt + (size_t)jj * h) + lr) = make_double2(dmul(tv.x, aj), dmul(tv.y, aj));
                 }
                 if (!tstore) gbase[(size_t)(j0 + jj) * (ldT / 2)] = tv;
             }
@@ -891,9 +837,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
     const int nst = (ncols + C - 1) / C;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const size_t tile_el = (size_t)C * h;
-    const size_t stage_stride = ((tile_el * (d.upd_prod ? 2 : 1) + 2 * (size_t)C) * 8 + 1023) / 1024 * 1024;
-    // small row blocks: the update lanes form the FTRAN products (update_role_small)
-    const bool prod = d.upd_prod && up && ft && !LPSG_XP(d, 32);
+    const size_t stage_stride = ((tile_el + 2 * (size_t)C) * 8 + 1023) / 1024 * 1024;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * stage_stride);
     uint64_t* upd = full + S;
     uint64_t* empty = upd + S;
@@ -971,7 +915,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         // zeroed multiplier of tiled_engine.cpp:241.
         const int nit = (h + 63) >> 6;
         if (h <= 32 && !LPSG_XP(d, 32)) {  // experiment bit 5: the one-column-per-warp path (A/B)
-            update_role_small(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, prod, warp, lane);
+            update_role_small(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, warp, lane);
         } else switch (nit) {
             case 1: update_role<1>(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, warp, lane); break;
             case 2: update_role<2>(d, smem, full, upd, stage_stride, tile_el, nst, S, C, h, i0, r, U, up, warp, lane); break;
@@ -994,37 +938,23 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                 if (m - j0 < C) f_bbar = tile[(m - j0) * h + t];  // updated b_bar_i (column m)
                 const double* as = tile + tile_el + C;
                 const double* col = tile + t;
-                if (prod) {
-                    // the products were formed by the update lanes: a pure DADD chain
-                    const double* pc = tile + tile_el + 2 * (size_t)C + t;
-                    int jj = 0;
-                    for (; jj + kFG <= nf; jj += kFG) {
-                        double pv[kFG];
+                // plain loads, scheduled by the compiler (volatile software
+                // pipelining is slower for a single chain: chain_rate.cu)
+                int jj = 0;
+                for (; jj + kFG <= nf; jj += kFG) {
+                    double tv[kFG], av[kFG];
 #pragma unroll
-                        for (int u = 0; u < kFG; ++u) pv[u] = pc[(jj + u) * h];
+                    for (int u = 0; u < kFG; ++u) tv[u] = col[(jj + u) * h];
 #pragma unroll
-                        for (int u = 0; u < kFG; ++u) acc = dadd(acc, pv[u]);
+                    for (int u = 0; u < kFG; u += 2) {
+                        const double2 a2 = *reinterpret_cast<const double2*>(as + jj + u);
+                        av[u] = a2.x;
+                        av[u + 1] = a2.y;
                     }
-                    for (; jj < nf; ++jj) acc = dadd(acc, pc[jj * h]);
-                } else {
-                    // plain loads, scheduled by the compiler (volatile software
-                    // pipelining is slower for a single chain: chain_rate.cu)
-                    int jj = 0;
-                    for (; jj + kFG <= nf; jj += kFG) {
-                        double tv[kFG], av[kFG];
 #pragma unroll
-                        for (int u = 0; u < kFG; ++u) tv[u] = col[(jj + u) * h];
-#pragma unroll
-                        for (int u = 0; u < kFG; u += 2) {
-                            const double2 a2 = *reinterpret_cast<const double2*>(as + jj + u);
-                            av[u] = a2.x;
-                            av[u + 1] = a2.y;
-                        }
-#pragma unroll
-                        for (int u = 0; u < kFG; ++u) acc = dadd(acc, dmul(tv[u], av[u]));
-                    }
-                    for (; jj < nf; ++jj) acc = dadd(acc, dmul(col[jj * h], as[jj]));
+                    for (int u = 0; u < kFG; ++u) acc = dadd(acc, dmul(tv[u], av[u]));
                 }
+                for (; jj < nf; ++jj) acc = dadd(acc, dmul(col[jj * h], as[jj]));
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
@@ -2185,9 +2115,7 @@ void configure_kernels(Dev& d) {
     if (const char* e = xp_env("LPSG_UPD_COLS")) d.upd_C = std::max(2, atoi(e)) & ~1;  // tuning experiments
     d.upd_U = 8;
     const size_t tile_el = (size_t)d.upd_C * h;
-    // h <= 32 (the update_role_small shapes): a product tile per stage (see update_role_small)
-    d.upd_prod = (h <= 32 && xp_env("LPSG_NO_UPD_PROD") == nullptr) ? 1 : 0;
-    const size_t stage = ((tile_el * (d.upd_prod ? 2 : 1) + 2 * (size_t)d.upd_C) * 8 + 1023) / 1024 * 1024;
+    const size_t stage = ((tile_el + 2 * (size_t)d.upd_C) * 8 + 1023) / 1024 * 1024;
     size_t s_cap = 8;
     if (const char* e = xp_env("LPSG_UPD_STAGES")) s_cap = (size_t)std::max(2, atoi(e));  // tuning experiments
     // >= 3 stages: the storer keeps 2 TMA stores in flight behind the update warps
@@ -2209,11 +2137,7 @@ void configure_kernels(Dev& d) {
         d.price_spt = 2;
         d.price_nwc = (gm.w + 63) / 64;  // consumer threads own slot pairs
     }
-    // narrow ranges (<= 64 slots per CTA: C1, C2, C4, the per-GPU shape of a
-    // sharded C3 / C5) are chain-bound: multiplier warps form the products
-    // so the chains are pure DADD (k_price)
-    d.price_nwm = (d.price_spt == 1 && gm.w <= 64 && xp_env("LPSG_NO_PRICE_MUL") == nullptr) ? 4 : 0;
-    d.price_threads = (d.price_nwc + d.price_nwm + 1) * 32;
+    d.price_threads = (d.price_nwc + 1) * 32;
     d.price_stage_bytes = 0;
     for (int n = 1; n <= ncols_local; n = (n < 64 ? n + 1 : n + n / 64)) {
         const PriceGeom g = price_geom(n, G);
@@ -2226,7 +2150,7 @@ void configure_kernels(Dev& d) {
         d.price_stage_bytes = std::max(d.price_stage_bytes, st);
     }
     d.price_S = (int)std::max<size_t>(2, std::min<size_t>(6, (size_t)(192 * 1024) / d.price_stage_bytes));
-    d.price_smem = (int)(d.price_S * d.price_stage_bytes + 3 * d.price_S * 8);
+    d.price_smem = (int)(d.price_S * d.price_stage_bytes + 2 * d.price_S * 8);
     cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, d.upd_smem);
     cudaFuncSetAttribute(k_price, cudaFuncAttributeMaxDynamicSharedMemorySize, d.price_smem);
     cudaFuncSetAttribute(k_la_gemm_price, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaPriceSmem));
