@@ -38,9 +38,6 @@ namespace lpsg {
 
 constexpr int kLookaheadExactBit = 16;  // lpsg_config.reserved[2]: see Dev::la_exact
 
-// device-side experiment bit test (0 in the default build)
-#define xp_env_dev(d, bits) (LPSG_XP(d, bits) ? 1 : 0)
-
 inline const char* xp_env(const char* name) {
 #ifdef LPSG_EXPERIMENTS
     return getenv(name);

@@ -256,15 +256,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 __device__ __forceinline__ int even_up(int v) { return (v + 1) & ~1; }
-// LSU-path async copies (cp.async, 16 bytes, L2 only; src-size < 16 zero-fills)
-// and the mbarrier arrive that fires when the calling thread's earlier cp.async
-// copies have landed (noinc: the barrier's count includes these arrivals).
-__device__ __forceinline__ void cpa16(void* dst, const void* src, int bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(dst)), "l"(src), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void cpa_arrive(uint64_t* b) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(su32(b)) : "memory");
-}
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
                                             uint64_t* b) {
@@ -386,15 +377,9 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
         const size_t stage_stride = (stage_el * 8 + 1023) / 1024 * 1024;
         uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * d.price_stage_bytes);
         uint64_t* empty = full + S;
-        // Narrow ranges (<= 64 slots: rows of <= 512 bytes) fill the stages with
-        // cp.async from the whole producer warp instead of 2D TMA boxes: a TMA
-        // box streams row by row, ~16 GB/s per SM for 128-byte rows, which is
-        // what bounded the one-chain path at C2 and the per-GPU shape of a
-        // sharded C3 (~15 cycles/row), not the chains.
-        const bool lsu = g.w <= 64 && xp_env_dev(d, 64) == 0;
         if (threadIdx.x == 0) {
             for (int k = 0; k < S; ++k) {
-                mbar_init(&full[k], lsu ? 32 : 1);
+                mbar_init(&full[k], 1);
                 mbar_init(&empty[k], nwc);
             }
             mbar_fence_init();
@@ -402,28 +387,7 @@ __global__ void __launch_bounds__(384) k_price(Dev d) {
         __syncthreads();
         const int nst = (m + R - 1) / R;
         const CUtensorMap* map = d.tm_nb + (g.wbx / 8 - 1);
-        if (warp == nwc && lsu) {
-            const int hw = w / 2;  // 16-byte pairs per row (w % 8 == 0)
-            int st = 0;
-            uint32_t ph = 0;
-            for (int k = 0; k < nst; ++k) {
-                if (k >= S) mbar_wait(&empty[st], ph ^ 1);
-                const int i0 = k * R;
-                unsigned char* sb = smem + (size_t)st * stage_stride;
-                double* tile = reinterpret_cast<double*>(sb);
-                double* ws = tile + (size_t)R * w;
-                for (int e = lane; e < R * hw; e += 32) {
-                    const int rr = e / hw, sp = e - rr * hw;
-                    const int sl = 2 * sp, q = sl / g.wbx, tq = sl - q * g.wbx;
-                    const bool ok = i0 + rr < m;
-                    cpa16(tile + (size_t)q * g.wbx * R + (size_t)rr * g.wbx + tq,
-                          ok ? d.A_nb + (size_t)(i0 + rr) * d.ld_nb + s0 + sl : d.A_nb, ok ? 16 : 0);
-                }
-                for (int e = lane; e < R / 2; e += 32) cpa16(ws + 2 * e, d.top + i0 + 2 * e, 16);  // top is padded
-                cpa_arrive(&full[st]);
-                if (++st == S) { st = 0; ph ^= 1; }
-            }
-        } else if (warp == nwc) {
+        if (warp == nwc) {
             if (lane == 0) {
                 const uint64_t pol = l2_evict_first();
                 int st = 0;
