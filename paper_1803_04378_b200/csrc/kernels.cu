@@ -721,7 +721,7 @@ __device__ __forceinline__ void ratio_put(const Dev& d) {
 // m + 1 <= kPivotPF * blockDim.x). Same arithmetic and bookkeeping as k_pivot,
 // which it replaces on that path: one kernel boundary per pivot less.
 constexpr int kPivotPF = 4;
-__device__ void pivot_cta(const Dev& d, Ctl* c) {
+__device__ __forceinline__ void pivot_cta(const Dev& d, Ctl* c) {
     const int m = d.m;
     const int r = ((volatile int*)&c->r)[0], q = c->q, n_scan = c->n_scan;
     const size_t ldT = (size_t)d.ldT;

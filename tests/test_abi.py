@@ -62,6 +62,38 @@ def test_config_defaults_match_reference():
     assert c.max_iter == 0 and c.anticycle == 0
 
 
+def test_config_struct_layout_and_public_fields():
+    """The ctypes mirror of lpsg_config matches the C struct (every field at
+    the C offset: a mismatch would shift memory_budget / reinvert_every), and
+    the public Python config carries the reference's fields plus the opt-in
+    modes, not the perf-experiment knobs (those live only in the
+    -DLPSG_EXPERIMENTS build)."""
+    import dataclasses
+    import os
+    import subprocess
+    import tempfile
+    from paper_1803_04378_b200 import SolverConfig, _lib
+    names = {f.name for f in dataclasses.fields(SolverConfig)}
+    for must in ("opt_tol", "pivot_tol", "feas_tol", "ratio_tie_tol", "max_iter", "anticycle",
+                 "kernel", "workers", "observer", "observer_rows", "memory_budget", "reinvert_every"):
+        assert must in names
+    for gone in ("experiment", "debug_flags", "use_graphs"):
+        assert gone not in names
+    src = ('#include <stddef.h>\n#include <stdio.h>\n#include "lpsg.h"\n'
+           'int main(void){printf("%zu %zu %zu %zu\\n", sizeof(lpsg_config), '
+           'offsetof(lpsg_config, peer), offsetof(lpsg_config, reinvert_every), '
+           'offsetof(lpsg_config, memory_budget)); return 0;}\n')
+    with tempfile.TemporaryDirectory() as d:
+        with open(os.path.join(d, "t.c"), "w") as f:
+            f.write(src)
+        exe = os.path.join(d, "t")
+        subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), os.path.join(d, "t.c"), "-o", exe],
+                       check=True)
+        got = [int(v) for v in subprocess.run([exe], capture_output=True, text=True).stdout.split()]
+    C_ = _lib.Config
+    assert got == [C.sizeof(C_), C_.peer.offset, C_.reinvert_every.offset, C_.memory_budget.offset]
+
+
 def test_null_arguments_are_rejected():
     from paper_1803_04378_b200 import _lib
     lib = _lib.load()

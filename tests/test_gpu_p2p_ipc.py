@@ -71,3 +71,31 @@ def test_p2p_two_processes(name):
             assert np.array_equal(tr[f], ref[f]), (r, f)
         assert np.array_equal(tr["objective"].view(np.uint64), ref["objective"].view(np.uint64))
         assert np.array_equal(np.frombuffer(xb, np.float64).view(np.uint64), g.x.view(np.uint64))
+
+
+@pytest.mark.parametrize("name", ["gen_256x512_f2_s1", "gen_1000x2000_f0_s1_max_iter400"])
+def test_p2p_two_processes_larger(name):
+    """Tie-heavy (batched lookahead exchanged over P2P) and m = 1000 prefixes."""
+    test_p2p_two_processes(name)
+
+
+def test_bench_two_ranks_fills_the_exchange_report():
+    """`torchrun --nproc-per-node 2 bench.py --gpus 2` end to end (both ranks on
+    this one B200, LPSG_BENCH_SAME_DEVICE: time-sliced, so a smoke test of the
+    multi-rank bench path, not a number): the line reports n_gpus 2 and the
+    per-pivot exchange accounting (collectives, payload, device time)."""
+    import json
+    import subprocess
+    import sys
+    env = dict(os.environ, LPSG_BENCH_SAME_DEVICE="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "c2", "--steps", "10",
+           "--warmup", "3", "--e2e-max-iter", "30", "--no-reinversion"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    line = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["steps"] == 10
+    ex = line["exchange"]
+    assert ex["collectives_per_pivot"] > 0 and ex["payload_bytes_per_pivot_per_rank"] > 0
+    assert ex["us_per_pivot_incl_merge_kernels"] is not None
