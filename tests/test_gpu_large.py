@@ -95,6 +95,17 @@ def test_large_sharded(name, shards):
     _check(z, rep, tr, (name, shards))
 
 
+@pytest.mark.parametrize("name", [n for n in NAMES if n in ("c3_p200", "c4_p20", "c5_p10", "c2_full")])
+def test_large_sharded_p2p(name):
+    """The device-initiated P2P transport (peer stores + flags, exchanges fused
+    into the producing kernels) at BASELINE sizes: 2 shards sharing this GPU."""
+    P = _P()
+    z, lp = _load(name)
+    rep, tr = P.solve_sharded(lp, P.SolverConfig(max_iter=int(z["cfg_max_iter"])), shards=2,
+                              trace=True, p2p=True)
+    _check(z, rep, tr, (name, 2, "p2p"))
+
+
 @pytest.mark.skipif("not __import__('paper_1803_04378_b200').device_count() > 1",
                     reason="one GPU: the spread placement needs several devices")
 @pytest.mark.parametrize("name", [n for n in NAMES if n in ("c3_p200", "c4_p20", "c5_p10")])
