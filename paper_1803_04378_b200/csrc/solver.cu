@@ -222,10 +222,6 @@ private:
     std::vector<int> art_row_host_;
     int run_phase_any();
     void reinvert();
-    void lookahead_split(const LookaheadDev& la, int* nf_b, int G);
-    cudaStream_t st2_ = nullptr;  // the second lookahead half
-    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
-    int* nf_b_ = nullptr;
 
     // ---- Case 2: out-of-core tiling (tiled_engine.cpp:29-54, 165-184, 246-263)
     struct Part {
@@ -682,11 +678,6 @@ void Solver::release() {
         cudaEventDestroy(r.b);
     }
     if (pool_) cudaMemPoolDestroy(pool_);
-    if (st2_) cudaStreamDestroy(st2_);
-    if (ev_fork_) cudaEventDestroy(ev_fork_);
-    if (ev_join_) cudaEventDestroy(ev_join_);
-    st2_ = nullptr;
-    ev_fork_ = ev_join_ = nullptr;
     if (st_) cudaStreamDestroy(st_);
     d_ = Dev{};
     cost_buf_ = scratch_ = chain_ = b0_ = nullptr;
@@ -1153,15 +1144,14 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
         for (int p = 0; p < P; ++p)
             if (p != resident_) porder.push_back(p);
     }
-    la.nonfinite = talloc<int>(2, st_, pool_);  // [1]: the second half's flag (lookahead_split)
-    nf_b_ = la.nonfinite + 1;
+    la.nonfinite = talloc<int>(1, st_, pool_);
     CK(cudaMemsetAsync(la.X, 0, sizeof(double) * (size_t)kb * ldx, st_));
     if (dbg_trace_) fprintf(stderr, "[solver r%d] lookahead K=%d\n", rank_, K);
     temp_alloc_fence();
     for (int k0 = 0; k0 < K; k0 += kb) {
         la.K = std::min(kb, K - k0);
         CK(cudaMemcpyAsync(rows_d, rows.data() + k0, sizeof(int) * la.K, cudaMemcpyHostToDevice, st_));
-        CK(cudaMemsetAsync(la.nonfinite, 0, 2 * sizeof(int), st_));
+        CK(cudaMemsetAsync(la.nonfinite, 0, sizeof(int), st_));
         ev_chain_ = nullptr;  // the copy is not a kernel of the profile
         // fp64 flops of the batched work: pricing K x m x n_scan(shard) dot terms
         // (DMUL + DADD); theta K x mloc x m terms of (T_ij - y_i X_kj) a_j
@@ -1179,13 +1169,6 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
             L(K_OTHER, 0.0, [&] { launch_la_x(d_, la, st_); });
         }
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->sum_i64(reinterpret_cast<long long*>(la.X), (size_t)la.K * ldx, st_); });
-        if (!sharded_ && !tiled_ && !prof_ && la.K >= 256) {
-            // Two candidate halves on two streams: theta'(A) runs while the
-            // pricing GEMM of B does, so each GEMM's last partial wave is
-            // filled by the other's CTAs (each alone ends ~15 % idle: K x m
-            // outputs are 1.7-3.4 rounds of the GPU). Same kernels, same bits.
-            lookahead_split(la, nf_b_, G);
-        } else {
         L(K_LA_PRICE, kf * (double)hctl_->n_scan, [&] { launch_la_price(d_, la, st_); });
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.pm, la.pm_all, sizeof(PriceMsg) * la.K, st_); });
         L(K_OTHER, 0.0, [&] { launch_la_decide(d_, la, sharded_ ? la.pm_all : la.pm, G, st_); });
@@ -1206,7 +1189,6 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
             if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.tl, la.tl_all, sizeof(double) * la.K, st_); });
             L(K_OTHER, 0.0, [&] { launch_la_score(d_, la, sharded_ ? la.tl_all : la.tl, G, st_); });
         }
-        }
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(scores.data() + k0, la.score, sizeof(double) * la.K, cudaMemcpyDeviceToHost, st_));
         CK(cudaStreamSynchronize(st_));
@@ -1215,50 +1197,6 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
                     la.pm, la.pm_all, la.tl, la.tl_all, la.own_t, la.nonfinite};
     for (void* p : bufs)
         if (p) CK(cudaFreeAsync(p, st_));
-}
-
-// The single-GPU lookahead after k_la_x, as two candidate halves: A on the
-// solver stream, B on st2_ (forked after k_la_x, joined before the scores are
-// read). Every per-candidate array is a disjoint slice, and each half has its
-// own non-finite flag, so the halves never read each other's results.
-void Solver::lookahead_split(const LookaheadDev& la, int* nf_b, int G) {
-    if (!st2_) {
-        CK(cudaStreamCreateWithFlags(&st2_, cudaStreamNonBlocking));
-        CK(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
-    }
-    const int KA = (la.K / 2 + 63) / 64 * 64;  // whole 64-candidate tiles in A
-    LookaheadDev a = la, b = la;
-    a.K = KA;
-    b.K = la.K - KA;
-    b.rows += KA;
-    b.X += (size_t)KA * la.ldx;
-    b.Wp += (size_t)KA * la.ldx;
-    b.bz += KA;
-    b.bj += KA;
-    b.theta += KA;
-    b.score += KA;
-    b.part_z += (size_t)KA * la.nblk;
-    b.part_j += (size_t)KA * la.nblk;
-    b.part_t += (size_t)KA * la.nblk_t;
-    b.pm += KA;
-    b.tl += KA;
-    b.own_t += KA;
-    b.nonfinite = nf_b;
-    CK(cudaEventRecord(ev_fork_, st_));
-    CK(cudaStreamWaitEvent(st2_, ev_fork_, 0));
-    launch_la_price(d_, a, st_);
-    launch_la_decide(d_, a, a.pm, 1, st_);
-    launch_la_price(d_, b, st2_);
-    launch_la_decide(d_, b, b.pm, 1, st2_);
-    launch_la_theta(d_, a, st_);
-    launch_la_score(d_, a, a.tl, 1, st_);
-    launch_la_theta(d_, b, st2_);
-    launch_la_score(d_, b, b.tl, 1, st2_);
-    CK(cudaEventRecord(ev_join_, st2_));
-    CK(cudaStreamWaitEvent(st_, ev_join_, 0));
-    launches_total += 2 * 9;  // per half: la_price 4 kernels, decide 1, la_theta 3, score 1
-    (void)G;
 }
 
 // One phase, through the reinversion mode when it is on: the device budget
