@@ -111,9 +111,6 @@ struct Ctl {
     double found_red;
     int no_ratio;      // FTRAN without the fused ratio test (drive-out, step API)
     int x_owner;       // sharded: this shard owns the current pivot row (k_pivot_row)
-    unsigned int piv_seq;  // fused pivot: k_update's last CTA publishes its decision
-    int piv_next;          // fused pivot: next pivot-row chunk to claim
-    int piv_done;          // fused pivot: chunks completed
     unsigned long long work[4];  // launches that did their work: price, update, pivot (profiling)
 };
 

@@ -716,36 +716,25 @@ __device__ __forceinline__ void ratio_put(const Dev& d) {
     peer_signal(a);
 }
 
-// pivot_update (solver.cpp:240-254) fused into the tail of k_update (single
-// GPU, fused schedule): once k_update's last CTA has decided r it publishes
-// ctl.piv_seq; the other CTAs, spinning on it, and the last CTA itself claim
-// chunks of blockDim pivot-row elements (division, x, W, A_nb slot column)
-// from an atomic counter, and the CTA that completes the last chunk does
-// k_pivot's bookkeeping. Work is claimed dynamically, so a CTA that gives up
-// waiting (a bounded spin: another kernel may hold SMs) costs nothing but
-// time. Same arithmetic as k_pivot; one kernel boundary per pivot less.
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ void pivot_fused(const Dev& d, Ctl* c) {
+// pivot_update (solver.cpp:240-254) of row r = ctl.r, run by ONE CTA: the
+// tail of k_update once its last CTA has decided r (single GPU, no tie,
+// m + 1 <= kPivotPF * blockDim.x). Same arithmetic and bookkeeping as k_pivot,
+// which it replaces on that path: one kernel boundary per pivot less.
+constexpr int kPivotPF = 4;
+__device__ __forceinline__ void pivot_cta(const Dev& d, Ctl* c) {
     const int m = d.m;
-    const int r = __ldcg(&c->r), q = __ldcg(&c->q), n_scan = __ldcg(&c->n_scan);
+    const int r = ((volatile int*)&c->r)[0], q = c->q, n_scan = c->n_scan;
     const size_t ldT = (size_t)d.ldT;
     const double yr = __ldcg(d.Y + r);
     if (fabs(yr) <= d.pivot_tol) {
         if (threadIdx.x == 0) c->status = ST_PIVOT_ERR;
         return;
     }
-    const double dk = __ldcg(d.top + m + 1), ndk = -dk;
-    const int p_leave = __ldcg(d.basic + r);
-    const int s_q = q < d.n_total ? __ldcg(d.col2slot + q) : -1;
-    const int last_col = n_scan > 0 ? __ldcg(d.slot2col + n_scan - 1) : -1;
+    const double dk = ((volatile double*)d.top)[m + 1];
+    const double ndk = -dk;
+    const int p_leave = d.basic[r];
+    const int s_q = q < d.n_total ? d.col2slot[q] : -1;
+    const int last_col = n_scan > 0 ? d.slot2col[n_scan - 1] : -1;
     const bool p_local = p_leave < d.n_total && p_leave >= d.col0 && p_leave < d.col1;
     const bool q_local = s_q >= 0;
     int dst = -1, src_col = -1;
@@ -756,44 +745,41 @@ __device__ void pivot_fused(const Dev& d, Ctl* c) {
         dst = s_q;
         src_col = last_col;
     }
-    const double* __restrict__ src = d.A_cm + (size_t)(dst >= 0 ? src_col : 0) * d.ld_cm;
-    const int li = __ldcg(&c->log_len);
+    const double xl = ddiv(yr, yr);
+    const int li = c->log_len;
     LogEntry* const ent = d.log + li % d.log_cap;
-    const int nch = (m + 1 + blockDim.x - 1) / blockDim.x;
-    __shared__ int s_ch, s_fin;
-    if (threadIdx.x == 0) s_fin = 0;
-    for (;;) {
-        if (threadIdx.x == 0) s_ch = atomicAdd(&c->piv_next, 1);
-        __syncthreads();
-        const int ch = s_ch;
-        __syncthreads();
-        if (ch >= nch) break;
-        const int j = ch * blockDim.x + threadIdx.x;
-        if (j <= m) {
-            const double x = ddiv(__ldcg(d.T + (size_t)j * ldT + r), yr);
-            const double ai = (dst >= 0 && j < m) ? src[j] : 0.0;
-            const double t0 = d.top[j];
-            d.xrow[j] = x;
-            d.T[(size_t)j * ldT + r] = x;  // in place, like pr[j] /= y_rk (solver.cpp:246-247)
-            const double p = dmul(ndk, x);
-            const bool wr = d.naive || p != 0.0;
-            const double nt = wr ? dadd(t0, p) : t0;
-            if (wr) d.top[j] = nt;
-            if (j == m) ent->objective = nt;
-            if (dst >= 0 && j < m) d.A_nb[(size_t)j * d.ld_nb + dst] = ai;
-        }
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0 && atomicAdd(&c->piv_done, 1) == nch - 1) s_fin = 1;
+    // every load first (kPivotPF per thread, all in flight together), then the
+    // arithmetic and the stores: row r of T is m+1 strided elements, and a
+    // load-divide-store loop would serialise one memory round trip per element
+    double tv[kPivotPF], wv[kPivotPF], av[kPivotPF];
+    const double* __restrict__ src = d.A_cm + (size_t)(dst >= 0 ? src_col : 0) * d.ld_cm;
+#pragma unroll
+    for (int u = 0; u < kPivotPF; ++u) {
+        const int j = threadIdx.x + u * blockDim.x;
+        tv[u] = j <= m ? __ldcg(d.T + (size_t)j * ldT + r) : 0.0;
+        wv[u] = j <= m ? d.top[j] : 0.0;
+        av[u] = (dst >= 0 && j < m) ? src[j] : 0.0;
     }
-    __syncthreads();
-    if (!s_fin || threadIdx.x != 0) return;
-    // every chunk is done (and fenced): the bookkeeping of k_pivot's last CTA
-    __threadfence();
-    d.xrow[m + 1] = ddiv(yr, yr);
-    c->work[2] = __ldcg(&c->work[2]) + 1;
+#pragma unroll
+    for (int u = 0; u < kPivotPF; ++u) {
+        const int j = threadIdx.x + u * blockDim.x;
+        if (j > m) break;
+        const double x = ddiv(tv[u], yr);
+        d.xrow[j] = x;
+        d.T[(size_t)j * ldT + r] = x;  // in place, like pr[j] /= y_rk (solver.cpp:246-247)
+        const double p = dmul(ndk, x);
+        const bool wr = d.naive || p != 0.0;
+        const double nt = wr ? dadd(wv[u], p) : wv[u];
+        if (wr) d.top[j] = nt;
+        if (j == m) ent->objective = nt;
+        if (dst >= 0 && j < m) d.A_nb[(size_t)j * d.ld_nb + dst] = av[u];
+    }
+    __syncthreads();  // every read of the d slot and the slot maps precedes their rewrite
+    if (threadIdx.x != 0) return;
+    d.xrow[m + 1] = xl;
+    c->work[2] += 1;
     {
-        const double p = dmul(ndk, ddiv(yr, yr));
+        const double p = dmul(ndk, xl);
         if (d.naive || p != 0.0) d.top[m + 1] = dadd(dk, p);
     }
     int ns = n_scan;
@@ -811,10 +797,9 @@ __device__ void pivot_fused(const Dev& d, Ctl* c) {
     if (q < d.n_total) d.col2slot[q] = -1;
     c->n_scan = ns;
     d.basic[r] = q;
-    const long long it = __ldcg(&c->total_iter) + 1;
-    c->total_iter = it;
-    ent->iteration = it;
-    ent->phase = __ldcg(&c->phase);
+    c->total_iter += 1;
+    ent->iteration = c->total_iter;
+    ent->phase = c->phase;
     ent->row = r;
     ent->leaving = p_leave;
     ent->entering = q;
@@ -1030,27 +1015,7 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
             d.rc_theta[blockIdx.x] = s_theta;
         }
     }
-    // fused pivot: every CTA reads the publication counter before its ticket, so
-    // none can miss the last CTA's publication (pivot_fused)
-    const bool gfuse = d.fuse_pivot && do_ratio;
-    __shared__ unsigned s_seq;
-    __shared__ int s_fin_wait;
-    if (gfuse && threadIdx.x == 0) s_seq = ((volatile unsigned*)&c->piv_seq)[0];
-    if (!last_block(&c->ticket_update)) {
-        if (!gfuse) return;
-        if (threadIdx.x == 0) {
-            const long long t0 = clock64();
-            while (ld_acquire_u32(&c->piv_seq) == s_seq) {
-                if (clock64() - t0 > 400000) break;  // ~0.2 ms: leave the work to the CTAs still here
-                __nanosleep(64);
-            }
-            s_fin_wait = ld_acquire_u32(&c->piv_seq) != s_seq;
-        }
-        __syncthreads();
-        if (!s_fin_wait || ((volatile int*)&c->status)[0] != ST_RUNNING) return;
-        pivot_fused(d, c);
-        return;
-    }
+    if (!last_block(&c->ticket_update)) return;
     if (threadIdx.x == 0) {
         c->ticket_update = 0;
         if (up && !d.keep_pending) c->pending = 0;
@@ -1079,10 +1044,6 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
                 d.rmsg->theta = kInf;
             } else {
                 c->status = ST_UNBOUNDED;
-            }
-            if (gfuse) {
-                __threadfence();
-                st_release_u32(&c->piv_seq, s_seq + 1);  // wake the waiting CTAs: no pivot
             }
         }
         if (d.sharded && d.fused) ratio_put(d);
@@ -1160,15 +1121,9 @@ __global__ void __launch_bounds__(512) k_update(Dev d) {
         else
             c->status = ST_TIE;
     }
-    if (!gfuse) return;
-    if (threadIdx.x == 0) {
-        c->piv_next = 0;
-        c->piv_done = 0;
-        __threadfence();
-        st_release_u32(&c->piv_seq, s_seq + 1);  // r (or the tie) is decided
-    }
+    if (!d.fuse_pivot) return;
     __syncthreads();
-    if (((volatile int*)&c->status)[0] == ST_RUNNING) pivot_fused(d, c);
+    if (((volatile int*)&c->status)[0] == ST_RUNNING) pivot_cta(d, c);
 }
 
 // world > 1: global ratio test over the gathered shard messages
@@ -1421,27 +1376,27 @@ __global__ void __launch_bounds__(256) k_pivot_row(Dev d) {
 // logged objective is recomputed from T[m][r] by the bookkeeping thread with the
 // (the new T[0][m]) is written into the log entry by the thread that owns j = m,
 // so no CTA ever reads another CTA's store.
-// The body of pivot_update over the calling grid: k_pivot, or (single GPU,
-// fused schedule) every CTA of k_update once its last CTA has published r.
-// In the second case ctl, Y, T's row r and the d slot were written by other
-// CTAs of the same launch, so they are read past L1 (__ldcg / volatile).
-__device__ __forceinline__ void pivot_body(const Dev& d, Ctl* c) {
+__global__ void __launch_bounds__(256) k_pivot(Dev d) {
+    pdl_wait();
+    pdl_trigger();
+    Ctl* c = d.ctl;
+    if (c->status != ST_RUNNING) return;
     const int m = d.m;
-    const int r = __ldcg(&c->r), q = __ldcg(&c->q), n_scan = __ldcg(&c->n_scan);
+    const int r = c->r, q = c->q, n_scan = c->n_scan;
     const bool sharded = d.sharded != 0;
     const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
     const int gstride = gridDim.x * blockDim.x;
     const size_t ldT = (size_t)d.ldT;
     // independent loads, all in flight together
-    const double yr = sharded ? d.xbuf[m + 2] : __ldcg(d.Y + r);
-    const double dk = __ldcg(d.top + m + 1);
+    const double yr = sharded ? d.xbuf[m + 2] : d.Y[r];
+    const double dk = d.top[m + 1];
     const int p_leave = d.basic[r];
     const int s_q = q < d.n_total ? d.col2slot[q] : -1;  // artificials have no slot
     const int last_col = n_scan > 0 ? d.slot2col[n_scan - 1] : -1;
     const bool one = gtid <= m && gtid + gstride > m;  // this thread owns at most one j
     double tj = 0.0, topj = 0.0;
     if (one) {
-        tj = sharded ? d.xbuf[gtid] : __ldcg(d.T + (size_t)gtid * ldT + r);
+        tj = sharded ? d.xbuf[gtid] : d.T[(size_t)gtid * ldT + r];
         topj = d.top[gtid];
     }
     if (fabs(yr) <= d.pivot_tol) {
@@ -1472,7 +1427,7 @@ __device__ __forceinline__ void pivot_body(const Dev& d, Ctl* c) {
     const double xl = ddiv(yr, yr);
     double xj = 0.0;
     if (one) xj = sharded ? tj : ddiv(tj, yr);
-    const int li = __ldcg(&c->log_len);  // monotonic; the log is a ring the host drains
+    const int li = c->log_len;  // monotonic; the log is a ring the host drains
     LogEntry* const ent = d.log + li % d.log_cap;
     const bool last = last_block(&c->ticket_misc);
     if (one) {
@@ -1487,7 +1442,7 @@ __device__ __forceinline__ void pivot_body(const Dev& d, Ctl* c) {
         if (gtid == m) ent->objective = nt;
     } else {
         for (int j = gtid; j <= m; j += gstride) {
-            const double x = sharded ? d.xbuf[j] : ddiv(__ldcg(d.T + (size_t)j * ldT + r), yr);
+            const double x = sharded ? d.xbuf[j] : ddiv(d.T[(size_t)j * ldT + r], yr);
             if (!sharded) {
                 d.xrow[j] = x;
                 d.T[(size_t)j * ldT + r] = x;
@@ -1508,7 +1463,7 @@ __device__ __forceinline__ void pivot_body(const Dev& d, Ctl* c) {
     if (gtid == 0 && !sharded) d.xrow[m + 1] = xl;
     if (!last || threadIdx.x != 0) return;
     c->ticket_misc = 0;
-    c->work[2] = __ldcg(&c->work[2]) + 1;
+    c->work[2] += 1;
     {
         // the d slot (T[0][m+1]) is every CTA's multiplier source
         const double p = dmul(ndk, xl);
@@ -1529,10 +1484,9 @@ __device__ __forceinline__ void pivot_body(const Dev& d, Ctl* c) {
     if (q < d.n_total) d.col2slot[q] = -1;
     c->n_scan = ns;
     d.basic[r] = q;
-    const long long it = __ldcg(&c->total_iter) + 1;
-    c->total_iter = it;
-    ent->iteration = it;
-    ent->phase = __ldcg(&c->phase);
+    c->total_iter += 1;
+    ent->iteration = c->total_iter;
+    ent->phase = c->phase;
     ent->row = r;
     ent->leaving = p_leave;
     ent->entering = q;
@@ -1540,14 +1494,6 @@ __device__ __forceinline__ void pivot_body(const Dev& d, Ctl* c) {
     c->pending = 1;
     c->upd_r = r;
     c->upd_q = q;
-}
-
-__global__ void __launch_bounds__(256) k_pivot(Dev d) {
-    pdl_wait();
-    pdl_trigger();
-    Ctl* c = d.ctl;
-    if (c->status != ST_RUNNING) return;
-    pivot_body(d, c);
 }
 
 // --------------------------------------------------------- drive-out scan ---

@@ -936,9 +936,12 @@ std::vector<int> Solver::gather_overflow_candidates() {
 
 // run_phase (solver.cpp:278-293) in the fused schedule.
 int Solver::run_phase() {
-    // the pivot runs in k_update's tail (kernels.cu pivot_fused) on the single-
-    // GPU fused schedule; its CTAs must all be resident together (one per SM)
-    d_.fuse_pivot = (!sharded_ && !unfused_ratio_ && !tiled_ && d_.update_grid <= d_.num_sms &&
+    // the fused pivot needs the whole pivot row in one CTA's registers
+    // (kernels.cu pivot_cta: 4 elements per thread). It pays where the pivot
+    // is launch-bound (C1 m = 256: 38-40k -> 42.5k it/s); at C2 (m = 2000) the
+    // single-CTA tail cost more than the k_pivot launch it saved (17.1k ->
+    // 16.2k it/s with 16 elements per thread), so larger m keep k_pivot
+    d_.fuse_pivot = (!sharded_ && !unfused_ratio_ && !tiled_ && (long long)m_ + 1 <= 4LL * d_.upd_threads &&
                      xp_env("LPSG_NO_FUSED_PIVOT") == nullptr) ? 1 : 0;
     struct Unfuse {
         Dev& d;
