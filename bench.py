@@ -570,6 +570,15 @@ def run_ours(args, cfg):
                                           f"workers = 1 (here {used})"}
         if w1 is not None:
             line["cpu_baseline"]["workers_1"] = w1
+        if val:
+            # the reference's time to the same final status,
+            # extrapolated as its measured time per pivot x the pivots of the
+            # bit-identical GPU run (labelled as an extrapolation, not a run)
+            piv = tto["iterations_phase1"] + tto["iterations_phase2"]
+            line["cpu_baseline"]["extrapolated_time_to_status_s"] = {
+                "status": tto["status"], "pivots": piv, "seconds": piv / val,
+                "note": "extrapolated: measured CPU time per pivot x the GPU run's pivot count "
+                        "(the pivot sequence is bit-identical)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
