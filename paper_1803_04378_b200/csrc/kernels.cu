@@ -1577,16 +1577,18 @@ __global__ void k_la_wp(Dev d, LookaheadDev la) {
 }
 
 // ---- register-tiled batched lookahead (a SIMT "GEMM" with sequential sums) --
-// The K candidates share every A_nb / T element they read: a CTA of 256
-// threads computes a 64-candidate x 128-column tile of outputs, 8 x 4 per
-// thread (32 independent chains per thread), and streams 16-deep chunks of both
-// operands into shared memory through a 3-stage cp.async ring (no register
-// staging, one barrier per chunk). A chunk step issues 64 (pricing) / 128
-// (theta) fp64 instructions per 12 (16) shared loads, and <= 128 registers per
+// The K candidates share every A_nb / T element they read. Pricing
+// (k_la_gemm_price): a CTA of 256 threads computes a 64-candidate x 128-slot
+// tile of outputs, 8 x 4 per thread (32 independent chains per thread), and
+// streams 16-deep chunks of both operands into shared memory through a 3-stage
+// cp.async ring (no register staging, one barrier per chunk); a chunk step
+// issues 64 fp64 instructions per 12 shared loads, and <= 128 registers per
 // thread keep 16 warps per SM to hide the DMUL -> DADD dependency (ncu: with
 // 8 x 8 tiles, 8-12 warps, "wait" was the top stall at 78 % pipe activity).
-// Each output is still one chain in ascending reduction index, bit for bit the
-// reference's dot (solver.cpp:190-200, 203-210): DMUL + DADD, never DFMA.
+// theta' (k_la_gemm_theta, below) keeps round 1's 64 x 64 / 4 x 4 form, which
+// measured faster than both cp.async variants. Each output is one chain in
+// ascending reduction index, bit for bit the reference's dot (solver.cpp:
+// 190-200, 203-210): DMUL + DADD, never DFMA.
 constexpr int kLK = 64;    // candidates per CTA tile
 constexpr int kLN = 128;   // slots (pricing) / rows (theta) per CTA tile
 constexpr int kLC = 16;    // reduction chunk
