@@ -37,10 +37,10 @@ CONFIGS = {
                label="C2 random dense LP m=2000 n=4000 (generator verbatim, equality rows), seed 1"),
     "c3": dict(rows=8000, cols=16000, form=0, seed=1, cpu_pivots=60, w1_steps=20, reinv_every=10000,
                label="C3 random dense LP m=8000 n=16000 (generator verbatim, equality rows), seed 1"),
-    "c4": dict(rows=4000, cols=8000, form=2, seed=1, cpu_pivots=1, ref_max_steps=1,
+    "c4": dict(rows=4000, cols=8000, form=2, seed=1, cpu_pivots=1, ref_max_steps=1, reinv_every=5000,
                label="C4 degenerate LP m=4000 n=8000 (<= rows, maximize, half the rows a_i - a_i+1 "
                      "with b_i = 0), seed 1"),
-    "c5": dict(rows=24000, cols=48000, form=0, seed=1, cpu_pivots=5,
+    "c5": dict(rows=24000, cols=48000, form=0, seed=1, cpu_pivots=5, reinv_every=20000,
                label="C5 random dense LP m=24000 n=48000 (generator verbatim), seed 1"),
 }
 def _metric():
