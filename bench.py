@@ -2,18 +2,25 @@
 """Benchmark: simplex iterations/s on BASELINE.json's headline config.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
-                    [--e2e-max-iter N] [--no-cpu-baseline]
+                    [--e2e-max-iter N] [--no-cpu-baseline] [--no-reinversion] [--transport p2p|nccl]
 
 A "step" is one pivot of the dense revised simplex (one pass of the hot path:
-ratio test, pivot row, pricing, fused update + FTRAN) on a synthetic LP from
+pivot row, pricing, fused update + FTRAN + ratio test) on a synthetic LP from
 the reference's own generator (seed 1), resident in HBM. W warm-up pivots run
 first (untimed), then exactly K pivots are timed with CUDA events on the
-solver's stream. The working set (A: 1.0 GB, B^-1: 0.5 GB at m=8000) is far
-larger than the 126 MB L2, so no flush is needed between pivots.
+solver's stream (`value`), and through the public API with the host clock
+(`e2e`, the same window). The working set (A: 1.0 GB, B^-1: 0.5 GB at m=8000)
+is far larger than the 126 MB L2, so no flush is needed between pivots.
+
+The line also carries the time to the final status (parity mode, the
+reference's own outcome) and, opt-in, with periodic reinversion; the roofline
+of the dominant kernel; and the unmodified reference CPU solver timed on the
+same LP and pivot window (`cpu_baseline`).
 
 Prints ONE JSON line (rank 0). `--impl reference` times the reference's own
 CPU implementation (oracle/_ref, i.e. lps::two_phase_solve compiled from the
-unmodified reference sources) on the same LP with all host cores.
+unmodified reference sources) on the LP the reference itself generates (same
+SHA-256, printed in `config`), over the same pivot window, with all host cores.
 """
 from __future__ import annotations
 
