@@ -44,10 +44,10 @@ CONFIGS = {
                label="C2 random dense LP m=2000 n=4000 (generator verbatim, equality rows), seed 1"),
     "c3": dict(rows=8000, cols=16000, form=0, seed=1, cpu_pivots=60, w1_steps=20, reinv_every=10000,
                label="C3 random dense LP m=8000 n=16000 (generator verbatim, equality rows), seed 1"),
-    "c4": dict(rows=4000, cols=8000, form=2, seed=1, cpu_pivots=1, ref_max_steps=1, reinv_every=5000,
+    "c4": dict(rows=4000, cols=8000, form=2, seed=1, cpu_pivots=1, ref_max_steps=1,
                label="C4 degenerate LP m=4000 n=8000 (<= rows, maximize, half the rows a_i - a_i+1 "
                      "with b_i = 0), seed 1"),
-    "c5": dict(rows=24000, cols=48000, form=0, seed=1, cpu_pivots=5, reinv_every=20000,
+    "c5": dict(rows=24000, cols=48000, form=0, seed=1, cpu_pivots=5,
                label="C5 random dense LP m=24000 n=48000 (generator verbatim), seed 1"),
 }
 def _metric():
@@ -519,7 +519,8 @@ def run_ours(args, cfg):
         # the opt-in reinversion mode (include/lpsg.h reinvert_every): NOT the
         # reference's arithmetic, so it is reported beside the parity-mode
         # result, never as the headline; same API, host buffers, full solve
-        cfg3 = solver_config(P, args, world, rank, local, reinvert_every=cfg["reinv_every"])
+        cfg3 = solver_config(P, args, world, rank, local, reinvert_every=cfg["reinv_every"],
+                             max_iter=args.e2e_max_iter)
         t0 = time.perf_counter()
         s3 = P.SimplexSolver(lp, cfg3)
         rep3 = s3.solve()
