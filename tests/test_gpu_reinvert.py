@@ -112,3 +112,24 @@ def test_reinversion_c3_reaches_optimal():
     # |B X 1 - 1| after the last rebuild: the two m = 8000 GEMVs of the probe
     # alone round at ~1e-12 (m eps |B| |X 1|)
     assert st["residual_after"] < 1e-10, st
+
+
+def test_reinversion_with_observer_rows():
+    """The unfused one-pivot-per-round-trip schedule (observer_rows) takes the
+    same reinversion stops: SCSD1 still reaches the Netlib optimum, and the
+    view's row 0 objective equals the report at the end."""
+    P = _P()
+    g = Golden("netlib_scsd1")
+    A, b, c, ck = g.arrays()
+    lp = P.StandardFormLP(g.m, g.n_total, A, b, c, ck)
+    seen = []
+    cfg = P.SolverConfig(reinvert_every=100, observer=lambda v: seen.append(v.tableau_row(0)[g.m]),
+                         observer_rows=True)
+    with P.SimplexSolver(lp, cfg) as s:
+        rep = s.solve()
+        st = s.reinvert_stats()
+    assert rep.status == P.SolveStatus.optimal and st["rebuilds"] >= 2
+    z = float(g.z["objective_sign"]) * rep.objective + float(g.z["objective_constant"])
+    assert abs(z - 8.6666667) <= 1e-7, z
+    assert len(seen) == rep.iterations
+    _check_point(lp, rep)
