@@ -76,6 +76,21 @@ double now_s() {
 
 long long round_up(long long v, long long a) { return (v + a - 1) / a * a; }
 
+// Two timing events, destroyed on every exit (the throwing ones included).
+struct EventPair {
+    cudaEvent_t a = nullptr, b = nullptr;
+    EventPair() {
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+    }
+    ~EventPair() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+    EventPair(const EventPair&) = delete;
+    EventPair& operator=(const EventPair&) = delete;
+};
+
 // Owns one device allocation until released (staging buffers freed on throw).
 struct DevBuf {
     void* p = nullptr;
@@ -1235,9 +1250,8 @@ int Solver::run_phase_any() {
 void Solver::reinvert() {
     const int m = m_;
     const long long ld = round_up(m, 4);
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
+    const EventPair ev;
+    cudaEvent_t e0 = ev.a, e1 = ev.b;
     CK(cudaEventRecord(e0, st_));
     double* Bm = talloc<double>((size_t)ld * m, st_, pool_);
     double* R = talloc<double>((size_t)ld * m, st_, pool_);
@@ -1282,8 +1296,6 @@ void Solver::reinvert() {
     CK(cudaStreamSynchronize(st_));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, e0, e1));
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
     ++reinv_count;
     reinv_steps += steps;
     reinv_res_before = before;
@@ -1549,9 +1561,8 @@ void Solver::enter_phase2() {
 // benchmark uses this to time K pivots after W warm-up pivots); any other
 // outcome is final.
 void Solver::solve(lpsg_report* rep) {
-    cudaEvent_t e0, e1;
-    CK(cudaEventCreate(&e0));
-    CK(cudaEventCreate(&e1));
+    const EventPair ev;
+    cudaEvent_t e0 = ev.a, e1 = ev.b;
     CK(cudaEventRecord(e0, st_));
     const double t0 = now_s();
     int status = final_status_;
@@ -1583,8 +1594,6 @@ void Solver::solve(lpsg_report* rep) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, e0, e1));
         last_device_ms = ms;
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
     }
     final_status_ = status;
     solved_ = true;
