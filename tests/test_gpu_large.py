@@ -4,10 +4,11 @@ compiled reference (tests/golden/large/, made by tests/make_large_golden.py).
   c2_full  C2 m=2000 n=4000 solved to optimality: every pivot, bit for bit
   c3_p200  C3 m=8000 n=16000, first 200 pivots (the headline config)
   c3_full  C3 solved to the reference's final status (67 548 phase-1 pivots, Infeasible)
-  c4_p3    C4 m=4000 n=8000 degenerate, first 3 pivots: each is a ~1000-way ratio
-  c4_p20   tie resolved by the batched tabu lookahead (the reference needs ~3 min
-           per pivot on one core); first 20 pivots
-  c5_p10   C5 m=24000 n=48000, first 10 pivots
+  c4_p3    C4 m=4000 n=8000 degenerate, first 3 / 20 / 60 pivots: each is a
+  c4_p20   ~1000-way ratio tie resolved by the batched tabu lookahead (the
+  c4_p60   reference needs ~3 min per pivot on one core: 3.3 h for c4_p60)
+  c5_p10   C5 m=24000 n=48000, first 10 / 100 pivots
+  c5_p100
 
 each on one GPU and split over 2 / 4 / 8 shards (the 8-GPU deployment shape),
 
