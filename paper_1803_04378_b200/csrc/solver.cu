@@ -186,6 +186,7 @@ private:
     void snapshot();
     void note_pivot(const LogEntry& e);
     void enqueue_pivots(int n);
+    long long room_ = 0;  // pivots the device budget still allows (run_phase)
     void seq_pivot();
     void seq_price();
     void seq_update();
@@ -907,6 +908,10 @@ void Solver::seq_update() {
 // k_update's last CTA already ran pivot_update, so a pivot is k_price +
 // k_update; otherwise k_pivot (or the sharded pivot-row exchange) leads.
 void Solver::enqueue_pivots(int n) {
+    // never enqueue pivots past the budget: they would only run as no-op
+    // launches behind the stop (room_ is set by run_phase)
+    n = (int)std::min<long long>(n, room_);
+    room_ -= n;
     for (int k = 0; k < n; ++k) {
         if (unfused_ratio_) L(K_RATIO, bytes_of(K_RATIO), [&] { launch_ratio(d_, st_); });
         if (!d_.fuse_pivot) seq_pivot();
@@ -967,6 +972,7 @@ int Solver::run_phase() {
     hctl_->no_ftran = 0;
     hctl_->no_ratio = unfused_ratio_ ? 1 : 0;
     hctl_->phase = phase_;
+    room_ = std::max<long long>(0, hctl_->budget - hctl_->total_iter);
     push();
     seq_price();   // price(W_t), first pivot of the phase
     seq_update();  // standalone FTRAN (pending == 0) + ratio test
@@ -1015,6 +1021,8 @@ int Solver::run_phase() {
             seq_pivot();
             seq_price();
             seq_update();
+            // the device stopped at hctl_->total_iter; the resumed pivot is the next one
+            room_ = std::max<long long>(0, hctl_->budget - hctl_->total_iter - 1);
             continue;
         }
         return out;
