@@ -68,9 +68,12 @@ def _ncu_traffic(kernel: str):
     `ncu --set full` summary under profiles/ (tools/ncu_summary.py), or None."""
     import glob
     best = None
-    # a checkout gives every file the same mtime: the *_final_* summary wins
-    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")),
-                    key=lambda p: ("_final_" in os.path.basename(p), os.path.getmtime(p))):
+    # a checkout gives every file the same mtime: the latest round's summary
+    # (r02 > r01) wins, then a *_final_* one
+    def rank(p):
+        b = os.path.basename(p)
+        return (b[:3], "_final_" in b, os.path.getmtime(p))
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_summary.json")), key=rank):
         try:
             with open(p) as f:
                 cap = json.load(f).get("captures", {}).get(kernel)
