@@ -250,6 +250,7 @@ private:
     RatioMsg* part_msgs_ = nullptr;
     int* part_row0_ = nullptr;
     double* xbuf_own_ = nullptr;  // Case 2: the pivot-row buffer (sharded runs use the comm heap)
+    double* host_T_ = nullptr;    // Case 2: page-locked rows of [B^-1 | b_bar], partition p at row0 * (m+1)
     void plan_tiles(int m, int n);
     Dev part_dev(int p) const;
     int part_of_row(int i) const;
@@ -540,7 +541,10 @@ void Solver::init(const lpsg_problem& lp) {
         std::vector<int> r0;
         for (const Part& q : parts_) r0.push_back(q.row0);
         CK(cudaMemcpy(part_row0_, r0.data(), sizeof(int) * r0.size(), cudaMemcpyHostToDevice));
-        for (Part& q : parts_) CK(cudaMallocHost(&q.host, sizeof(double) * (size_t)q.rows * (m + 1)));
+        // one page-locked block for every partition (a tiny budget can mean
+        // thousands of partitions; one allocation each would be slow)
+        CK(cudaMallocHost(&host_T_, sizeof(double) * (size_t)m * (m + 1)));
+        for (Part& q : parts_) q.host = host_T_ + (size_t)q.row0 * (m + 1);
     }
     if (sharded_) {
         d_.xbuf = static_cast<double*>(comm_->sym_alloc(sizeof(double) * (m + 4)));
@@ -678,8 +682,8 @@ void Solver::release() {
                     chain_, b0_, art_row_, part_msgs_, part_row0_, xbuf_own_};
     for (void* p : bufs)
         if (p) cudaFree(p);
-    for (Part& q : parts_)
-        if (q.host) cudaFreeHost(q.host);
+    if (host_T_) cudaFreeHost(host_T_);
+    host_T_ = nullptr;
     parts_.clear();
     part_msgs_ = nullptr;
     part_row0_ = nullptr;
