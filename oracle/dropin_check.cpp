@@ -17,7 +17,12 @@
 // This is the reference-side integration shown in INTEGRATION.md, exercised
 // for real.
 //
-// usage: dropin_check ROWS COLS FORM SEED [rows] [steps=N]   (FORM 0 eq, 1 le+max, 2 degenerate)
+//   4. `parts=P`: both libraries under a memory budget of ~P row partitions
+//      (the reference's own Case 2, tiled_engine.cpp:29-54, against lpsg's),
+//      `naive`: both with KernelMode::naive.
+//
+// usage: dropin_check ROWS COLS FORM SEED [rows] [steps=N] [parts=P] [naive]
+//        (FORM 0 eq, 1 le+max, 2 degenerate)
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -67,16 +72,18 @@ std::vector<double> sample_rows(const View& v, int m) {
 
 int main(int argc, char** argv) {
     if (argc < 5) {
-        std::fprintf(stderr, "usage: %s ROWS COLS FORM SEED [rows] [steps=N]\n", argv[0]);
+        std::fprintf(stderr, "usage: %s ROWS COLS FORM SEED [rows] [steps=N] [parts=P] [naive]\n", argv[0]);
         return 2;
     }
     const int rows = std::atoi(argv[1]), cols = std::atoi(argv[2]), form = std::atoi(argv[3]);
     const unsigned long long seed = std::strtoull(argv[4], nullptr, 10);
-    bool with_rows = false;
-    int steps = 0;
+    bool with_rows = false, naive = false;
+    int steps = 0, parts = 0;
     for (int a = 5; a < argc; ++a) {
         if (std::strcmp(argv[a], "rows") == 0) with_rows = true;
+        if (std::strcmp(argv[a], "naive") == 0) naive = true;
         if (std::strncmp(argv[a], "steps=", 6) == 0) steps = std::atoi(argv[a] + 6);
+        if (std::strncmp(argv[a], "parts=", 6) == 0) parts = std::atoi(argv[a] + 6);
     }
     lps::GeneralLP g = lps::generate({rows, cols, lps::SparsityClass::dense, seed});
     if (form >= 1) {
@@ -92,8 +99,15 @@ int main(int argc, char** argv) {
     const int m = lp.m;
 
     // ---- 1 + 2: two_phase_solve with observers
+    // parts=P: a memory budget of ~P row partitions on BOTH sides, i.e. the
+    // reference's own Case 2 (tiled_engine.cpp:29-54) against lpsg's
+    const unsigned long long row_bytes = 8ULL * (unsigned long long)(m + 2);
+    const unsigned long long budget =
+        parts > 0 ? row_bytes * (unsigned long long)((m + 1 + parts - 1) / parts + 1) : 0ULL;
     std::vector<Piv> ref_tr, gpu_tr;
     lps::SolverConfig rc;
+    if (budget) rc.memory_budget = lps::MemoryBudget::of_bytes(budget);
+    if (naive) rc.kernel = lps::KernelMode::naive;
     rc.observer = [&](const lps::IterationView& v) {
         Piv p{v.iteration, v.phase, v.objective, std::vector<int>(v.basic.begin(), v.basic.end()), {}};
         if (with_rows) p.rows = sample_rows(v, m);
@@ -103,6 +117,8 @@ int main(int argc, char** argv) {
 
     lpsg::SolverConfig gc;
     gc.observer_rows = with_rows;
+    gc.memory_budget = budget;
+    if (naive) gc.kernel = lpsg::KernelMode::naive;
     gc.observer = [&](const lpsg::IterationView& v) {
         Piv p{v.iteration, v.phase, v.objective, std::vector<int>(v.basic.begin(), v.basic.end()), {}};
         if (with_rows) p.rows = sample_rows(v, m);
@@ -129,6 +145,7 @@ int main(int argc, char** argv) {
     expect(same_bits(q.objective, r.objective) || (q.objective != q.objective && r.objective != r.objective),
            "objective");
     expect(same_bits(q.x, r.x), "x");
+    expect(q.case_used == (r.case_used == lps::TileCase::tiled ? 1 : 0), "case_used");
 
     // ---- 3: the step API by hand
     int step_pivots = 0;
@@ -181,9 +198,10 @@ int main(int argc, char** argv) {
     }
 
     const bool ok = fails == 0;
-    std::printf("%s %dx%d form %d seed %llu%s: %zu pivots, status %d, objective %.17g (ref %.17g), "
+    std::printf("%s %dx%d form %d seed %llu%s%s%s: %zu pivots, status %d, objective %.17g (ref %.17g), "
                 "ref %.3f s, lpsg %.3f s, step-API pivots %d, lpsg device bytes %llu\n",
-                ok ? "PASS" : "FAIL", rows, cols, form, seed, with_rows ? " rows" : "", gpu_tr.size(),
+                ok ? "PASS" : "FAIL", rows, cols, form, seed, with_rows ? " rows" : "", naive ? " naive" : "",
+                q.case_used ? " tiled" : "", gpu_tr.size(),
                 int(q.status), q.objective, r.objective, r.total_seconds, q.total_seconds, step_pivots,
                 (unsigned long long)(q.memory.device_read_bytes + q.memory.device_write_bytes));
     return ok ? 0 : 1;

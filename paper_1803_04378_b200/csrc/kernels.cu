@@ -763,16 +763,17 @@ __device__ __forceinline__ void pivot_cta(const Dev& d, Ctl* c) {
 #pragma unroll
     for (int u = 0; u < kPivotPF; ++u) {
         const int j = threadIdx.x + u * blockDim.x;
-        if (j > m) break;
-        const double x = ddiv(tv[u], yr);
-        d.xrow[j] = x;
-        d.T[(size_t)j * ldT + r] = x;  // in place, like pr[j] /= y_rk (solver.cpp:246-247)
-        const double p = dmul(ndk, x);
-        const bool wr = d.naive || p != 0.0;
-        const double nt = wr ? dadd(wv[u], p) : wv[u];
-        if (wr) d.top[j] = nt;
-        if (j == m) ent->objective = nt;
-        if (dst >= 0 && j < m) d.A_nb[(size_t)j * d.ld_nb + dst] = av[u];
+        if (j <= m) {
+            const double x = ddiv(tv[u], yr);
+            d.xrow[j] = x;
+            d.T[(size_t)j * ldT + r] = x;  // in place, like pr[j] /= y_rk (solver.cpp:246-247)
+            const double p = dmul(ndk, x);
+            const bool wr = d.naive || p != 0.0;
+            const double nt = wr ? dadd(wv[u], p) : wv[u];
+            if (wr) d.top[j] = nt;
+            if (j == m) ent->objective = nt;
+            if (dst >= 0 && j < m) d.A_nb[(size_t)j * d.ld_nb + dst] = av[u];
+        }
     }
     __syncthreads();  // every read of the d slot and the slot maps precedes their rewrite
     if (threadIdx.x != 0) return;
