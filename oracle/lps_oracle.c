@@ -489,7 +489,7 @@ int lpo_solve(int m, int n_total, const double* A, const double* b, const double
     for (int i = 0; i < m; ++i)
         if (s->basic[i] < 0) ++n_art;
     s->n_work = n_total + n_art;
-    s->cols = (double*)calloc((size_t)s->n_work * m, sizeof(double));
+    s->cols = (double*)calloc((size_t)(unsigned)s->n_work * (size_t)(unsigned)m, sizeof(double));
     for (int j = 0; j < n_total; ++j)
         for (int i = 0; i < m; ++i) s->cols[(size_t)j * m + i] = A[(size_t)i * n_total + j];
     s->c_true = (double*)calloc((size_t)s->n_work, sizeof(double));
