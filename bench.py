@@ -42,7 +42,7 @@ CONFIGS = {
                label="C1 random dense LP m=256 n=512 (<= rows, maximize; slack start), seed 1"),
     "c2": dict(rows=2000, cols=4000, form=0, seed=1, cpu_pivots=300, w1_steps=100, reinv_every=2000,
                label="C2 random dense LP m=2000 n=4000 (generator verbatim, equality rows), seed 1"),
-    "c3": dict(rows=8000, cols=16000, form=0, seed=1, cpu_pivots=60, w1_steps=20, reinv_every=10000,
+    "c3": dict(rows=8000, cols=16000, form=0, seed=1, cpu_pivots=60, w1_steps=20, reinv_every=50000,
                label="C3 random dense LP m=8000 n=16000 (generator verbatim, equality rows), seed 1"),
     "c4": dict(rows=4000, cols=8000, form=2, seed=1, cpu_pivots=1, ref_max_steps=1,
                label="C4 degenerate LP m=4000 n=8000 (<= rows, maximize, half the rows a_i - a_i+1 "
