@@ -273,9 +273,9 @@ void launch_drive_red(const Dev& d, cudaStream_t st);
 // lookahead phases; world > 1 exchanges between them (solver.cu)
 double fp64_probe_tflops(cudaStream_t st);  // k_fp64_probe, best of 5
 void launch_la_x(const Dev& d, LookaheadDev& la, cudaStream_t st);
-void launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st);
+bool launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st);  // false: TMA descriptor encode failed
 void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int nsrc, cudaStream_t st);
-void launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st);
+bool launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st);
 void launch_la_score(const Dev& d, LookaheadDev& la, const double* tl, int nsrc, cudaStream_t st);
 // in-process shard exchange helpers (LocalComm): out[k] = sum_g in[g*n + k] / min_g
 void launch_sum_i64(const long long* in, int nsrc, size_t n, long long* out, cudaStream_t st);

@@ -1580,44 +1580,39 @@ __global__ void k_la_wp(Dev d, LookaheadDev la) {
 // ---- register-tiled batched lookahead (a SIMT "GEMM" with sequential sums) --
 // The K candidates share every A_nb / T element they read. Pricing
 // (k_la_gemm_price): a CTA of 256 threads computes a 64-candidate x 128-slot
-// tile of outputs, 8 x 4 per thread (32 independent chains per thread), and
-// streams 16-deep chunks of both operands into shared memory through a 3-stage
-// cp.async ring (no register staging, one barrier per chunk); a chunk step
-// issues 64 fp64 instructions per 12 shared loads, and <= 128 registers per
-// thread keep 16 warps per SM to hide the DMUL -> DADD dependency (ncu: with
-// 8 x 8 tiles, 8-12 warps, "wait" was the top stall at 78 % pipe activity).
-// theta' (k_la_gemm_theta, below) keeps round 1's 64 x 64 / 4 x 4 form, which
-// measured faster than both cp.async variants. Each output is one chain in
+// tile of outputs, 8 x 4 per thread (32 independent chains per thread); theta'
+// (k_la_gemm_theta): 64 candidates x 64 rows, 4 x 4 per thread. Both stream
+// 16-deep chunks of their operands into a 3-stage shared-memory ring with 2D
+// TMA tensor copies issued by one thread (a full mbarrier per stage carries
+// the bytes; the chunk barrier frees the stage two chunks ahead), so no thread
+// spends issue slots on loads: on the C4 shape the per-thread cp.async form of
+// the same loop ran at 0.80 of the fp64 peak, the TMA form at 0.92, the loop
+// with no loads at all at 0.95 (tools/microbench/la_price_rate.cu). The
+// candidate-side operands land as [64 k][16 i] boxes and are read two chunk
+// rows at a time (LDS.128 broadcasts). <= 128 registers per thread keep 16
+// warps per SM to hide the DMUL -> DADD dependency. Each output is one chain in
 // ascending reduction index, bit for bit the reference's dot (solver.cpp:
 // 190-200, 203-210): DMUL + DADD, never DFMA.
 constexpr int kLK = 64;    // candidates per CTA tile
-constexpr int kLN = 128;   // slots (pricing) / rows (theta) per CTA tile
+constexpr int kLN = 128;   // slots per pricing tile
 constexpr int kLC = 16;    // reduction chunk
-constexpr int kLS = 3;     // cp.async stages
-constexpr int kLThreads = 256;  // 8 x 4 outputs per thread, 2 CTAs (16 warps) per SM
-
-__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool ok) {
-    // src-size 0 zero-fills the destination (out-of-range elements)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(su32(dst)), "l"(src), "r"(ok ? 8 : 0)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, int bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(su32(dst)), "l"(src), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+constexpr int kLS = 3;     // ring stages
+constexpr int kLThreads = 256;
 
 struct LaPriceSmem {
-    double W[kLS][kLC][kLK];   // [i][k]
-    double A[kLS][kLC][kLN];   // [i][s]
+    double W[kLS][kLK][kLC];   // [k][i]  W'_k, i = chunk row
+    double A[kLS][kLC][kLN];   // [i][s]  A_nb slots
+    uint64_t full[kLS];
 };
 
 // z_k(s) = dot(W'_k, a_s) - c_j over this shard's slots (j = slot2col[s] != q):
 // the best (z, j) of the tile's 128 slots per candidate -> part_z/part_j[k][bx].
-__global__ void __launch_bounds__(kLThreads, 2) k_la_gemm_price(Dev d, LookaheadDev la) {
-    extern __shared__ __align__(16) unsigned char la_smem[];
+// tmW: W' as {m, K} with box {16, 64}; tmA: A_nb as {ld_nb, m} with box
+// {128, 16} (slots past n_scan hold stale values whose outputs are discarded).
+__global__ void __launch_bounds__(kLThreads, 2)
+k_la_gemm_price(Dev d, LookaheadDev la, const __grid_constant__ CUtensorMap tmW,
+                const __grid_constant__ CUtensorMap tmA) {
+    extern __shared__ __align__(128) unsigned char la_smem[];
     LaPriceSmem& sm = *reinterpret_cast<LaPriceSmem*>(la_smem);
     const int n_scan = d.ctl->n_scan;
     const double* cost = phase_cost(d, d.ctl->phase);
@@ -1625,68 +1620,69 @@ __global__ void __launch_bounds__(kLThreads, 2) k_la_gemm_price(Dev d, Lookahead
     // warp = one group of 8 candidates tk * 8 + u; lanes = 32 consecutive slots ts + 32 v
     const int t = threadIdx.x, tk = t >> 5, ts = t & 31;
     const int m = d.m;
+    if (t == 0) {
+        for (int s = 0; s < kLS; ++s) mbar_init(&sm.full[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
     double acc[8][4];
 #pragma unroll
     for (int u = 0; u < 8; ++u)
 #pragma unroll
         for (int v = 0; v < 4; ++v) acc[u][v] = 0.0;
-    // chunk loads: W 16 x 64 as 8-byte copies (candidate-fast: conflict-free
-    // stores, L1 reuse of each candidate's 32-byte sectors); A_nb 16 x 128 as
-    // 16-byte copies along the slot rows
+    constexpr uint32_t kBytes = (kLK * kLC + kLC * kLN) * 8;
     auto issue = [&](int stage, int i0) {
-#pragma unroll
-        for (int q = 0; q < kLC * kLK / kLThreads; ++q) {
-            const int e = t + kLThreads * q;
-            const int kk = e % kLK, ii = e / kLK;
-            const int k = k0 + kk, i = i0 + ii;
-            const bool ok = k < la.K && i < m;
-            cp_async8(&sm.W[stage][ii][kk], ok ? la.Wp + (size_t)k * la.ldx + i : la.Wp, ok);
-        }
-#pragma unroll
-        for (int q = 0; q < kLC * kLN / (2 * kLThreads); ++q) {
-            const int e = t + kLThreads * q;
-            const int sp = e % (kLN / 2), ii = e / (kLN / 2);
-            const int sl = s0 + 2 * sp, i = i0 + ii;
-            const int nb = (i < m) ? 8 * max(0, min(2, n_scan - sl)) : 0;
-            cp_async16(&sm.A[stage][ii][2 * sp], nb ? d.A_nb + (size_t)i * d.ld_nb + sl : d.A_nb, nb);
-        }
+        mbar_expect_tx(&sm.full[stage], kBytes);
+        tma_load_2d(&sm.W[stage][0][0], &tmW, i0, k0, &sm.full[stage]);
+        tma_load_2d(&sm.A[stage][0][0], &tmA, s0, i0, &sm.full[stage]);
     };
     const int nch = (m + kLC - 1) / kLC;
-#pragma unroll
-    for (int st = 0; st < kLS - 1; ++st) {
-        if (st < nch) issue(st, st * kLC);
-        cp_async_commit();
-    }
+    if (t == 0)
+        for (int st = 0; st < kLS - 1 && st < nch; ++st) issue(st, st * kLC);
     for (int ch = 0; ch < nch; ++ch) {
-        cp_async_wait<kLS - 2>();
-        __syncthreads();  // chunk ch landed for every thread; stage (ch-1) % S is free
-        if (ch + kLS - 1 < nch) issue((ch + kLS - 1) % kLS, (ch + kLS - 1) * kLC);
-        cp_async_commit();
+        __syncthreads();  // every thread is done with chunk ch - 1: its stage takes chunk ch + 2
+        if (t == 0 && ch + kLS - 1 < nch) issue((ch + kLS - 1) % kLS, (ch + kLS - 1) * kLC);
         const int stg = ch % kLS;
+        mbar_wait(&sm.full[stg], (uint32_t)(ch / kLS) & 1u);
         const int lim = min(kLC, m - ch * kLC);
-        auto step = [&](int ii) {
-            double w[8], a[4];
-#pragma unroll
-            for (int u = 0; u < 8; u += 2) {  // candidates tk*8 .. tk*8+7: 4 broadcast LDS.128
-                const double2 v2 = *reinterpret_cast<const double2*>(&sm.W[stg][ii][tk * 8 + u]);
-                w[u] = v2.x;
-                w[u + 1] = v2.y;
-            }
-#pragma unroll
-            for (int v = 0; v < 4; ++v) a[v] = sm.A[stg][ii][ts + 32 * v];
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) acc[u][v] = dadd(acc[u][v], dmul(w[u], a[v]));
-        };
         if (lim == kLC) {
 #pragma unroll
-            for (int ii = 0; ii < kLC; ++ii) step(ii);
+            for (int ii = 0; ii < kLC; ii += 2) {
+                double w0[8], w1[8], a0[4], a1[4];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {  // broadcast: the warp shares its 8 candidates
+                    const double2 v2 = *reinterpret_cast<const double2*>(&sm.W[stg][tk * 8 + u][ii]);
+                    w0[u] = v2.x;
+                    w1[u] = v2.y;
+                }
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    a0[v] = sm.A[stg][ii][ts + 32 * v];
+                    a1[v] = sm.A[stg][ii + 1][ts + 32 * v];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[u][v] = dadd(acc[u][v], dmul(w0[u], a0[v]));
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[u][v] = dadd(acc[u][v], dmul(w1[u], a1[v]));
+            }
         } else {
-            for (int ii = 0; ii < lim; ++ii) step(ii);
+            for (int ii = 0; ii < lim; ++ii) {
+                double w[8], a[4];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) w[u] = sm.W[stg][tk * 8 + u][ii];
+#pragma unroll
+                for (int v = 0; v < 4; ++v) a[v] = sm.A[stg][ii][ts + 32 * v];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) acc[u][v] = dadd(acc[u][v], dmul(w[u], a[v]));
+            }
         }
     }
-    cp_async_wait<0>();
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
         double bz = -kInf;
@@ -1840,29 +1836,51 @@ __global__ void __launch_bounds__(kDT) k_la_own(Dev d, LookaheadDev la) {
 
 constexpr int kLT = 64;  // theta tile edge
 
+struct LaThetaSmem {
+    double T[kLS][kLC][kLT];  // [j][i]  T_ij of the tile's 64 rows
+    double X[kLS][kLT][kLC];  // [k][j]  X_kj
+    double B[kLS][kLT][kLC];  // [k][j]  a_{b_k}[j] (gathered by k_la_gather)
+    uint64_t full[kLS];
+    int bj[kLT], rk[kLT];
+};
+
+// Bg[k][j] = a_{b_k}[j] (j < m), zero rows for candidates without an entering
+// column: the theta' GEMM's third operand as one strided matrix that a TMA box
+// can stream (it reuses W', which pricing no longer needs).
+__global__ void k_la_gather(Dev d, LookaheadDev la) {
+    const int k = blockIdx.y;
+    const int b = la.bj[k];
+    double* out = la.Wp + (size_t)k * la.ldx;
+    const double* a = b >= 0 ? d.A_cm + (size_t)b * d.ld_cm : nullptr;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < d.m; j += gridDim.x * blockDim.x)
+        out[j] = a ? a[j] : 0.0;
+}
+
 // y'_ik = sum_j t_ij(k) a_{b_k}[j] for this shard's rows, t = X_kj on the
 // candidate's own row, T_ij where y_i == 0, else T_ij - y_i X_kj (solver.cpp:
 // 177-184, 203-210); theta'_k partial (min ratio) per 64-row tile -> part_t[k][bx].
-// 64 x 64 tiles, 4 x 4 outputs per thread over 256 threads, register-staged
-// 16-deep chunks: at C4 this measured 13.6 TFLOP/s against 11.4-12.1 for 8 x 4
-// / 8 x 8 tiles fed by a cp.async ring (those have half the CTAs per round, so
-// a larger wave tail, and more long-scoreboard stalls; profiles/r02_c4_*).
-__global__ void __launch_bounds__(256, 2) k_la_gemm_theta(Dev d, LookaheadDev la) {
-    __shared__ double Ts[kLC][kLT];      // [j][i]
-    __shared__ double Xs[kLC][kLT + 1];  // [j][k]
-    __shared__ double Bs[kLC][kLT + 1];  // [j][k]  a_{b_k}[j]
-    __shared__ int s_bj[kLT], s_rk[kLT];
+// 64 x 64 tiles, 4 x 4 outputs per thread over 256 threads. tmT: T as
+// {mloc, m} with box {64, 16}; tmX / tmB: X and Bg as {m, K} with box {16, 64}.
+__global__ void __launch_bounds__(256, 2)
+k_la_gemm_theta(Dev d, LookaheadDev la, const __grid_constant__ CUtensorMap tmT,
+                const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmB) {
+    extern __shared__ __align__(128) unsigned char la_smem[];
+    LaThetaSmem& sm = *reinterpret_cast<LaThetaSmem*>(la_smem);
     const int m = d.m;
     const int i0 = blockIdx.x * kLT, k0 = blockIdx.y * kLT;
     const int t = threadIdx.x, ti = t & 15, tk = t >> 4;
     if (t < kLT) {
         const int k = k0 + t;
-        s_bj[t] = k < la.K ? la.bj[k] : -1;
-        s_rk[t] = k < la.K ? la.rows[k] : -1;
+        sm.bj[t] = k < la.K ? la.bj[k] : -1;
+        sm.rk[t] = k < la.K ? la.rows[k] : -1;
+    }
+    if (t == 0) {
+        for (int s = 0; s < kLS; ++s) mbar_init(&sm.full[s], 1);
+        mbar_fence_init();
     }
     __syncthreads();
     bool any = false;
-    for (int kk = 0; kk < kLT; ++kk) any |= s_bj[kk] >= 0;
+    for (int kk = 0; kk < kLT; ++kk) any |= sm.bj[kk] >= 0;
     if (!any) {  // no candidate of this tile has an entering column: score 0
         if (ti == 0)
             for (int v = 0; v < 4; ++v) {
@@ -1895,74 +1913,82 @@ __global__ void __launch_bounds__(256, 2) k_la_gemm_theta(Dev d, LookaheadDev la
     // some X_kj is inf/NaN: keep the select (la_exact forces it: a parity check
     // of that path, tests/test_gpu_parity.py)
     const bool exact = *la.nonfinite != 0 || d.la_exact != 0;
-    double rt[4], rx[4], rb[4];
-    auto fetch = [&](int j0) {
+    constexpr uint32_t kBytes = (kLC * kLT + 2 * kLT * kLC) * 8;
+    auto issue = [&](int stage, int j0) {
+        mbar_expect_tx(&sm.full[stage], kBytes);
+        tma_load_2d(&sm.T[stage][0][0], &tmT, i0, j0, &sm.full[stage]);
+        tma_load_2d(&sm.X[stage][0][0], &tmX, j0, k0, &sm.full[stage]);
+        tma_load_2d(&sm.B[stage][0][0], &tmB, j0, k0, &sm.full[stage]);
+    };
+    const int nch = (m + kLC - 1) / kLC;
+    if (t == 0)
+        for (int st = 0; st < kLS - 1 && st < nch; ++st) issue(st, st * kLC);
+    // exact: rows with y_i == 0 take T_ij itself (a select per element).
+    // fast: T_ij - y_i X_kj for every row. With y_i = +-0 and X_kj finite
+    // that differs from T_ij only in the sign of a zero, and a zero term
+    // never changes the chain (acc starts at +0.0 and round-to-nearest
+    // never produces -0.0 from it), so the chains are bit-identical.
+    auto step = [&](const double (&tv)[4], const double (&xv)[4], const double (&bv)[4], auto sel) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int e = t + 256 * q;
-            const int ii = e % kLT, jj = e / kLT;
-            const int li = i0 + ii, j = j0 + jj;
-            rt[q] = (li < d.mloc && j < m) ? d.T[(size_t)j * d.ldT + li] : 0.0;
-            const int jx = e % kLC, kk = e / kLC;
-            const int k = k0 + kk, j2 = j0 + jx;
-            const bool okk = k < la.K && j2 < m;
-            rx[q] = okk ? la.X[(size_t)k * la.ldx + j2] : 0.0;
-            rb[q] = (okk && s_bj[kk] >= 0) ? d.A_cm[(size_t)s_bj[kk] * d.ld_cm + j2] : 0.0;
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const double sub = dsub(tv[u], dmul(yv[u], xv[v]));
+                acc[u][v] = dadd(acc[u][v], dmul(decltype(sel)::value && zrow[u] ? tv[u] : sub, bv[v]));
+            }
+    };
+    auto run = [&](int stg, int lim, auto sel) {
+        if (lim == kLC) {
+#pragma unroll
+            for (int jj = 0; jj < kLC; jj += 2) {
+                double t0[4], t1[4], x0[4], x1[4], b0[4], b1[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    t0[u] = sm.T[stg][jj][ti + 16 * u];
+                    t1[u] = sm.T[stg][jj + 1][ti + 16 * u];
+                    const double2 xx = *reinterpret_cast<const double2*>(&sm.X[stg][tk + 16 * u][jj]);
+                    const double2 bb = *reinterpret_cast<const double2*>(&sm.B[stg][tk + 16 * u][jj]);
+                    x0[u] = xx.x;
+                    x1[u] = xx.y;
+                    b0[u] = bb.x;
+                    b1[u] = bb.y;
+                }
+                step(t0, x0, b0, sel);
+                step(t1, x1, b1, sel);
+            }
+        } else {
+            for (int jj = 0; jj < lim; ++jj) {
+                double tv[4], xv[4], bv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    tv[u] = sm.T[stg][jj][ti + 16 * u];
+                    xv[u] = sm.X[stg][tk + 16 * u][jj];
+                    bv[u] = sm.B[stg][tk + 16 * u][jj];
+                }
+                step(tv, xv, bv, sel);
+            }
         }
     };
-    fetch(0);
-    for (int j0 = 0; j0 < m; j0 += kLC) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int e = t + 256 * q;
-            Ts[e / kLT][e % kLT] = rt[q];
-            Xs[e % kLC][e / kLC] = rx[q];
-            Bs[e % kLC][e / kLC] = rb[q];
-        }
-        __syncthreads();
-        if (j0 + kLC < m) fetch(j0 + kLC);
-        // exact: rows with y_i == 0 take T_ij itself (a select per element).
-        // fast: T_ij - y_i X_kj for every row. With y_i = +-0 and X_kj finite
-        // that differs from T_ij only in the sign of a zero, and a zero term
-        // never changes the chain (acc starts at +0.0 and round-to-nearest
-        // never produces -0.0 from it), so the chains are bit-identical.
-        auto step = [&](int jj, auto sel) {
-            double tv[4], xv[4], bv[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                tv[u] = Ts[jj][ti + 16 * u];
-                xv[u] = Xs[jj][tk + 16 * u];
-                bv[u] = Bs[jj][tk + 16 * u];
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    const double sub = dsub(tv[u], dmul(yv[u], xv[v]));
-                    acc[u][v] = dadd(acc[u][v], dmul(decltype(sel)::value && zrow[u] ? tv[u] : sub, bv[v]));
-                }
-        };
-        if (exact) {
-            for (int jj = 0; jj < min(kLC, m - j0); ++jj) step(jj, std::true_type{});
-        } else if (j0 + kLC <= m) {
-#pragma unroll
-            for (int jj = 0; jj < kLC; ++jj) step(jj, std::false_type{});
-        } else {
-            for (int jj = 0; jj < m - j0; ++jj) step(jj, std::false_type{});
-        }
-        __syncthreads();
+    for (int ch = 0; ch < nch; ++ch) {
+        __syncthreads();  // every thread is done with chunk ch - 1: its stage takes chunk ch + 2
+        if (t == 0 && ch + kLS - 1 < nch) issue((ch + kLS - 1) % kLS, (ch + kLS - 1) * kLC);
+        const int stg = ch % kLS;
+        mbar_wait(&sm.full[stg], (uint32_t)(ch / kLS) & 1u);
+        const int lim = min(kLC, m - ch * kLC);
+        if (exact) run(stg, lim, std::true_type{});
+        else run(stg, lim, std::false_type{});
     }
     const double* bcol = d.T + (size_t)m * d.ldT;
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
         const int kk = tk + 16 * v, k = k0 + kk;
         double th = kInf;
-        if (k < la.K && s_bj[kk] >= 0) {
+        if (k < la.K && sm.bj[kk] >= 0) {
             const double xm = la.X[(size_t)k * la.ldx + m];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int li = i0 + ti + 16 * u;
-                if (!rowok[u] || d.frozen[d.row0 + li] || d.row0 + li == s_rk[kk]) continue;
+                if (!rowok[u] || d.frozen[d.row0 + li] || d.row0 + li == sm.rk[kk]) continue;
                 if (acc[u][v] <= d.pivot_tol) continue;
                 const double bb = zrow[u] ? bcol[li] : dsub(bcol[li], dmul(yv[u], xm));
                 th = min_keep(th, ddiv(bb, acc[u][v]));
@@ -2157,6 +2183,7 @@ void configure_kernels(Dev& d) {
     cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, d.upd_smem);
     cudaFuncSetAttribute(k_price, cudaFuncAttributeMaxDynamicSharedMemorySize, d.price_smem);
     cudaFuncSetAttribute(k_la_gemm_price, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaPriceSmem));
+    cudaFuncSetAttribute(k_la_gemm_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaThetaSmem));
     // One shared-memory carveout for every kernel: SMs never reconfigure the
     // L1/shared split between the streaming kernels and the small ones, and a
     // shard's spin-waiting exchange kernel can share an SM with another shard's
@@ -2252,23 +2279,38 @@ void launch_la_x(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     k_la_x<<<dim3((d.m + 1 + 255) / 256, la.K), 256, 0, st>>>(d, la);
 }
 
-void launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st) {
+bool launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     k_la_wp<<<dim3((d.m + 255) / 256, la.K), 256, 0, st>>>(d, la);
     // la.nblk = slot tiles + 1 (the last partial holds the leaving column)
-    if (la.nblk > 1)
-        k_la_gemm_price<<<dim3(la.nblk - 1, (la.K + kLK - 1) / kLK), kLThreads, sizeof(LaPriceSmem), st>>>(d, la);
+    if (la.nblk > 1) {
+        CUtensorMap tmW, tmA;
+        if (!encode_2d(&tmW, la.Wp, (uint64_t)d.m, (uint64_t)la.K, (uint64_t)la.ldx * 8, kLC, kLK) ||
+            !encode_2d(&tmA, d.A_nb, (uint64_t)d.ld_nb, (uint64_t)d.m, (uint64_t)d.ld_nb * 8, kLN, kLC))
+            return false;
+        k_la_gemm_price<<<dim3(la.nblk - 1, (la.K + kLK - 1) / kLK), kLThreads, sizeof(LaPriceSmem), st>>>(d, la, tmW,
+                                                                                                         tmA);
+    }
     k_la_leave<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
     k_la_price_local<<<la.K, 32, 0, st>>>(d, la);
+    return true;
 }
 
 void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int nsrc, cudaStream_t st) {
     k_la_decide<<<(la.K + 127) / 128, 128, 0, st>>>(d, la, msgs, nsrc);
 }
 
-void launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st) {
-    k_la_gemm_theta<<<dim3(la.nblk_t, (la.K + kLT - 1) / kLT), 256, 0, st>>>(d, la);
+bool launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st) {
+    CUtensorMap tmT, tmX, tmB;
+    if (!encode_2d(&tmT, d.T, (uint64_t)d.mloc, (uint64_t)d.m, (uint64_t)d.ldT * 8, kLT, kLC) ||
+        !encode_2d(&tmX, la.X, (uint64_t)d.m, (uint64_t)la.K, (uint64_t)la.ldx * 8, kLC, kLT) ||
+        !encode_2d(&tmB, la.Wp, (uint64_t)d.m, (uint64_t)la.K, (uint64_t)la.ldx * 8, kLC, kLT))
+        return false;
+    k_la_gather<<<dim3((d.m + 255) / 256, la.K), 256, 0, st>>>(d, la);
+    k_la_gemm_theta<<<dim3(la.nblk_t, (la.K + kLT - 1) / kLT), 256, sizeof(LaThetaSmem), st>>>(d, la, tmT, tmX,
+                                                                                                tmB);
     k_la_own<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
     k_la_theta_local<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);
+    return true;
 }
 
 void launch_la_score(const Dev& d, LookaheadDev& la, const double* tl, int nsrc, cudaStream_t st) {

@@ -76,6 +76,12 @@ double now_s() {
 
 long long round_up(long long v, long long a) { return (v + a - 1) / a * a; }
 
+// The lookahead GEMMs encode their TMA descriptors per batch (the operand
+// buffers are stream-ordered temporaries).
+void la_ok(bool ok) {
+    if (!ok) throw Error(LPSG_CUDA_ERROR, "lookahead: cuTensorMapEncodeTiled failed");
+}
+
 // Two timing events, destroyed on every exit (the throwing ones included).
 struct EventPair {
     cudaEvent_t a = nullptr, b = nullptr;
@@ -1196,7 +1202,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
             L(K_OTHER, 0.0, [&] { launch_la_x(d_, la, st_); });
         }
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->sum_i64(reinterpret_cast<long long*>(la.X), (size_t)la.K * ldx, st_); });
-        L(K_LA_PRICE, kf * (double)hctl_->n_scan, [&] { launch_la_price(d_, la, st_); });
+        L(K_LA_PRICE, kf * (double)hctl_->n_scan, [&] { la_ok(launch_la_price(d_, la, st_)); });
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.pm, la.pm_all, sizeof(PriceMsg) * la.K, st_); });
         L(K_OTHER, 0.0, [&] { launch_la_decide(d_, la, sharded_ ? la.pm_all : la.pm, G, st_); });
         if (tiled_) {
@@ -1205,14 +1211,14 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
                 const int p = porder[k];
                 ensure_resident(p);
                 const Dev dp = part_dev(p);
-                L(K_LA_THETA, 2.0 * kf * (double)dp.mloc, [&] { launch_la_theta(dp, la, st_); });
+                L(K_LA_THETA, 2.0 * kf * (double)dp.mloc, [&] { la_ok(launch_la_theta(dp, la, st_)); });
                 CK(cudaMemcpyAsync(la.tl_all + (size_t)p * la.K, la.tl, sizeof(double) * la.K,
                                    cudaMemcpyDeviceToDevice, st_));
                 ev_chain_ = nullptr;
             }
             L(K_OTHER, 0.0, [&] { launch_la_score(d_, la, la.tl_all, P, st_); });
         } else {
-            L(K_LA_THETA, 2.0 * kf * (double)d_.mloc, [&] { launch_la_theta(d_, la, st_); });
+            L(K_LA_THETA, 2.0 * kf * (double)d_.mloc, [&] { la_ok(launch_la_theta(d_, la, st_)); });
             if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.tl, la.tl_all, sizeof(double) * la.K, st_); });
             L(K_OTHER, 0.0, [&] { launch_la_score(d_, la, sharded_ ? la.tl_all : la.tl, G, st_); });
         }
