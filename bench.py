@@ -392,6 +392,7 @@ def run_ours(args, cfg):
         stats = s.profile_stats()
         prof_range = [W + done, rep_p.iterations]
         done_p = rep_p.iterations - W - done
+    la_stats = s.lookahead_stats()
     s.close()
 
     # ---- roofline of the dominant kernel (per GPU) and of the whole pivot
@@ -453,11 +454,19 @@ def run_ours(args, cfg):
             # cores: either would change the bits), so the roofline is the fp64 pipe
             ldom = max(la, key=lambda k: la[k]["ms_total"])
             fpk = P.fp64_peak(device)
+            src = ("measured in this run: lpsg_fp64_peak (independent DMUL/DADD chains on all SMs, "
+                   "1 flop per instruction)")
+            if ldom == "lookahead_price" and la_stats["price_bounded"]:
+                # the bounded pricing's screen runs on the fp64 tensor cores (DMMA
+                # m8n8k4): 37.1 TFLOP/s measured, 2 x the DMUL/DADD instruction rate
+                # (tools/microbench/dmma_rate.cu)
+                fpk *= 2
+                src += ("; x 2 for the bounded pricing's DMMA screen (fp64 tensor cores, "
+                        "tools/microbench/dmma_rate.cu: 37.1 TFLOP/s)")
             roofline = {"bound": "fp64", "kernel": ldom, "achieved": la[ldom]["tflops"],
                         "peak": round(fpk, 2), "unit": "TFLOP/s",
                         "frac": round(la[ldom]["tflops"] / fpk, 4), "traffic": None,
-                        "peak_source": "measured in this run: lpsg_fp64_peak (independent DMUL/DADD "
-                                       "chains on all SMs, 1 flop per instruction)",
+                        "peak_source": src,
                         "lookahead_share_of_profiled_time": round(la_ms / tot, 4),
                         "lookahead_tflops_all": round(sum(stats[k]["bytes"] for k in la) /
                                                       (la_ms / 1e3) / 1e12, 3),
@@ -569,6 +578,14 @@ def run_ours(args, cfg):
     }
     if exchange:
         line["exchange"] = exchange
+    if any(la_stats.values()):
+        line["lookahead"] = dict(la_stats, note=(
+            "lookaheads of >= 16 candidates over the timed + profiled windows. bounded / full: "
+            "select_leaving ties settled by the bounded selection (every later score provably "
+            "<= the first survivor's +-0; the theta' GEMM skipped) vs scored in full. "
+            "price_bounded / price_exact: pricings settled by the DMMA screen with rigorous "
+            "error bounds + exact chains for the columns it cannot exclude vs the exact GEMM "
+            "rerun. Decisions are the reference's either way (DESIGN.md §4)"))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         kc = min(K, cfg["cpu_pivots"])

@@ -76,7 +76,10 @@ typedef struct {
                                   fused epilogue;
                               [1] bit 0: attach the NCCL exchange path even for
                                   world_size 1 (exercises NCCL on one GPU);
-                              [2] bit 4: lookahead theta' keeps the y_i == 0 select.
+                              [2] bit 4: lookahead theta' keeps the y_i == 0 select;
+                                  bit 5: select_leaving tries the bounded selection
+                                  on every tie of >= 2 survivors (default: >= 16);
+                                  bit 6: never (every tie scored in full).
                               Other bits of [2] are read only by the
                               -DLPSG_EXPERIMENTS build (device.cuh). */
     /* Sharded solve over NCCL, one process (or thread) per GPU:
@@ -210,6 +213,13 @@ int lpsg_get_memory(lpsg_solver* s, lpsg_memory* out);
  * one, and device seconds spent rebuilding. */
 int lpsg_reinvert_stats(lpsg_solver* s, long* rebuilds, long* steps, double* residual_before,
                         double* residual_after, double* seconds);
+/* Batched lookaheads of >= 16 candidates. select_leaving's
+ * (solver.cpp:215-238, one GPU): how many the bounded selection settled (every
+ * later score provably <= the first survivor's) and how many were scored in
+ * full. All of them: how many pricings the DMMA screen + exact chains settled
+ * and how many needed the exact GEMM after all. Results are identical either way. */
+int lpsg_lookahead_stats(lpsg_solver* s, long long* bounded, long long* full, long long* price_bounded,
+                         long long* price_exact);
 
 /* ---- multi-GPU -------------------------
  * NCCL unique id for lpsg_config.nccl_id (rank 0 creates it, the caller

@@ -37,6 +37,10 @@
 namespace lpsg {
 
 constexpr int kLookaheadExactBit = 16;  // lpsg_config.reserved[2]: see Dev::la_exact
+// lpsg_config.reserved[2]: select_leaving's bounded selection on every tie of
+// >= 2 survivors (verification) / never (A/B); default from 16 survivors up
+constexpr int kLookaheadBoundAllBit = 32;
+constexpr int kLookaheadBoundOffBit = 64;
 
 inline const char* xp_env(const char* name) {
 #ifdef LPSG_EXPERIMENTS
@@ -245,7 +249,35 @@ struct LookaheadDev {
     int* nonfinite;   // set by k_la_wp when some X_kj (j < m) is inf/NaN (host zeroes it)
     int x_owned_only; // Case 2: k_la_x writes only the rows of the resident partition (runs once
                       // per partition) instead of zero-filling the others for a sum exchange
+    // bounded selection (k_la_probe*, select_leaving only): probe rows, their T
+    // columns gathered [j][r], per-candidate certificates, the verdict
+    int* prow;        // kLaProbe probe rows (ascending)
+    int* nprow;       // how many
+    double* Tg;       // m x kLaProbe
+    int* ok;          // K: some probe row proves theta'_k <= 0
+    int* clist;       // candidates still unproven (ascending), for the next probe round
+    int* ncl;         // how many
+    int* first;       // 1: the first candidate is provably chosen
+    // bounded pricing (k_la_gemm_price<true> + k_la_cands/k_la_exact): z~ by
+    // any-order DFMA with a rigorous error bound, exact chains only where the
+    // bound cannot exclude the argmax
+    const double* anorm;  // n_total: ||a_j||_2 of the original columns
+    double* wnorm;    // K: ||W'_k||_2
+    double* ztil;     // K x ldz: z~_k(s)
+    long long ldz;
+    double* part_L;   // K x nblk: per-tile max lower bound
+    int* cj;          // K x kLaCand: columns whose interval reaches the best lower bound
+    int* cn;          // K: how many (> kLaCand: overflow -> exact GEMM)
+    double* cz;       // K x kLaCand: their exact z
+    int* pairs;       // flattened k * kLaCand + e, for the exact chains
+    int* npairs;
+    int* fail;        // 1: some bound unusable (non-finite, list overflow): run the exact GEMM
 };
+constexpr int kLaCand = 8;         // exact candidates per lookahead candidate
+constexpr int kLaPairs = 1 << 14;  // exact chains per batch
+constexpr int kLaProbeRound = 64;                     // probe rows per round
+constexpr int kLaProbeRounds = 6;                     // rounds before falling back to full scoring
+constexpr int kLaProbe = kLaProbeRound * kLaProbeRounds;  // probe rows gathered
 
 // ---- launchers (kernels.cu) -------------------------------------------------
 void configure_kernels(Dev& d);
@@ -273,9 +305,15 @@ void launch_drive_red(const Dev& d, cudaStream_t st);
 // lookahead phases; world > 1 exchanges between them (solver.cu)
 double fp64_probe_tflops(cudaStream_t st);  // k_fp64_probe, best of 5
 void launch_la_x(const Dev& d, LookaheadDev& la, cudaStream_t st);
-bool launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st);  // false: TMA descriptor encode failed
+// false: TMA descriptor encode failed. bounded: the DFMA screen + exact chains
+// (la.anorm ... la.fail set); else the exact GEMM over every slot.
+bool launch_la_price(const Dev& d, LookaheadDev& la, bool bounded, cudaStream_t st);
+void launch_colnorm(const Dev& d, double* out, cudaStream_t st);  // ||a_j||_2, j < n_total
 void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int nsrc, cudaStream_t st);
 bool launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st);
+// select_leaving's bounded path (unsharded, in-core): la.first = 1 when the
+// first candidate provably wins ("bounded selection")
+void launch_la_probe(const Dev& d, LookaheadDev& la, cudaStream_t st);
 void launch_la_score(const Dev& d, LookaheadDev& la, const double* tl, int nsrc, cudaStream_t st);
 // in-process shard exchange helpers (LocalComm): out[k] = sum_g in[g*n + k] / min_g
 void launch_sum_i64(const long long* in, int nsrc, size_t n, long long* out, cudaStream_t st);

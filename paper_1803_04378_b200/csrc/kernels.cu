@@ -1609,9 +1609,13 @@ struct LaPriceSmem {
 // the best (z, j) of the tile's 128 slots per candidate -> part_z/part_j[k][bx].
 // tmW: W' as {m, K} with box {16, 64}; tmA: A_nb as {ld_nb, m} with box
 // {128, 16} (slots past n_scan hold stale values whose outputs are discarded).
+//
+// only_if_fail: the fallback of the bounded pricing (exits at once unless
+// la.fail was set).
 __global__ void __launch_bounds__(kLThreads, 2)
 k_la_gemm_price(Dev d, LookaheadDev la, const __grid_constant__ CUtensorMap tmW,
-                const __grid_constant__ CUtensorMap tmA) {
+                const __grid_constant__ CUtensorMap tmA, int only_if_fail) {
+    if (only_if_fail && !*la.fail) return;
     extern __shared__ __align__(128) unsigned char la_smem[];
     LaPriceSmem& sm = *reinterpret_cast<LaPriceSmem*>(la_smem);
     const int n_scan = d.ctl->n_scan;
@@ -1999,6 +2003,426 @@ k_la_gemm_theta(Dev d, LookaheadDev la, const __grid_constant__ CUtensorMap tmT,
     }
 }
 
+// ---- bounded pricing: a DMMA screen, exact chains only where it is unsure --
+// z~_k(s) = W'_k . a_s - c_j on the fp64 tensor cores (mma.sync m8n8k4: any
+// summation order, so its value differs from the reference's sequential chain
+// by at most E = 3 gamma_m ||W'_k|| ||a_j|| + 4 u |z~| + 1e-300: both lie
+// within gamma_m sum_i |W'_ki a_ij| (<= the norm product, Cauchy-Schwarz) of
+// the exact dot, each subtraction of c_j adds u |z| (Higham, Accuracy and
+// Stability of Numerical Algorithms, 3.1), and the absolute term covers
+// flushed subnormals). The tile is pricing's 64 candidates x 128 slots; 8
+// warps = 2 candidate halves x 4 slot quarters, 32 x 32 outputs per warp as
+// 4 x 4 fragments; W' boxes land 128B-swizzled (conflict-free A fragments).
+// Per tile and candidate it keeps max(z~ - E) -> part_L; z~ -> ztil.
+// tools/microbench/la_price_rate.cu: 0.83 of the 37 TFLOP/s DMMA peak, against
+// 0.69 for the same screen as SIMT DFMA.
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c[0]), "+d"(c[1])
+                 : "d"(a), "d"(b));
+}
+struct LaScreenSmem {
+    double W[kLS][kLK][kLC];  // [k][i], rows 128B-swizzled by TMA
+    double A[kLS][kLC][kLN];  // [i][s]
+    uint64_t full[kLS];
+    double lo[kLK][4];        // per candidate x slot quarter
+};
+__global__ void __launch_bounds__(kLThreads, 2)
+k_la_screen(Dev d, LookaheadDev la, const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA) {
+    extern __shared__ __align__(1024) unsigned char la_smem[];
+    LaScreenSmem& sm =
+        *reinterpret_cast<LaScreenSmem*>((reinterpret_cast<uintptr_t>(la_smem) + 1023) & ~uintptr_t(1023));
+    const int n_scan = d.ctl->n_scan;
+    const double* cost = phase_cost(d, d.ctl->phase);
+    const int s0 = blockIdx.x * kLN, k0 = blockIdx.y * kLK;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, g = lane >> 2, tq = lane & 3;
+    const int wc = warp & 1, ws = warp >> 1;
+    const int m = d.m;
+    if (t == 0) {
+        for (int s = 0; s < kLS; ++s) mbar_init(&sm.full[s], 1);
+        mbar_fence_init();
+    }
+    __syncthreads();
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    constexpr uint32_t kBytes = (kLK * kLC + kLC * kLN) * 8;
+    auto issue = [&](int stage, int i0) {
+        mbar_expect_tx(&sm.full[stage], kBytes);
+        tma_load_2d(&sm.W[stage][0][0], &tmW, i0, k0, &sm.full[stage]);
+        tma_load_2d(&sm.A[stage][0][0], &tmA, s0, i0, &sm.full[stage]);
+    };
+    const int nch = (m + kLC - 1) / kLC;  // a partial last chunk is zero-filled by TMA
+    if (t == 0)
+        for (int st = 0; st < kLS - 1 && st < nch; ++st) issue(st, st * kLC);
+    for (int ch = 0; ch < nch; ++ch) {
+        __syncthreads();  // every thread is done with chunk ch - 1: its stage takes chunk ch + 2
+        if (t == 0 && ch + kLS - 1 < nch) issue((ch + kLS - 1) % kLS, (ch + kLS - 1) * kLC);
+        const int stg = ch % kLS;
+        mbar_wait(&sm.full[stg], (uint32_t)(ch / kLS) & 1u);
+        const double* Ws = &sm.W[stg][0][0];
+#pragma unroll
+        for (int kk = 0; kk < kLC / 4; ++kk) {
+            const int e = kk * 4 + tq;
+            double af[4], bf[4];
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb) {  // A fragment: row g, column tq (128B swizzle: 16-byte chunk ^ row % 8)
+                const int r = wc * 32 + cb * 8 + g;
+                af[cb] = Ws[r * kLC + ((((e >> 1) ^ (r & 7)) << 1) | (e & 1))];
+            }
+#pragma unroll
+            for (int sb = 0; sb < 4; ++sb) bf[sb] = sm.A[stg][e][ws * 32 + sb * 8 + g];  // B: row tq, column g
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+                for (int sb = 0; sb < 4; ++sb) dmma_8x8x4(acc[cb][sb], af[cb], bf[sb]);
+        }
+    }
+    const double uu = 1.1102230246251565e-16;
+    const double cE = 3.0 * (m * uu / (1.0 - m * uu)) * (1.0 + 1e-6);
+    bool bad = false;
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) {
+        const int kl = wc * 32 + cb * 8 + g, k = k0 + kl;
+        const double wn = k < la.K ? la.wnorm[k] : 0.0;
+        double lo = -kInf;
+#pragma unroll
+        for (int sb = 0; sb < 4; ++sb)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {  // C fragment: row g, columns 2 tq + h
+                const int sl = s0 + ws * 32 + sb * 8 + 2 * tq + h;
+                if (sl < n_scan && k < la.K) {
+                    const int j = d.slot2col[sl];
+                    const double z = acc[cb][sb][h] - cost[j];
+                    const double e = cE * wn * la.anorm[j] + 4.0 * uu * fabs(z) + 1e-300;
+                    bad |= !isfinite(z) || !isfinite(e);
+                    la.ztil[(size_t)k * la.ldz + sl] = z;
+                    if (j != la.q) lo = fmax(lo, z - e);
+                }
+            }
+        lo = fmax(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
+        lo = fmax(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
+        if (tq == 0) sm.lo[kl][ws] = lo;
+    }
+    if (bad) *la.fail = 1;
+    __syncthreads();
+    if (t < kLK && k0 + t < la.K)
+        la.part_L[(size_t)(k0 + t) * la.nblk + blockIdx.x] =
+            fmax(fmax(sm.lo[t][0], sm.lo[t][1]), fmax(sm.lo[t][2], sm.lo[t][3]));
+}
+
+// exact chains only where the screen is unsure:
+
+__global__ void k_colnorm(Dev d, double* out) {  // one warp per column
+    const int j = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+    if (j >= d.n_total) return;
+    const double* a = d.A_cm + (size_t)j * d.ld_cm;
+    double s = 0.0;
+    for (int i = lane; i < d.m; i += 32) s = fma(a[i], a[i], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[j] = sqrt(s);
+}
+
+__global__ void k_la_wnorm(Dev d, LookaheadDev la) {  // one CTA per candidate
+    __shared__ double red[32];
+    const int k = blockIdx.x;
+    const double* w = la.Wp + (size_t)k * la.ldx;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < d.m; i += blockDim.x) s = fma(w[i], w[i], s);
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int v = 0; v < (int)(blockDim.x >> 5); ++v) t += red[v];
+        la.wnorm[k] = sqrt(t);
+        la.cn[k] = 0;
+    }
+}
+
+// Candidate k's columns whose interval [z~ - E, z~ + E] reaches L_k, the best
+// lower bound (the tiles' and the leaving column's exact z): every column
+// that can be the exact (max z, min j) lies among them (one CTA per candidate).
+__global__ void __launch_bounds__(256) k_la_cands(Dev d, LookaheadDev la) {
+    __shared__ double red[8];
+    const int k = blockIdx.x;
+    const int ntile = la.nblk - 1;
+    double L = la.part_z[(size_t)k * la.nblk + ntile];  // leaving column, exact (k_la_leave)
+    for (int b = threadIdx.x; b < ntile; b += blockDim.x) L = fmax(L, la.part_L[(size_t)k * la.nblk + b]);
+    for (int o = 16; o > 0; o >>= 1) L = fmax(L, __shfl_xor_sync(0xffffffffu, L, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = L;
+    __syncthreads();
+    L = red[0];
+    for (int v = 1; v < 8; ++v) L = fmax(L, red[v]);
+    const int n_scan = d.ctl->n_scan;
+    const double* cost = phase_cost(d, d.ctl->phase);
+    const double uu = 1.1102230246251565e-16;
+    const double cE = 3.0 * (d.m * uu / (1.0 - d.m * uu)) * (1.0 + 1e-6);
+    const double wn = la.wnorm[k];
+    for (int sl = threadIdx.x; sl < n_scan; sl += blockDim.x) {
+        const int j = d.slot2col[sl];
+        if (j == la.q) continue;
+        const double z = la.ztil[(size_t)k * la.ldz + sl];
+        const double e = cE * wn * la.anorm[j] + 4.0 * uu * fabs(z) + 1e-300;
+        if (z + e >= L) {
+            const int c = atomicAdd(la.cn + k, 1);
+            if (c >= kLaCand) {
+                *la.fail = 1;
+                continue;
+            }
+            la.cj[k * kLaCand + c] = j;
+            const int p = atomicAdd(la.npairs, 1);
+            if (p < kLaPairs) la.pairs[p] = k * kLaCand + c;
+            else *la.fail = 1;
+        }
+    }
+    (void)cost;
+}
+
+// The listed (k, j): exact z = dot(W'_k, a_j) - c_j, the reference's chain
+// (solver.cpp:190-200), 16 per CTA through cta_batched_dot.
+__global__ void __launch_bounds__(kDT) k_la_exact(Dev d, LookaheadDev la) {
+    __shared__ DotSmem sm;
+    const int np = min(*la.npairs, kLaPairs);
+    const int p0 = blockIdx.x * kDC;
+    if (p0 >= np || *la.fail) return;
+    if (threadIdx.x < kDC) {
+        const int p = p0 + threadIdx.x;
+        const int e = p < np ? la.pairs[p] : -1;
+        sm.vc[threadIdx.x] = e >= 0 ? la.cj[e] : -1;
+        sm.ub[threadIdx.x] = e >= 0 ? la.Wp + (size_t)(e / kLaCand) * la.ldx : nullptr;
+    }
+    __syncthreads();
+    const double acc = cta_batched_dot(sm, d.A_cm, d.ld_cm, d.m);
+    const int p = p0 + threadIdx.x;
+    if (threadIdx.x >= kDC || p >= np) return;
+    const double* cost = phase_cost(d, d.ctl->phase);
+    la.cz[la.pairs[p]] = dsub(acc, cost[sm.vc[threadIdx.x]]);
+}
+
+// Each candidate's exact best over its list into pricing partial 0 (the other
+// tile partials are cleared; the leaving column's stays in nblk - 1).
+__global__ void k_la_cands_best(Dev d, LookaheadDev la) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= la.K || *la.fail) return;
+    double bz = -kInf;
+    int bj = INT_MAX;
+    const int n = min(la.cn[k], kLaCand);
+    for (int c = 0; c < n; ++c) {
+        const double z = la.cz[k * kLaCand + c];
+        const int j = la.cj[k * kLaCand + c];
+        if (better(z, j, bz, bj)) { bz = z; bj = j; }
+    }
+    for (int b = 0; b < la.nblk - 1; ++b) {
+        la.part_z[(size_t)k * la.nblk + b] = b == 0 ? bz : -kInf;
+        la.part_j[(size_t)k * la.nblk + b] = b == 0 ? bj : INT_MAX;
+    }
+}
+
+// ---- bounded selection: select_leaving without the theta' GEMM ----------
+// select_leaving keeps the FIRST survivor with the largest score (strict '>'
+// from best = -1, solver.cpp:228-235). Scores are best_z * theta' with
+// best_z > opt_tol, so score_k <= 0 as soon as ONE eligible row of candidate k's
+// pivoted tableau has a ratio <= 0: rhs'_ik <= 0 and y'_ik > pivot_tol (theta'
+// is a min). On a degenerate tie that holds for every candidate (C4: all ~1000
+// scores are exactly 0), and if the first candidate's score is provably +-0
+// (some ratio <= 0 and no eligible ratio < 0, i.e. no row with rhs' < 0), no
+// later candidate can beat it. The probe computes y'_ik on kLaProbe rows with
+// b_bar_i <= 0 for every candidate, in the reference's exact order and
+// arithmetic (the same chain as k_la_gemm_theta), so each certificate is a
+// fact about the reference's own values; anything unproven falls back to the
+// full scoring. The decision is the reference's, bit for bit, either way.
+
+// the first kLaProbe non-frozen rows with b_bar_i <= 0, ascending (one CTA);
+// round r probes rows [64 r, 64 r + 64) of them
+__global__ void __launch_bounds__(1024) k_la_probe_rows(Dev d, LookaheadDev la) {
+    __shared__ int base, wcnt[32];
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    const double* bcol = d.T + (size_t)d.m * d.ldT;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int i0 = 0; i0 < d.m; i0 += 1024) {
+        const int i = i0 + threadIdx.x;
+        const bool pick = i < d.m && !d.frozen[i] && bcol[i] <= 0.0;
+        const unsigned bal = __ballot_sync(0xffffffffu, pick);
+        if (lane == 0) wcnt[w] = __popc(bal);
+        __syncthreads();
+        int off = base;
+        for (int v = 0; v < w; ++v) off += wcnt[v];
+        off += __popc(bal & ((1u << lane) - 1u));
+        if (pick && off < kLaProbe) la.prow[off] = i;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int v = 0; v < 32; ++v) base += wcnt[v];
+        __syncthreads();
+        if (base >= kLaProbe) break;
+    }
+    if (threadIdx.x == 0) *la.nprow = min(base, kLaProbe);
+}
+
+// Tg[j][r] = T_{prow[r], j} (j < m), zero for r >= nprow
+__global__ void k_la_probe_gather(Dev d, LookaheadDev la) {
+    const int np = *la.nprow;
+    const size_t n = (size_t)d.m * kLaProbe;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+        const int r = (int)(e % kLaProbe);
+        const size_t j = e / kLaProbe;
+        la.Tg[e] = r < np ? d.T[j * d.ldT + la.prow[r]] : 0.0;
+    }
+}
+
+// candidates with a best column and no certificate yet, ascending (one CTA)
+__global__ void __launch_bounds__(1024) k_la_probe_list(LookaheadDev la) {
+    __shared__ int base, wcnt[32];
+    if (threadIdx.x == 0) base = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int k0 = 0; k0 < la.K; k0 += 1024) {
+        const int k = k0 + threadIdx.x;
+        const bool pick = k < la.K && la.bj[k] >= 0 && !la.ok[k];
+        const unsigned bal = __ballot_sync(0xffffffffu, pick);
+        if (lane == 0) wcnt[w] = __popc(bal);
+        __syncthreads();
+        int off = base;
+        for (int v = 0; v < w; ++v) off += wcnt[v];
+        if (pick) la.clist[off + __popc(bal & ((1u << lane) - 1u))] = k;
+        __syncthreads();
+        if (threadIdx.x == 0)
+            for (int v = 0; v < 32; ++v) base += wcnt[v];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *la.ncl = base;
+}
+
+// One probe round: y'_ik for the round's kLaProbeRound probe rows x the
+// unproven candidates. A CTA of 128 threads takes the 64 rows x 8 candidates,
+// 2 x 2 chains per thread (rows t % 32 + {0, 32}, candidates t / 32 + {0, 4}):
+// per chain step 6 shared loads feed 16 fp64 instructions, which balances the
+// shared-memory wavefronts against the fp64 pipe. 16-deep chunks are
+// register-staged; the chains run in the reference's order and arithmetic
+// (solver.cpp:177-184, 205). ok[k] = 1 when some row i != r_k has rhs'_ik <= 0
+// and y'_ik > pivot_tol.
+constexpr int kPC = 16, kPKc = 8;
+__global__ void __launch_bounds__(128) k_la_probe(Dev d, LookaheadDev la, int round) {
+    __shared__ double Ts[kPC][kLaProbeRound];
+    __shared__ double Xs[kPKc][kPC];
+    __shared__ double Bs[kPKc][kPC];
+    const int ncl = *la.ncl, np = *la.nprow;
+    const int r0 = round * kLaProbeRound;
+    if (blockIdx.x * kPKc >= ncl || r0 >= np) return;
+    const int m = d.m, t = threadIdx.x, tr = t & 31, tc = t >> 5;
+    int kk[2], row[2];
+    double yv[2];
+    bool zr[2];
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+        const int ci = blockIdx.x * kPKc + tc + 4 * v;
+        kk[v] = ci < ncl ? la.clist[ci] : -1;
+        const int r = r0 + tr + 32 * v;
+        row[v] = r < np ? la.prow[r] : -1;
+        yv[v] = row[v] >= 0 ? d.Y[row[v]] : 0.0;
+        zr[v] = yv[v] == 0.0;
+    }
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [row][candidate]
+    // chunk loads: Tg 16 j x 64 rows (8 per thread), X and Bg 8 candidates x 16 j (1 each)
+    double rt[8], rx, rb;
+    auto fetch = [&](int j0) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = t + 128 * q, rr = e % kLaProbeRound, jj = e / kLaProbeRound;
+            rt[q] = j0 + jj < m ? la.Tg[(size_t)(j0 + jj) * kLaProbe + r0 + rr] : 0.0;
+        }
+        const int jj = t % kPC, cc = t / kPC;
+        const int c2 = blockIdx.x * kPKc + cc;
+        const int k2 = c2 < ncl ? la.clist[c2] : -1;
+        const bool ok = k2 >= 0 && j0 + jj < m;
+        rx = ok ? la.X[(size_t)k2 * la.ldx + j0 + jj] : 0.0;
+        rb = ok ? la.Wp[(size_t)k2 * la.ldx + j0 + jj] : 0.0;
+    };
+    fetch(0);
+    for (int j0 = 0; j0 < m; j0 += kPC) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int e = t + 128 * q;
+            Ts[e / kLaProbeRound][e % kLaProbeRound] = rt[q];
+        }
+        Xs[t / kPC][t % kPC] = rx;
+        Bs[t / kPC][t % kPC] = rb;
+        __syncthreads();
+        if (j0 + kPC < m) fetch(j0 + kPC);
+        auto step = [&](int jj) {
+            double tv[2], xv[2], bv[2];
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+                tv[v] = Ts[jj][tr + 32 * v];
+                xv[v] = Xs[tc + 4 * v][jj];
+                bv[v] = Bs[tc + 4 * v][jj];
+            }
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    // rows with y_i == 0 keep T_ij (solver.cpp:177-184)
+                    const double tij = zr[u] ? tv[u] : dsub(tv[u], dmul(yv[u], xv[v]));
+                    acc[u][v] = dadd(acc[u][v], dmul(tij, bv[v]));
+                }
+        };
+        if (j0 + kPC <= m) {
+#pragma unroll
+            for (int jj = 0; jj < kPC; ++jj) step(jj);
+        } else {
+            for (int jj = 0; jj < m - j0; ++jj) step(jj);
+        }
+        __syncthreads();
+    }
+    const double* bcol = d.T + (size_t)m * d.ldT;
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+        const int k = kk[v];
+        if (k < 0) continue;
+        const double xm = la.X[(size_t)k * la.ldx + m];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (row[u] < 0 || row[u] == la.rows[k]) continue;
+            const double rhs = zr[u] ? bcol[row[u]] : dsub(bcol[row[u]], dmul(yv[u], xm));
+            if (rhs <= 0.0 && acc[u][v] > d.pivot_tol) la.ok[k] = 1;
+        }
+    }
+}
+
+// first = every candidate is certified (score <= 0) and the first one's score
+// is exactly +-0: no best column, or (certified, best_z finite, and no eligible
+// row -- own row included -- with rhs' < 0, so theta'_0 = +-0).
+// Not proven: first = -(1 + 2 * uncertified candidates + (first score not
+// provably +-0)), for the solver's trace.
+__global__ void __launch_bounds__(1024) k_la_probe_decide(Dev d, LookaheadDev la) {
+    __shared__ int nbad;
+    if (threadIdx.x == 0) nbad = 0;
+    __syncthreads();
+    for (int k = threadIdx.x; k < la.K; k += blockDim.x)
+        if (la.bj[k] >= 0 && !la.ok[k]) atomicAdd(&nbad, 1);
+    bool neg = false;
+    if (la.bj[0] >= 0) {
+        const int r0 = la.rows[0];
+        const double* X0 = la.X;
+        const double xm = X0[d.m];
+        const double* bcol = d.T + (size_t)d.m * d.ldT;
+        for (int i = threadIdx.x; i < d.m; i += blockDim.x) {
+            if (d.frozen[i]) continue;
+            const double y = d.Y[i];
+            const double rhs = i == r0 ? xm : (y == 0.0 ? bcol[i] : dsub(bcol[i], dmul(y, xm)));
+            neg |= rhs < 0.0;
+        }
+    }
+    neg = __syncthreads_or(neg);
+    if (threadIdx.x == 0) {
+        const bool cert = la.bj[0] < 0 || (!neg && isfinite(la.bz[0]));
+        *la.first = (nbad == 0 && cert) ? 1 : -(1 + 2 * nbad + (cert ? 0 : 1));
+    }
+}
+
 __global__ void k_la_price_local(Dev d, LookaheadDev la) {
     const int k = blockIdx.x;
     if (threadIdx.x >= 32) return;
@@ -2183,6 +2607,7 @@ void configure_kernels(Dev& d) {
     cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, d.upd_smem);
     cudaFuncSetAttribute(k_price, cudaFuncAttributeMaxDynamicSharedMemorySize, d.price_smem);
     cudaFuncSetAttribute(k_la_gemm_price, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaPriceSmem));
+    cudaFuncSetAttribute(k_la_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaScreenSmem) + 1024);
     cudaFuncSetAttribute(k_la_gemm_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaThetaSmem));
     // One shared-memory carveout for every kernel: SMs never reconfigure the
     // L1/shared split between the streaming kernels and the small ones, and a
@@ -2195,7 +2620,7 @@ void configure_kernels(Dev& d) {
                          (const void*)k_pivot_row, (const void*)k_pivot, (const void*)k_gather_row,
                          (const void*)k_drive_scan, (const void*)k_drive_red, (const void*)k_la_x,
                          (const void*)k_la_wp, (const void*)k_la_price_local,
-                         (const void*)k_la_gemm_price, (const void*)k_la_gemm_theta, (const void*)k_la_leave,
+                         (const void*)k_la_gemm_price, (const void*)k_la_screen, (const void*)k_la_gemm_theta, (const void*)k_la_leave,
                          (const void*)k_la_own,
                          (const void*)k_la_decide, (const void*)k_la_theta_local,
                          (const void*)k_la_score, (const void*)k_sum_i64, (const void*)k_min_i32,
@@ -2218,7 +2643,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 bool encode_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
-               uint32_t box_inner, uint32_t box_outer) {
+               uint32_t box_inner, uint32_t box_outer, bool swizzle128 = false) {
     auto fn = get_encode();
     if (!fn) return false;
     const cuuint64_t dims[2] = {inner, outer};
@@ -2226,8 +2651,8 @@ bool encode_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t oute
     const cuuint32_t box[2] = {box_inner, box_outer};
     const cuuint32_t estr[2] = {1, 1};
     return fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+              CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 }  // namespace
 
@@ -2279,20 +2704,40 @@ void launch_la_x(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     k_la_x<<<dim3((d.m + 1 + 255) / 256, la.K), 256, 0, st>>>(d, la);
 }
 
-bool launch_la_price(const Dev& d, LookaheadDev& la, cudaStream_t st) {
+bool launch_la_price(const Dev& d, LookaheadDev& la, bool bounded, cudaStream_t st) {
     k_la_wp<<<dim3((d.m + 255) / 256, la.K), 256, 0, st>>>(d, la);
     // la.nblk = slot tiles + 1 (the last partial holds the leaving column)
-    if (la.nblk > 1) {
-        CUtensorMap tmW, tmA;
-        if (!encode_2d(&tmW, la.Wp, (uint64_t)d.m, (uint64_t)la.K, (uint64_t)la.ldx * 8, kLC, kLK) ||
-            !encode_2d(&tmA, d.A_nb, (uint64_t)d.ld_nb, (uint64_t)d.m, (uint64_t)d.ld_nb * 8, kLN, kLC))
+    CUtensorMap tmW, tmA;
+    if (la.nblk > 1 &&
+        (!encode_2d(&tmW, la.Wp, (uint64_t)d.m, (uint64_t)la.K, (uint64_t)la.ldx * 8, kLC, kLK) ||
+         !encode_2d(&tmA, d.A_nb, (uint64_t)d.ld_nb, (uint64_t)d.m, (uint64_t)d.ld_nb * 8, kLN, kLC)))
+        return false;
+    const dim3 grid(la.nblk - 1, (la.K + kLK - 1) / kLK);
+    if (bounded) {
+        cudaMemsetAsync(la.fail, 0, sizeof(int), st);
+        cudaMemsetAsync(la.npairs, 0, sizeof(int), st);
+        k_la_wnorm<<<la.K, 256, 0, st>>>(d, la);
+        CUtensorMap tmWs;
+        if (la.nblk > 1 &&
+            !encode_2d(&tmWs, la.Wp, (uint64_t)d.m, (uint64_t)la.K, (uint64_t)la.ldx * 8, kLC, kLK, true))
             return false;
-        k_la_gemm_price<<<dim3(la.nblk - 1, (la.K + kLK - 1) / kLK), kLThreads, sizeof(LaPriceSmem), st>>>(d, la, tmW,
-                                                                                                         tmA);
+        if (la.nblk > 1) k_la_screen<<<grid, kLThreads, sizeof(LaScreenSmem) + 1024, st>>>(d, la, tmWs, tmA);
+        k_la_leave<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
+        k_la_cands<<<la.K, 256, 0, st>>>(d, la);
+        k_la_exact<<<kLaPairs / kDC, kDT, 0, st>>>(d, la);
+        k_la_cands_best<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);
+        // a bound was unusable: the exact GEMM after all (its CTAs exit at once otherwise)
+        if (la.nblk > 1) k_la_gemm_price<<<grid, kLThreads, sizeof(LaPriceSmem), st>>>(d, la, tmW, tmA, 1);
+    } else {
+        if (la.nblk > 1) k_la_gemm_price<<<grid, kLThreads, sizeof(LaPriceSmem), st>>>(d, la, tmW, tmA, 0);
+        k_la_leave<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
     }
-    k_la_leave<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
     k_la_price_local<<<la.K, 32, 0, st>>>(d, la);
     return true;
+}
+
+void launch_colnorm(const Dev& d, double* out, cudaStream_t st) {
+    k_colnorm<<<(d.n_total + 7) / 8, 256, 0, st>>>(d, out);
 }
 
 void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int nsrc, cudaStream_t st) {
@@ -2311,6 +2756,20 @@ bool launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     k_la_own<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
     k_la_theta_local<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);
     return true;
+}
+
+void launch_la_probe(const Dev& d, LookaheadDev& la, cudaStream_t st) {
+    cudaMemsetAsync(la.ok, 0, sizeof(int) * la.K, st);
+    k_la_probe_rows<<<1, 1024, 0, st>>>(d, la);
+    k_la_gather<<<dim3((d.m + 255) / 256, la.K), 256, 0, st>>>(d, la);
+    k_la_probe_gather<<<4 * 148, 256, 0, st>>>(d, la);
+    // rounds over further probe rows for the candidates still unproven; a
+    // round with nothing left exits at once
+    for (int r = 0; r < kLaProbeRounds; ++r) {
+        k_la_probe_list<<<1, 1024, 0, st>>>(la);
+        k_la_probe<<<(la.K + kPKc - 1) / kPKc, 128, 0, st>>>(d, la, r);
+    }
+    k_la_probe_decide<<<1, 1024, 0, st>>>(d, la);
 }
 
 void launch_la_score(const Dev& d, LookaheadDev& la, const double* tl, int nsrc, cudaStream_t st) {

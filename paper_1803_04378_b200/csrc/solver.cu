@@ -76,6 +76,10 @@ double now_s() {
 
 long long round_up(long long v, long long a) { return (v + a - 1) / a * a; }
 
+// select_leaving tries the bounded selection (k_la_probe*) from this many
+// survivors up; smaller ties are cheap to score in full.
+constexpr int kLaBoundMin = 16;
+
 // The lookahead GEMMs encode their TMA descriptors per batch (the operand
 // buffers are stream-ordered temporaries).
 void la_ok(bool ok) {
@@ -155,7 +159,15 @@ public:
     void step_compute_direction(int entering, double red);
     void step_ratio(int* unbounded, double* theta, std::vector<int>& cand);
     int select_leaving(const std::vector<int>& cand, int entering);
-    void lookahead(const std::vector<int>& rows, int entering, std::vector<double>& scores);
+    // first_proven != nullptr: select_leaving's bounded path may settle the
+    // choice (then *first_proven = true and `scores` is not filled)
+    void lookahead(const std::vector<int>& rows, int entering, std::vector<double>& scores,
+                   bool* first_proven = nullptr);
+    long long la_bounded_ = 0, la_full_ = 0;  // select_leaving lookaheads: settled by the probe / fully scored
+    long long la_price_bounded_ = 0, la_price_exact_ = 0;  // lookahead pricings: DMMA screen held / exact GEMM rerun
+    int la_bound_min_ = 16;                   // survivors from which the probe / bounded pricing are used
+    double* anorm_ = nullptr;                 // ||a_j||_2 of A's columns (bounded pricing), made on first use
+    void free_la(LookaheadDev& la, int* rows_d);
     void step_pivot(int r, int q);
     void read_row(int i, double* out);
 
@@ -518,8 +530,10 @@ void Solver::init(const lpsg_problem& lp) {
         throw Error(LPSG_INVALID_ARGUMENT, "lpsg_create: reinversion is single-GPU only");
     reinv_every_ = cfg_.reinvert_every;
     d_.naive = cfg_.kernel == 1 ? 1 : 0;
-    d_.dbg = cfg_.reserved[2] & ~kLookaheadExactBit;  // perf experiments (-DLPSG_EXPERIMENTS only)
-    d_.la_exact = (cfg_.reserved[2] & kLookaheadExactBit) != 0;
+    d_.dbg = cfg_.reserved[2] & ~(kLookaheadExactBit | kLookaheadBoundAllBit | kLookaheadBoundOffBit);
+    d_.la_exact = (cfg_.reserved[2] & kLookaheadExactBit) != 0;  // (dbg: -DLPSG_EXPERIMENTS only)
+    la_bound_min_ = (cfg_.reserved[2] & kLookaheadBoundOffBit) ? INT_MAX
+                    : (cfg_.reserved[2] & kLookaheadBoundAllBit) ? 2 : kLaBoundMin;
     // PDL hides kernel-boundary latency; it pays up to m ~ 10^4 (C1 +21 %, C3
     // +1.4 %) and was measured to cost ~17 % at m = 24000, where the boundaries
     // are noise against 3 ms pivots
@@ -685,7 +699,7 @@ void Solver::release() {
     void* bufs[] = {d_.T, d_.top, d_.Y, d_.xrow, shared_A_cm_ ? nullptr : (void*)d_.A_cm, d_.A_nb, d_.slot2col, d_.col2slot,
                     d_.basic, d_.frozen, cost_buf_, d_.ctl, d_.cand, d_.pz, d_.pj, d_.log, scratch_, tmaps_,
                     d_.rc_theta, d_.rc_cnt, d_.rc_row, d_.rc_ratio, d_.cand_ratio, d_.pmsg, d_.rmsg,
-                    chain_, b0_, art_row_, part_msgs_, part_row0_, xbuf_own_};
+                    chain_, b0_, art_row_, part_msgs_, part_row0_, xbuf_own_, anorm_};
     for (void* p : bufs)
         if (p) cudaFree(p);
     if (host_T_) cudaFreeHost(host_T_);
@@ -694,6 +708,7 @@ void Solver::release() {
     part_msgs_ = nullptr;
     part_row0_ = nullptr;
     xbuf_own_ = nullptr;
+    anorm_ = nullptr;
     if (hctl_) cudaFreeHost(hctl_);
     if (hlog_) cudaFreeHost(hlog_);
     if (hone_) cudaFreeHost(hone_);
@@ -1122,7 +1137,12 @@ int Solver::select_leaving(const std::vector<int>& cand, int entering) {
     int chosen = survivors.front();
     if (survivors.size() > 1) {
         std::vector<double> scores;
-        lookahead(survivors, entering, scores);
+        bool first = false;
+        lookahead(survivors, entering, scores, &first);
+        if (first) {  // proven: every later score <= the first one's (+-0)
+            banned.insert(basic_[chosen]);
+            return chosen;
+        }
         double best = -1.0;
         for (size_t k = 0; k < survivors.size(); ++k)
             if (scores[k] > best) {
@@ -1137,10 +1157,12 @@ int Solver::select_leaving(const std::vector<int>& cand, int entering) {
 // lookahead_score (solver.cpp:164-213) for every row in `rows`, batched on the
 // device. Sharded: pivot rows from their owners, pricing and theta' per shard,
 // exact max / min merges (every rank computes the same scores).
-void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<double>& scores) {
+void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<double>& scores,
+                       bool* first_proven) {
     const int K = (int)rows.size();
     scores.assign(K, 0.0);
     if (K == 0) return;
+    if (first_proven) *first_proven = false;
     const int m = m_;
     const int G = world_;
     const int ldx = (int)round_up(m + 1, 32);
@@ -1178,6 +1200,26 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
             if (p != resident_) porder.push_back(p);
     }
     la.nonfinite = talloc<int>(1, st_, pool_);
+    // bounded pricing (kernels.cu k_la_gemm_price<true>, k_la_cands, k_la_exact):
+    // from la_bound_min_ candidates up, the exact argmax without the exact GEMM
+    const bool bounded = kb >= la_bound_min_;
+    if (bounded) {
+        if (!anorm_) {
+            anorm_ = dalloc<double>(n_total_);
+            launch_colnorm(d_, anorm_, st_);
+        }
+        la.anorm = anorm_;
+        la.ldz = round_up(std::max(1, hctl_->n_scan), 4);
+        la.wnorm = talloc<double>(kb, st_, pool_);
+        la.ztil = talloc<double>((size_t)kb * la.ldz, st_, pool_);
+        la.part_L = talloc<double>((size_t)kb * la.nblk, st_, pool_);
+        la.cj = talloc<int>((size_t)kb * kLaCand, st_, pool_);
+        la.cz = talloc<double>((size_t)kb * kLaCand, st_, pool_);
+        la.cn = talloc<int>(kb, st_, pool_);
+        la.pairs = talloc<int>(kLaPairs, st_, pool_);
+        la.npairs = talloc<int>(1, st_, pool_);
+        la.fail = talloc<int>(1, st_, pool_);
+    }
     CK(cudaMemsetAsync(la.X, 0, sizeof(double) * (size_t)kb * ldx, st_));
     if (dbg_trace_) fprintf(stderr, "[solver r%d] lookahead K=%d\n", rank_, K);
     temp_alloc_fence();
@@ -1202,9 +1244,58 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
             L(K_OTHER, 0.0, [&] { launch_la_x(d_, la, st_); });
         }
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->sum_i64(reinterpret_cast<long long*>(la.X), (size_t)la.K * ldx, st_); });
-        L(K_LA_PRICE, kf * (double)hctl_->n_scan, [&] { la_ok(launch_la_price(d_, la, st_)); });
+        L(K_LA_PRICE, kf * (double)hctl_->n_scan, [&] { la_ok(launch_la_price(d_, la, bounded, st_)); });
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.pm, la.pm_all, sizeof(PriceMsg) * la.K, st_); });
         L(K_OTHER, 0.0, [&] { launch_la_decide(d_, la, sharded_ ? la.pm_all : la.pm, G, st_); });
+        // bounded selection (kernels.cu, k_la_probe*): one GPU, in-core, one batch
+        if (first_proven && !sharded_ && !tiled_ && la.K == K && K >= la_bound_min_) {
+            la.prow = talloc<int>(kLaProbe, st_, pool_);
+            la.nprow = talloc<int>(1, st_, pool_);
+            la.Tg = talloc<double>((size_t)m * kLaProbe, st_, pool_);
+            la.ok = talloc<int>(K, st_, pool_);
+            la.clist = talloc<int>(K, st_, pool_);
+            la.ncl = talloc<int>(1, st_, pool_);
+            la.first = talloc<int>(1, st_, pool_);
+            L(K_LA_THETA, 2.0 * kf * kLaProbeRound, [&] { launch_la_probe(d_, la, st_); });
+            CK(cudaGetLastError());
+            int first = 0;
+            CK(cudaMemcpyAsync(&first, la.first, sizeof(int), cudaMemcpyDeviceToHost, st_));
+            int pfail = 0;
+            if (bounded) CK(cudaMemcpyAsync(&pfail, la.fail, sizeof(int), cudaMemcpyDeviceToHost, st_));
+            CK(cudaStreamSynchronize(st_));
+            if (bounded) ++(pfail ? la_price_exact_ : la_price_bounded_);
+            if (dbg_trace_) {
+                std::vector<int> bjh(K), okh(K);
+                int np = 0;
+                CK(cudaMemcpy(bjh.data(), la.bj, sizeof(int) * K, cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(okh.data(), la.ok, sizeof(int) * K, cudaMemcpyDeviceToHost));
+                int unc_hi = 0, unc_lo = 0;
+                for (int k = 0; k < K; ++k)
+                    if (bjh[k] >= 0 && !okh[k]) (bjh[k] >= n_total_ - m ? unc_hi : unc_lo)++;
+                fprintf(stderr, "[solver r%d]   uncertified: %d with best_j in the last m columns, %d below\n", rank_,
+                        unc_hi, unc_lo);
+                CK(cudaMemcpy(&np, la.nprow, sizeof(int), cudaMemcpyDeviceToHost));
+                std::sort(bjh.begin(), bjh.end());
+                const long distinct = std::unique(bjh.begin(), bjh.end()) - bjh.begin();
+                std::vector<double> bb(m);
+                CK(cudaMemcpy(bb.data(), d_.T + (size_t)m * d_.ldT, sizeof(double) * m, cudaMemcpyDeviceToHost));
+                np = (int)std::count_if(bb.begin(), bb.end(), [](double v) { return v <= 0.0; });
+                fprintf(stderr, "[solver r%d] bounded selection K=%d: %d uncertified, first %s, %ld distinct best_j, %d rows with b_bar <= 0\n",
+                        rank_, K, first == 1 ? 0 : (-first - 1) / 2,
+                        first != 1 && ((-first - 1) & 1) ? "not provably 0" : "ok", distinct, np);
+            }
+            void* pb[] = {la.prow, la.nprow, la.Tg, la.ok, la.clist, la.ncl, la.first};
+            for (void* p : pb) CK(cudaFreeAsync(p, st_));
+            if (first == 1) {
+                ++la_bounded_;
+                *first_proven = true;
+                free_la(la, rows_d);
+                return;
+            }
+            ++la_full_;
+        } else if (first_proven) {
+            ++la_full_;
+        }
         if (tiled_) {
             // Case 2: theta' per partition (resident first), merged by the exact min of la_score
             for (int k = 0; k < P; ++k) {
@@ -1224,10 +1315,18 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
         }
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(scores.data() + k0, la.score, sizeof(double) * la.K, cudaMemcpyDeviceToHost, st_));
+        int pfail = 0;
+        if (bounded) CK(cudaMemcpyAsync(&pfail, la.fail, sizeof(int), cudaMemcpyDeviceToHost, st_));
         CK(cudaStreamSynchronize(st_));
+        if (bounded) ++(pfail ? la_price_exact_ : la_price_bounded_);
     }
+    free_la(la, rows_d);
+}
+
+void Solver::free_la(LookaheadDev& la, int* rows_d) {
     void* bufs[] = {rows_d, la.X, la.Wp, la.bz, la.bj, la.theta, la.score, la.part_z, la.part_j, la.part_t,
-                    la.pm, la.pm_all, la.tl, la.tl_all, la.own_t, la.nonfinite};
+                    la.pm, la.pm_all, la.tl, la.tl_all, la.own_t, la.nonfinite, la.wnorm, la.ztil, la.part_L,
+                    la.cj, la.cz, la.cn, la.pairs, la.npairs, la.fail};
     for (void* p : bufs)
         if (p) CK(cudaFreeAsync(p, st_));
 }
@@ -2106,6 +2205,16 @@ int lpsg_reinvert_stats(lpsg_solver* s, long* rebuilds, long* steps, double* res
     if (residual_before) *residual_before = s->s->reinv_res_before;
     if (residual_after) *residual_after = s->s->reinv_res_after;
     if (seconds) *seconds = s->s->reinv_seconds;
+    return LPSG_OK;
+}
+
+int lpsg_lookahead_stats(lpsg_solver* s, long long* bounded, long long* full, long long* price_bounded,
+                         long long* price_exact) {
+    if (!s) return bad("lpsg_lookahead_stats: null solver");
+    if (bounded) *bounded = s->s->la_bounded_;
+    if (full) *full = s->s->la_full_;
+    if (price_bounded) *price_bounded = s->s->la_price_bounded_;
+    if (price_exact) *price_exact = s->s->la_price_exact_;
     return LPSG_OK;
 }
 

@@ -106,6 +106,9 @@ class SolverConfig:
     # verification modes, result-identical to the default (tests/test_gpu_parity.py):
     unfused_ratio: bool = False           # standalone ratio-test kernel, not the fused epilogue
     lookahead_exact_select: bool = False  # theta' keeps the y_i == 0 select
+    # select_leaving's bounded selection: "auto" from 16
+    # survivors up, "always" on every tie (verification), "off" (A/B)
+    lookahead_bound: str = "auto"
     # opt-in periodic reinversion on the device (NOT bit-identical to the
     # reference; include/lpsg.h lpsg_config.reinvert_every): 0 = off
     reinvert_every: int = 0
@@ -128,8 +131,11 @@ class SolverConfig:
         c.memory_budget = int(self.memory_budget)
         # (tools/dbg set `_experiment` on an instance; it only has an effect in
         # the -DLPSG_EXPERIMENTS library, LPSG_EXPERIMENTS_LIB=1)
+        if self.lookahead_bound not in ("auto", "always", "off"):
+            raise Error(f"lookahead_bound must be auto, always or off, got {self.lookahead_bound!r}")
         c.reserved[2] = (16 if self.lookahead_exact_select else 0) | (
-            int(getattr(self, "_experiment", 0)) & ~16)
+            {"auto": 0, "always": 32, "off": 64}[self.lookahead_bound]) | (
+            int(getattr(self, "_experiment", 0)) & ~(16 | 32 | 64))
         if self.nccl_id:
             if len(self.nccl_id) != 128:
                 raise Error("nccl_id must be 128 bytes")
@@ -366,6 +372,14 @@ class SimplexSolver:
                                             C.byref(r1), C.byref(t)))
         return dict(rebuilds=n.value, steps=k.value, residual_before=r0.value,
                     residual_after=r1.value, seconds=t.value)
+
+    def lookahead_stats(self) -> dict:
+        """select_leaving's lookaheads settled by the bounded selection vs scored
+        in full; lookahead pricings settled by the DFMA screen vs the exact GEMM
+        (include/lpsg.h lpsg_lookahead_stats)."""
+        v = [C.c_longlong() for _ in range(4)]
+        _check(self.lib.lpsg_lookahead_stats(self._h, *[C.byref(x) for x in v]))
+        return dict(zip(("bounded", "full", "price_bounded", "price_exact"), (x.value for x in v)))
 
     def memory(self) -> dict:
         """SolveReport::memory counterpart (include/lpsg.h lpsg_memory)."""

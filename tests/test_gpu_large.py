@@ -78,7 +78,31 @@ def test_large_single_gpu(name):
         s.keep_trace(True)
         rep = s.solve()
         tr = s.trace()
+        st = s.lookahead_stats()
     _check(z, rep, tr, name)
+    if name.startswith("c4"):
+        # every C4 pivot is a ~1000-way degenerate tie whose scores are all 0:
+        # the bounded selection settles each one without the theta' GEMM, and
+        # the DFMA screen settles the pricing without the exact GEMM
+        assert st["bounded"] > 0 and st["full"] == 0, st
+        assert st["price_bounded"] > 0, st
+
+
+@pytest.mark.parametrize("name", [n for n in NAMES if n.startswith("c4")])
+def test_large_c4_full_scoring(name):
+    """The C4 prefixes with the bounded selection and pricing off: every tie
+    scored by the full batched lookahead (both exact GEMMs), the same pivots bit
+    for bit."""
+    P = _P()
+    z, lp = _load(name)
+    with P.SimplexSolver(lp, P.SolverConfig(max_iter=int(z["cfg_max_iter"]),
+                                            lookahead_bound="off")) as s:
+        s.keep_trace(True)
+        rep = s.solve()
+        tr = s.trace()
+        st = s.lookahead_stats()
+    _check(z, rep, tr, (name, "off"))
+    assert st["bounded"] == 0 and st["full"] > 0 and st["price_bounded"] == 0 and st["price_exact"] == 0, st
 
 
 @pytest.mark.parametrize("shards", [2, 4, 8])

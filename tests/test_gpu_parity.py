@@ -89,6 +89,50 @@ def test_lookahead_exact_select_path(name):
     assert np.array_equal(_bits(rep.x), _bits(g.x)), name
 
 
+@pytest.mark.parametrize("name", NAMES)
+def test_bounded_selection_always_same_pivots(name):
+    """select_leaving's bounded selection (a probe that proves every later
+    survivor's score <= the first one's +-0) tried on EVERY tie
+    of >= 2 survivors instead of from 16 up: the pivots, x and objective stay
+    the reference's, bit for bit, whether the probe settles a tie or falls back
+    to full scoring."""
+    P = _P()
+    g = Golden(name)
+    with P.SimplexSolver(_golden_lp(g), P.SolverConfig(
+            max_iter=g.max_iter, pivot_tol=g.pivot_tol, kernel=g.kernel,
+            anticycle=P.Anticycle(g.anticycle), lookahead_bound="always")) as s:
+        s.keep_trace(True)
+        rep = s.solve()
+        tr = s.trace()
+        st = s.lookahead_stats()
+    assert int(rep.status) == g.status, (name, rep.status, g.status)
+    _assert_trace(tr, g.trace[: g.trace_len], name)
+    assert np.array_equal(_bits(rep.x), _bits(g.x)), name
+    if g.anticycle == int(P.Anticycle.none):
+        assert not any(st.values()), (name, st)
+
+
+def test_bounded_selection_both_branches_run():
+    """Across the tie fixtures the probe both settles ties and falls back, the
+    bounded pricing (DFMA screen + exact chains) settles pricings (so the test
+    above exercises those branches), and "off" tries neither."""
+    P = _P()
+    tot = dict(bounded=0, full=0, price_bounded=0, price_exact=0)
+    for name in [n for n in NAMES if "_f2_" in n or n.startswith(("beale", "netlib"))]:
+        g = Golden(name)
+        for mode in ("always", "off"):
+            with P.SimplexSolver(_golden_lp(g), P.SolverConfig(
+                    max_iter=g.max_iter, pivot_tol=g.pivot_tol, kernel=g.kernel,
+                    anticycle=P.Anticycle(g.anticycle), lookahead_bound=mode)) as s:
+                s.solve()
+                st = s.lookahead_stats()
+            if mode == "off":
+                assert st["bounded"] == 0 and st["price_bounded"] == 0 and st["price_exact"] == 0, (name, st)
+            else:
+                tot = {k: tot[k] + st[k] for k in tot}
+    assert tot["bounded"] > 0 and tot["full"] > 0 and tot["price_bounded"] > 0, tot
+
+
 @pytest.mark.parametrize("rows,cols,form,seed", [
     (48, 80, 0, 11), (48, 80, 1, 12), (48, 80, 2, 13), (150, 300, 0, 21), (150, 300, 2, 22),
     (333, 500, 1, 31), (300, 450, 2, 32), (513, 700, 0, 33), (1, 3, 0, 4), (2, 2, 1, 5),

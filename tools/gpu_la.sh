@@ -2,7 +2,7 @@
 set -x
 mkdir -p gpurun_out
 TAG=${TAG:-la}
-timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_sharded.py -q -x --timeout 600 -p no:cacheprovider -k "f2 or beale or lookahead or netlib" > gpurun_out/pt_la_$TAG.log 2>&1
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_sharded.py -q -x --timeout 600 -p no:cacheprovider -k "f2 or beale or lookahead or netlib or bounded" > gpurun_out/pt_la_$TAG.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pt_la_$TAG.log
 timeout 1200 python -m pytest tests/test_gpu_large.py tests/test_gpu_tiled.py -q --timeout 900 -p no:cacheprovider -k "c4 or tiled" > gpurun_out/pt_la_large_$TAG.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pt_la_large_$TAG.log

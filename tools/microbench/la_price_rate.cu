@@ -144,7 +144,7 @@ struct SmemT {
     double A[kLS][kLC][kLN];  // [i][s]
     uint64_t full[kLS];
 };
-template <int PAIR>
+template <int PAIR, bool FMA = false, bool VOUT = false>
 __global__ void __launch_bounds__(kLThreads, 2)
 k_price_tma(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA, int K, int m, double* out) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -190,14 +190,27 @@ k_price_tma(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
                     a0[v] = sm.A[stg][ii][ts + 32 * v];
                     a1[v] = sm.A[stg][ii + 1][ts + 32 * v];
                 }
+                if (VOUT) {
+#pragma unroll
+                    for (int v = 0; v < 4; ++v)
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) acc[u][v] = __fma_rn(w0[u], a0[v], acc[u][v]);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v)
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) acc[u][v] = __fma_rn(w1[u], a1[v], acc[u][v]);
+                } else {
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) acc[u][v] = xadd(acc[u][v], xmul(w0[u], a0[v]));
+                    for (int v = 0; v < 4; ++v)
+                        acc[u][v] = FMA ? __fma_rn(w0[u], a0[v], acc[u][v]) : xadd(acc[u][v], xmul(w0[u], a0[v]));
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) acc[u][v] = xadd(acc[u][v], xmul(w1[u], a1[v]));
+                    for (int v = 0; v < 4; ++v)
+                        acc[u][v] = FMA ? __fma_rn(w1[u], a1[v], acc[u][v]) : xadd(acc[u][v], xmul(w1[u], a1[v]));
+                }
             };
             if (lim == kLC) {
 #pragma unroll
@@ -232,7 +245,7 @@ k_price_tma(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUt
 }
 
 static bool encode_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
-                      uint32_t box_inner, uint32_t box_outer) {
+                      uint32_t box_inner, uint32_t box_outer, bool swz = false) {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess || !p) return false;
@@ -245,10 +258,81 @@ static bool encode_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64
     const cuuint32_t box[2] = {box_inner, box_outer};
     const cuuint32_t estr[2] = {1, 1};
     return fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, swz ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// ---- DMMA form (mma.sync m8n8k4 f64): 8 warps = 2 candidate halves x 4 slot
+// quarters, 32 x 32 outputs per warp (4 x 4 fragments); W' box 128B-swizzled.
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                 : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
+}
+struct SmemD {
+    double W[kLS][kLK][kLC];  // [k][i], 128B-swizzled rows
+    double A[kLS][kLC][kLN];  // [i][s]
+    uint64_t full[kLS];
+};
+__global__ void __launch_bounds__(kLThreads, 2)
+k_price_dmma(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA, int K, int m, double* out) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    SmemD& sm = *reinterpret_cast<SmemD*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int s0 = blockIdx.x * kLN, k0 = blockIdx.y * kLK;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31, g = lane >> 2, tq = lane & 3;
+    const int wc = warp & 1, ws = warp >> 1;
+    if (t == 0) {
+        for (int s = 0; s < kLS; ++s) mbar_init(&sm.full[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    double acc[4][4][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    constexpr uint32_t kBytes = (kLK * kLC + kLC * kLN) * 8;
+    auto issue = [&](int stage, int i0) {
+        mbar_expect_tx(&sm.full[stage], kBytes);
+        tma_load_2d(&sm.W[stage][0][0], &tmW, i0, k0, &sm.full[stage]);
+        tma_load_2d(&sm.A[stage][0][0], &tmA, s0, i0, &sm.full[stage]);
+    };
+    const int nch = (m + kLC - 1) / kLC;
+    if (t == 0)
+        for (int st = 0; st < kLS - 1 && st < nch; ++st) issue(st, st * kLC);
+    for (int ch = 0; ch < nch; ++ch) {
+        __syncthreads();
+        if (t == 0 && ch + kLS - 1 < nch) issue((ch + kLS - 1) % kLS, (ch + kLS - 1) * kLC);
+        const int stg = ch % kLS;
+        mbar_wait(&sm.full[stg], (ch / kLS) & 1);
+        const double* Ws = &sm.W[stg][0][0];
+#pragma unroll
+        for (int kk = 0; kk < kLC / 4; ++kk) {
+            const int e = kk * 4 + tq;
+            double af[4], bf[4];
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb) {
+                const int r = wc * 32 + cb * 8 + g;
+                af[cb] = Ws[r * kLC + ((((e >> 1) ^ (r & 7)) << 1) | (e & 1))];
+            }
+#pragma unroll
+            for (int sb = 0; sb < 4; ++sb) bf[sb] = sm.A[stg][e][ws * 32 + sb * 8 + g];
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb)
+#pragma unroll
+                for (int sb = 0; sb < 4; ++sb) dmma(acc[cb][sb], af[cb], bf[sb]);
+        }
+    }
+    double sum = 0.0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) sum += acc[a][b][0] + acc[a][b][1];
+    out[((size_t)blockIdx.y * gridDim.x + blockIdx.x) * kLThreads + t] = sum;
+}
+
+static bool encode_2d(CUtensorMap* out, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch_bytes,
+                      uint32_t box_inner, uint32_t box_outer, bool swz);
 int main() {
     const int m = 4000, K = 1000;
     const int nmax = 8064;
@@ -301,13 +385,17 @@ int main() {
     }
     cudaFuncSetAttribute(k_price_tma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemT));
     cudaFuncSetAttribute(k_price_tma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemT));
-    for (int pair = 0; pair < 2; ++pair)
+    cudaFuncSetAttribute(k_price_tma<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemT));
+    cudaFuncSetAttribute(k_price_tma<1, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemT));
+    for (int pair = 0; pair < 4; ++pair)
     for (const Case& c : cases) {
         dim3 grid((c.n_scan + kLN - 1) / kLN, c.kgrid);
         float best = 1e30f;
         for (int rep = 0; rep < 5; ++rep) {
             cudaEventRecord(e0);
-            if (pair) k_price_tma<1><<<grid, kLThreads, sizeof(SmemT)>>>(tmW, tmA, K, m, out);
+            if (pair == 3) k_price_tma<1, true, true><<<grid, kLThreads, sizeof(SmemT)>>>(tmW, tmA, K, m, out);
+            else if (pair == 2) k_price_tma<1, true><<<grid, kLThreads, sizeof(SmemT)>>>(tmW, tmA, K, m, out);
+            else if (pair) k_price_tma<1><<<grid, kLThreads, sizeof(SmemT)>>>(tmW, tmA, K, m, out);
             else k_price_tma<0><<<grid, kLThreads, sizeof(SmemT)>>>(tmW, tmA, K, m, out);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
@@ -316,8 +404,29 @@ int main() {
             if (ms < best) best = ms;
         }
         const double inst = 2.0 * m * (double)grid.x * kLN * grid.y * kLK;
-        printf("%-13s %-30s %.3f ms  %.2f T fp64 instr/s = %.3f of 18.5\n", pair ? "TMA pairs" : "TMA", c.name, best,
-               inst / (best * 1e-3) / 1e12, inst / (best * 1e-3) / 18.5e12);
+        const double in2 = pair >= 2 ? inst / 2 : inst;  // DFMA: one instruction per multiply-add
+        printf("%-13s %-30s %.3f ms  %.2f T fp64 instr/s = %.3f of 18.5\n",
+               pair == 3 ? "TMA DFMA v-out" : pair == 2 ? "TMA DFMA" : pair ? "TMA pairs" : "TMA", c.name, best,
+               in2 / (best * 1e-3) / 1e12, in2 / (best * 1e-3) / 18.5e12);
+    }
+    CUtensorMap tmWs;
+    if (!encode_2d(&tmWs, Wp, m, K, ldx * 8, kLC, kLK, true)) { printf("encode swz failed\n"); return 1; }
+    cudaFuncSetAttribute(k_price_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemD) + 1024);
+    for (const Case& c : cases) {
+        dim3 grid((c.n_scan + kLN - 1) / kLN, c.kgrid);
+        float best = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            cudaEventRecord(e0);
+            k_price_dmma<<<grid, kLThreads, sizeof(SmemD) + 1024>>>(tmWs, tmA, K, m, out);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            float ms;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (ms < best) best = ms;
+        }
+        const double fl = 2.0 * m * (double)grid.x * kLN * grid.y * kLK;
+        printf("%-13s %-30s %.3f ms  %.2f TFLOP/s = %.3f of 37.1 (DMMA)\n", "DMMA", c.name, best,
+               fl / (best * 1e-3) / 1e12, fl / (best * 1e-3) / 37.1e12);
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
     return 0;
