@@ -14,6 +14,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 for k in k_update k_price k_pivot; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 40 -c 1 -o gpurun_out/prof_${k}_$TAG python bench.py --steps 60 --warmup 20 --no-cpu-baseline --e2e-max-iter 5 --no-profile --no-reinversion > gpurun_out/ncu_${k}_$TAG.log 2>&1
 done
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_la_screen|k_la_probe$" -s 2 -c 2 -o gpurun_out/prof_c4_$TAG python bench.py --config c4 --steps 4 --warmup 3 --no-cpu-baseline --e2e-max-iter 2 --no-profile --no-reinversion > gpurun_out/ncu_c4_$TAG.log 2>&1
 timeout 3600 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 1500 --durations=25 > gpurun_out/pytest_gpu_$TAG.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pytest_gpu_$TAG.log
 timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1
