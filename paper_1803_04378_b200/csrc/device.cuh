@@ -258,13 +258,19 @@ struct LookaheadDev {
     int* clist;       // candidates still unproven (ascending), for the next probe round
     int* ncl;         // how many
     int* first;       // 1: the first candidate is provably chosen
+    double* yacc;     // K x 128: the probe screen's y~ partial sums (atomic)
+    double* pxb;      // K: X_k . B_k
+    double* pxn;      // K: ||X_k||
+    double* pbn;      // K: ||B_k||
+    double* ptn;      // 128: ||T_i|| of the screened probe rows
     // bounded pricing (k_la_gemm_price<true> + k_la_cands/k_la_exact): z~ by
     // any-order DFMA with a rigorous error bound, exact chains only where the
     // bound cannot exclude the argmax
     const double* anorm;  // n_total: ||a_j||_2 of the original columns
     double* wnorm;    // K: ||W'_k||_2
-    double* ztil;     // K x ldz: z~_k(s)
-    long long ldz;
+    int* tl_s;        // K x tiles x kLaTile: slots whose interval reaches the tile's bound
+    double* tl_z;     // their z~
+    int* tl_n;        // K x tiles: how many
     double* part_L;   // K x nblk: per-tile max lower bound
     int* cj;          // K x kLaCand: columns whose interval reaches the best lower bound
     int* cn;          // K: how many (> kLaCand: overflow -> exact GEMM)
@@ -274,6 +280,7 @@ struct LookaheadDev {
     int* fail;        // 1: some bound unusable (non-finite, list overflow): run the exact GEMM
 };
 constexpr int kLaCand = 8;         // exact candidates per lookahead candidate
+constexpr int kLaTile = 4;         // screen survivors kept per (candidate, 128-slot tile)
 constexpr int kLaPairs = 1 << 14;  // exact chains per batch
 constexpr int kLaProbeRound = 64;                     // probe rows per round
 constexpr int kLaProbeRounds = 6;                     // rounds before falling back to full scoring
@@ -313,7 +320,8 @@ void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int 
 bool launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st);
 // select_leaving's bounded path (unsharded, in-core): la.first = 1 when the
 // first candidate provably wins ("bounded selection")
-void launch_la_probe(const Dev& d, LookaheadDev& la, cudaStream_t st);
+bool launch_la_probe(const Dev& d, LookaheadDev& la, cudaStream_t st);
+void launch_la_probe_rounds(const Dev& d, LookaheadDev& la, cudaStream_t st);  // when la.ncl > 0
 void launch_la_score(const Dev& d, LookaheadDev& la, const double* tl, int nsrc, cudaStream_t st);
 // in-process shard exchange helpers (LocalComm): out[k] = sum_g in[g*n + k] / min_g
 void launch_sum_i64(const long long* in, int nsrc, size_t n, long long* out, cudaStream_t st);

@@ -2013,7 +2013,8 @@ k_la_gemm_theta(Dev d, LookaheadDev la, const __grid_constant__ CUtensorMap tmT,
 // flushed subnormals). The tile is pricing's 64 candidates x 128 slots; 8
 // warps = 2 candidate halves x 4 slot quarters, 32 x 32 outputs per warp as
 // 4 x 4 fragments; W' boxes land 128B-swizzled (conflict-free A fragments).
-// Per tile and candidate it keeps max(z~ - E) -> part_L; z~ -> ztil.
+// Per tile and candidate it keeps max(z~ - E) -> part_L, and the few slots
+// whose interval reaches that tile bound -> tl_s / tl_z.
 // tools/microbench/la_price_rate.cu: 0.83 of the 37 TFLOP/s DMMA peak, against
 // 0.69 for the same screen as SIMT DFMA.
 __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
@@ -2026,14 +2027,23 @@ struct LaScreenSmem {
     double A[kLS][kLC][kLN];  // [i][s]
     uint64_t full[kLS];
     double lo[kLK][4];        // per candidate x slot quarter
+    int cnt[kLK];             // tile list: slots that may reach the candidate's global bound
+    int cs[kLK][kLaTile];
+    double cz[kLK][kLaTile];
 };
+//
+// PROBE (the bounded selection's screen): the same tiles over a_{b_k} (in W''s
+// buffer) x the gathered probe rows Tg (128 of them), split along the
+// reduction over gridDim.z segments whose partial dots are atomically added
+// into la.yacc (any order is fine for a screen); k_la_probe_cert bounds them.
+template <bool PROBE>
 __global__ void __launch_bounds__(kLThreads, 2)
 k_la_screen(Dev d, LookaheadDev la, const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA) {
     extern __shared__ __align__(1024) unsigned char la_smem[];
     LaScreenSmem& sm =
         *reinterpret_cast<LaScreenSmem*>((reinterpret_cast<uintptr_t>(la_smem) + 1023) & ~uintptr_t(1023));
-    const int n_scan = d.ctl->n_scan;
-    const double* cost = phase_cost(d, d.ctl->phase);
+    const int n_scan = PROBE ? 0 : d.ctl->n_scan;
+    const double* cost = PROBE ? nullptr : phase_cost(d, d.ctl->phase);
     const int s0 = blockIdx.x * kLN, k0 = blockIdx.y * kLK;
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31, g = lane >> 2, tq = lane & 3;
     const int wc = warp & 1, ws = warp >> 1;
@@ -2054,12 +2064,16 @@ k_la_screen(Dev d, LookaheadDev la, const __grid_constant__ CUtensorMap tmW, con
         tma_load_2d(&sm.W[stage][0][0], &tmW, i0, k0, &sm.full[stage]);
         tma_load_2d(&sm.A[stage][0][0], &tmA, s0, i0, &sm.full[stage]);
     };
-    const int nch = (m + kLC - 1) / kLC;  // a partial last chunk is zero-filled by TMA
+    // chunks [c0, c0 + nch) of the reduction (a partial last chunk is zero-filled by TMA)
+    const int nall = (m + kLC - 1) / kLC;
+    const int per = (nall + gridDim.z - 1) / gridDim.z;
+    const int c0 = blockIdx.z * per;
+    const int nch = max(0, min(per, nall - c0));
     if (t == 0)
-        for (int st = 0; st < kLS - 1 && st < nch; ++st) issue(st, st * kLC);
+        for (int st = 0; st < kLS - 1 && st < nch; ++st) issue(st, (c0 + st) * kLC);
     for (int ch = 0; ch < nch; ++ch) {
         __syncthreads();  // every thread is done with chunk ch - 1: its stage takes chunk ch + 2
-        if (t == 0 && ch + kLS - 1 < nch) issue((ch + kLS - 1) % kLS, (ch + kLS - 1) * kLC);
+        if (t == 0 && ch + kLS - 1 < nch) issue((ch + kLS - 1) % kLS, (c0 + ch + kLS - 1) * kLC);
         const int stg = ch % kLS;
         mbar_wait(&sm.full[stg], (uint32_t)(ch / kLS) & 1u);
         const double* Ws = &sm.W[stg][0][0];
@@ -2080,6 +2094,20 @@ k_la_screen(Dev d, LookaheadDev la, const __grid_constant__ CUtensorMap tmW, con
                 for (int sb = 0; sb < 4; ++sb) dmma_8x8x4(acc[cb][sb], af[cb], bf[sb]);
         }
     }
+    if (PROBE) {
+        if (nch == 0) return;
+#pragma unroll
+        for (int cb = 0; cb < 4; ++cb) {
+            const int k = k0 + wc * 32 + cb * 8 + g;
+            if (k >= la.K) continue;
+#pragma unroll
+            for (int sb = 0; sb < 4; ++sb)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) atomicAdd(la.yacc + (size_t)k * kLN + ws * 32 + sb * 8 + 2 * tq + h,
+                                                      acc[cb][sb][h]);
+        }
+        return;
+    }
     const double uu = 1.1102230246251565e-16;
     const double cE = 3.0 * (m * uu / (1.0 - m * uu)) * (1.0 + 1e-6);
     bool bad = false;
@@ -2098,19 +2126,59 @@ k_la_screen(Dev d, LookaheadDev la, const __grid_constant__ CUtensorMap tmW, con
                     const double z = acc[cb][sb][h] - cost[j];
                     const double e = cE * wn * la.anorm[j] + 4.0 * uu * fabs(z) + 1e-300;
                     bad |= !isfinite(z) || !isfinite(e);
-                    la.ztil[(size_t)k * la.ldz + sl] = z;
+                    acc[cb][sb][h] = j != la.q ? z : -kInf;  // keep z~ (and e below) for the tile list
                     if (j != la.q) lo = fmax(lo, z - e);
+                } else {
+                    acc[cb][sb][h] = -kInf;
                 }
             }
         lo = fmax(lo, __shfl_xor_sync(0xffffffffu, lo, 1));
         lo = fmax(lo, __shfl_xor_sync(0xffffffffu, lo, 2));
         if (tq == 0) sm.lo[kl][ws] = lo;
+        if (t < kLK) sm.cnt[t] = 0;
     }
     if (bad) *la.fail = 1;
     __syncthreads();
-    if (t < kLK && k0 + t < la.K)
-        la.part_L[(size_t)(k0 + t) * la.nblk + blockIdx.x] =
+    // The tile's own best lower bound L_t <= the global L_k, so a slot with
+    // z~ + E < L_t can never enter k_la_cands' list: only the few others are
+    // kept (slot, z~), kLaTile per (candidate, tile); more sets la.fail.
+#pragma unroll
+    for (int cb = 0; cb < 4; ++cb) {
+        const int kl = wc * 32 + cb * 8 + g, k = k0 + kl;
+        if (k >= la.K) continue;
+        const double Lt = fmax(fmax(sm.lo[kl][0], sm.lo[kl][1]), fmax(sm.lo[kl][2], sm.lo[kl][3]));
+        const double wn = la.wnorm[k];
+#pragma unroll
+        for (int sb = 0; sb < 4; ++sb)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const double z = acc[cb][sb][h];
+                if (z == -kInf) continue;
+                const int sl = s0 + ws * 32 + sb * 8 + 2 * tq + h;
+                const double e = cE * wn * la.anorm[d.slot2col[sl]] + 4.0 * uu * fabs(z) + 1e-300;
+                if (z + e >= Lt) {
+                    const int c = atomicAdd(&sm.cnt[kl], 1);
+                    if (c < kLaTile) {
+                        sm.cs[kl][c] = sl;
+                        sm.cz[kl][c] = z;
+                    }
+                }
+            }
+    }
+    __syncthreads();
+    if (t < kLK && k0 + t < la.K) {
+        const int k = k0 + t;
+        la.part_L[(size_t)k * la.nblk + blockIdx.x] =
             fmax(fmax(sm.lo[t][0], sm.lo[t][1]), fmax(sm.lo[t][2], sm.lo[t][3]));
+        const int n = sm.cnt[t];
+        if (n > kLaTile) *la.fail = 1;
+        const size_t base = ((size_t)k * (la.nblk - 1) + blockIdx.x) * kLaTile;
+        la.tl_n[(size_t)k * (la.nblk - 1) + blockIdx.x] = min(n, kLaTile);
+        for (int c = 0; c < min(n, kLaTile); ++c) {
+            la.tl_s[base + c] = sm.cs[t][c];
+            la.tl_z[base + c] = sm.cz[t][c];
+        }
+    }
 }
 
 // exact chains only where the screen is unsure:
@@ -2156,15 +2224,15 @@ __global__ void __launch_bounds__(256) k_la_cands(Dev d, LookaheadDev la) {
     __syncthreads();
     L = red[0];
     for (int v = 1; v < 8; ++v) L = fmax(L, red[v]);
-    const int n_scan = d.ctl->n_scan;
-    const double* cost = phase_cost(d, d.ctl->phase);
     const double uu = 1.1102230246251565e-16;
     const double cE = 3.0 * (d.m * uu / (1.0 - d.m * uu)) * (1.0 + 1e-6);
     const double wn = la.wnorm[k];
-    for (int sl = threadIdx.x; sl < n_scan; sl += blockDim.x) {
-        const int j = d.slot2col[sl];
-        if (j == la.q) continue;
-        const double z = la.ztil[(size_t)k * la.ldz + sl];
+    for (int e0 = threadIdx.x; e0 < ntile * kLaTile; e0 += blockDim.x) {  // the tiles' lists
+        const int b = e0 / kLaTile, c0 = e0 % kLaTile;
+        if (c0 >= la.tl_n[(size_t)k * ntile + b]) continue;
+        const size_t at = ((size_t)k * ntile + b) * kLaTile + c0;
+        const int j = d.slot2col[la.tl_s[at]];
+        const double z = la.tl_z[at];
         const double e = cE * wn * la.anorm[j] + 4.0 * uu * fabs(z) + 1e-300;
         if (z + e >= L) {
             const int c = atomicAdd(la.cn + k, 1);
@@ -2178,7 +2246,6 @@ __global__ void __launch_bounds__(256) k_la_cands(Dev d, LookaheadDev la) {
             else *la.fail = 1;
         }
     }
-    (void)cost;
 }
 
 // The listed (k, j): exact z = dot(W'_k, a_j) - c_j, the reference's chain
@@ -2271,6 +2338,80 @@ __global__ void k_la_probe_gather(Dev d, LookaheadDev la) {
         const size_t j = e / kLaProbe;
         la.Tg[e] = r < np ? d.T[j * d.ldT + la.prow[r]] : 0.0;
     }
+}
+
+// Screen inputs, any summation order: B_k = a_{b_k} gathered into W''s buffer
+// (as k_la_gather) with xb = X_k . B_k, ||X_k|| and ||B_k|| on the way (blocks
+// b < K, one per candidate), and ||T_i|| (j < m) of the screened probe rows
+// from their gathered columns (blocks K .. K + 127).
+__global__ void k_la_probe_norms(Dev d, LookaheadDev la) {
+    __shared__ double red[3][32];
+    const int b = blockIdx.x;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    if (b < la.K) {
+        const int c = la.bj[b];
+        const double* x = la.X + (size_t)b * la.ldx;
+        const double* a = c >= 0 ? d.A_cm + (size_t)c * d.ld_cm : nullptr;
+        double* out = la.Wp + (size_t)b * la.ldx;
+        for (int j = threadIdx.x; j < d.m; j += blockDim.x) {
+            const double w = a ? a[j] : 0.0, xv = x[j];
+            out[j] = w;
+            s0 = fma(xv, w, s0);
+            s1 = fma(xv, xv, s1);
+            s2 = fma(w, w, s2);
+        }
+    } else {  // probe row r = b - K: ||T_row|| from its gathered column
+        const int r = b - la.K;
+        for (int j = threadIdx.x; j < d.m; j += blockDim.x) {
+            const double v = la.Tg[(size_t)j * kLaProbe + r];
+            s1 = fma(v, v, s1);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) { red[0][w] = s0; red[1][w] = s1; red[2][w] = s2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double a = 0.0, c = 0.0, e = 0.0;
+        for (int v = 0; v < (int)(blockDim.x >> 5); ++v) { a += red[0][v]; c += red[1][v]; e += red[2][v]; }
+        if (b < la.K) {
+            la.pxb[b] = a;
+            la.pxn[b] = sqrt(c);
+            la.pbn[b] = sqrt(e);
+        } else {
+            la.ptn[b - la.K] = sqrt(c);
+        }
+    }
+}
+
+// Certificates from the screen (first kLN probe rows): y~ = yacc - y_i xb_k
+// differs from the reference's y'_ik by at most
+// E = (2 gamma_m + 5u)(1 + 1e-6)(||T_i|| + |y_i| ||X_k||) ||B_k|| + 2u|y~| + 1e-300
+// (the elementwise T'_ij = T_ij - y_i X_kj rounding, both dots' gamma_m, the
+// final subtraction; flushed subnormals in the absolute term). ok[k] = 1 when a
+// row i != r_k has rhs'_ik <= 0 (exact) and y~ - E > pivot_tol.
+__global__ void k_la_probe_cert(Dev d, LookaheadDev la) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = e / kLN, r = e % kLN;
+    if (k >= la.K || r >= *la.nprow || la.bj[k] < 0) return;
+    const int row = la.prow[r];
+    if (row == la.rows[k]) return;
+    const int m = d.m;
+    const double uu = 1.1102230246251565e-16;
+    const double gam = m * uu / (1.0 - m * uu);
+    const double y = d.Y[row];
+    const double yt = la.yacc[(size_t)k * kLN + r] - y * la.pxb[k];
+    const double E = (2.0 * gam + 5.0 * uu) * (1.0 + 1e-6) * (la.ptn[r] + fabs(y) * la.pxn[k]) * la.pbn[k] +
+                     2.0 * uu * fabs(yt) + 1e-300;
+    if (!isfinite(yt) || !isfinite(E)) return;
+    const double xm = la.X[(size_t)k * la.ldx + m];
+    const double bi = d.T[(size_t)m * d.ldT + row];
+    const double rhs = y == 0.0 ? bi : dsub(bi, dmul(y, xm));
+    if (rhs <= 0.0 && yt - E > d.pivot_tol) la.ok[k] = 1;
 }
 
 // candidates with a best column and no certificate yet, ascending (one CTA)
@@ -2607,7 +2748,8 @@ void configure_kernels(Dev& d) {
     cudaFuncSetAttribute(k_update, cudaFuncAttributeMaxDynamicSharedMemorySize, d.upd_smem);
     cudaFuncSetAttribute(k_price, cudaFuncAttributeMaxDynamicSharedMemorySize, d.price_smem);
     cudaFuncSetAttribute(k_la_gemm_price, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaPriceSmem));
-    cudaFuncSetAttribute(k_la_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaScreenSmem) + 1024);
+    cudaFuncSetAttribute(k_la_screen<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaScreenSmem) + 1024);
+    cudaFuncSetAttribute(k_la_screen<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaScreenSmem) + 1024);
     cudaFuncSetAttribute(k_la_gemm_theta, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LaThetaSmem));
     // One shared-memory carveout for every kernel: SMs never reconfigure the
     // L1/shared split between the streaming kernels and the small ones, and a
@@ -2620,7 +2762,7 @@ void configure_kernels(Dev& d) {
                          (const void*)k_pivot_row, (const void*)k_pivot, (const void*)k_gather_row,
                          (const void*)k_drive_scan, (const void*)k_drive_red, (const void*)k_la_x,
                          (const void*)k_la_wp, (const void*)k_la_price_local,
-                         (const void*)k_la_gemm_price, (const void*)k_la_screen, (const void*)k_la_gemm_theta, (const void*)k_la_leave,
+                         (const void*)k_la_gemm_price, (const void*)k_la_screen<false>, (const void*)k_la_screen<true>, (const void*)k_la_gemm_theta, (const void*)k_la_leave,
                          (const void*)k_la_own,
                          (const void*)k_la_decide, (const void*)k_la_theta_local,
                          (const void*)k_la_score, (const void*)k_sum_i64, (const void*)k_min_i32,
@@ -2721,7 +2863,7 @@ bool launch_la_price(const Dev& d, LookaheadDev& la, bool bounded, cudaStream_t 
         if (la.nblk > 1 &&
             !encode_2d(&tmWs, la.Wp, (uint64_t)d.m, (uint64_t)la.K, (uint64_t)la.ldx * 8, kLC, kLK, true))
             return false;
-        if (la.nblk > 1) k_la_screen<<<grid, kLThreads, sizeof(LaScreenSmem) + 1024, st>>>(d, la, tmWs, tmA);
+        if (la.nblk > 1) k_la_screen<false><<<grid, kLThreads, sizeof(LaScreenSmem) + 1024, st>>>(d, la, tmWs, tmA);
         k_la_leave<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
         k_la_cands<<<la.K, 256, 0, st>>>(d, la);
         k_la_exact<<<kLaPairs / kDC, kDT, 0, st>>>(d, la);
@@ -2758,15 +2900,33 @@ bool launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     return true;
 }
 
-void launch_la_probe(const Dev& d, LookaheadDev& la, cudaStream_t st) {
+bool launch_la_probe(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     cudaMemsetAsync(la.ok, 0, sizeof(int) * la.K, st);
     k_la_probe_rows<<<1, 1024, 0, st>>>(d, la);
-    k_la_gather<<<dim3((d.m + 255) / 256, la.K), 256, 0, st>>>(d, la);
     k_la_probe_gather<<<4 * 148, 256, 0, st>>>(d, la);
-    // rounds over further probe rows for the candidates still unproven; a
-    // round with nothing left exits at once
+    // DMMA screen of the first kLN probe rows for every candidate (split along
+    // the reduction to fill the GPU), then certificates from its error bound;
+    // the exact rounds below only see the candidates it leaves unproven
+    CUtensorMap tmB, tmT;
+    if (!encode_2d(&tmB, la.Wp, (uint64_t)d.m, (uint64_t)la.K, (uint64_t)la.ldx * 8, kLC, kLK, true) ||
+        !encode_2d(&tmT, la.Tg, (uint64_t)kLaProbe, (uint64_t)d.m, (uint64_t)kLaProbe * 8, kLN, kLC))
+        return false;
+    cudaMemsetAsync(la.yacc, 0, sizeof(double) * la.K * kLN, st);
+    k_la_probe_norms<<<la.K + kLN, 256, 0, st>>>(d, la);
+    const int ktiles = (la.K + kLK - 1) / kLK;
+    const int split = std::max(1, std::min((d.m + kLC - 1) / kLC, (2 * 148 + ktiles - 1) / ktiles));
+    k_la_screen<true><<<dim3(1, ktiles, split), kLThreads, sizeof(LaScreenSmem) + 1024, st>>>(d, la, tmB, tmT);
+    k_la_probe_cert<<<(la.K * kLN + 255) / 256, 256, 0, st>>>(d, la);
+    k_la_probe_list<<<1, 1024, 0, st>>>(la);  // la.ncl: candidates the screen left unproven
+    k_la_probe_decide<<<1, 1024, 0, st>>>(d, la);
+    return true;
+}
+
+// The exact rounds for the candidates the screen left unproven (the host runs
+// them only when la.ncl > 0): rows [64 r, 64 r + 64) of the probe set per round.
+void launch_la_probe_rounds(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     for (int r = 0; r < kLaProbeRounds; ++r) {
-        k_la_probe_list<<<1, 1024, 0, st>>>(la);
+        if (r) k_la_probe_list<<<1, 1024, 0, st>>>(la);
         k_la_probe<<<(la.K + kPKc - 1) / kPKc, 128, 0, st>>>(d, la, r);
     }
     k_la_probe_decide<<<1, 1024, 0, st>>>(d, la);

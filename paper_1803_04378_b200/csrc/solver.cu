@@ -1209,9 +1209,11 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
             launch_colnorm(d_, anorm_, st_);
         }
         la.anorm = anorm_;
-        la.ldz = round_up(std::max(1, hctl_->n_scan), 4);
+        const size_t nt = (size_t)kb * std::max(1, la.nblk - 1);
         la.wnorm = talloc<double>(kb, st_, pool_);
-        la.ztil = talloc<double>((size_t)kb * la.ldz, st_, pool_);
+        la.tl_s = talloc<int>(nt * kLaTile, st_, pool_);
+        la.tl_z = talloc<double>(nt * kLaTile, st_, pool_);
+        la.tl_n = talloc<int>(nt, st_, pool_);
         la.part_L = talloc<double>((size_t)kb * la.nblk, st_, pool_);
         la.cj = talloc<int>((size_t)kb * kLaCand, st_, pool_);
         la.cz = talloc<double>((size_t)kb * kLaCand, st_, pool_);
@@ -1254,15 +1256,27 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
             la.Tg = talloc<double>((size_t)m * kLaProbe, st_, pool_);
             la.ok = talloc<int>(K, st_, pool_);
             la.clist = talloc<int>(K, st_, pool_);
+            la.yacc = talloc<double>((size_t)K * 128, st_, pool_);
+            la.pxb = talloc<double>(K, st_, pool_);
+            la.pxn = talloc<double>(K, st_, pool_);
+            la.pbn = talloc<double>(K, st_, pool_);
+            la.ptn = talloc<double>(128, st_, pool_);
             la.ncl = talloc<int>(1, st_, pool_);
             la.first = talloc<int>(1, st_, pool_);
-            L(K_LA_THETA, 2.0 * kf * kLaProbeRound, [&] { launch_la_probe(d_, la, st_); });
+            L(K_LA_THETA, 2.0 * kf * kLaProbeRound, [&] { la_ok(launch_la_probe(d_, la, st_)); });
             CK(cudaGetLastError());
-            int first = 0;
+            int first = 0, ncl = 0;
             CK(cudaMemcpyAsync(&first, la.first, sizeof(int), cudaMemcpyDeviceToHost, st_));
+            CK(cudaMemcpyAsync(&ncl, la.ncl, sizeof(int), cudaMemcpyDeviceToHost, st_));
             int pfail = 0;
             if (bounded) CK(cudaMemcpyAsync(&pfail, la.fail, sizeof(int), cudaMemcpyDeviceToHost, st_));
             CK(cudaStreamSynchronize(st_));
+            if (first != 1 && ncl > 0) {  // the screen left candidates unproven: exact rounds
+                L(K_LA_THETA, 0.0, [&] { launch_la_probe_rounds(d_, la, st_); });
+                CK(cudaGetLastError());
+                CK(cudaMemcpyAsync(&first, la.first, sizeof(int), cudaMemcpyDeviceToHost, st_));
+                CK(cudaStreamSynchronize(st_));
+            }
             if (bounded) ++(pfail ? la_price_exact_ : la_price_bounded_);
             if (dbg_trace_) {
                 std::vector<int> bjh(K), okh(K);
@@ -1284,7 +1298,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
                         rank_, K, first == 1 ? 0 : (-first - 1) / 2,
                         first != 1 && ((-first - 1) & 1) ? "not provably 0" : "ok", distinct, np);
             }
-            void* pb[] = {la.prow, la.nprow, la.Tg, la.ok, la.clist, la.ncl, la.first};
+            void* pb[] = {la.prow, la.nprow, la.Tg, la.ok, la.clist, la.ncl, la.first, la.yacc, la.pxb, la.pxn, la.pbn, la.ptn};
             for (void* p : pb) CK(cudaFreeAsync(p, st_));
             if (first == 1) {
                 ++la_bounded_;
@@ -1325,7 +1339,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
 
 void Solver::free_la(LookaheadDev& la, int* rows_d) {
     void* bufs[] = {rows_d, la.X, la.Wp, la.bz, la.bj, la.theta, la.score, la.part_z, la.part_j, la.part_t,
-                    la.pm, la.pm_all, la.tl, la.tl_all, la.own_t, la.nonfinite, la.wnorm, la.ztil, la.part_L,
+                    la.pm, la.pm_all, la.tl, la.tl_all, la.own_t, la.nonfinite, la.wnorm, la.tl_s, la.tl_z, la.tl_n, la.part_L,
                     la.cj, la.cz, la.cn, la.pairs, la.npairs, la.fail};
     for (void* p : bufs)
         if (p) CK(cudaFreeAsync(p, st_));

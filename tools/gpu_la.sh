@@ -7,7 +7,7 @@ echo "pytest rc=$?" >> gpurun_out/pt_la_$TAG.log
 timeout 1200 python -m pytest tests/test_gpu_large.py tests/test_gpu_tiled.py -q --timeout 900 -p no:cacheprovider -k "c4 or tiled" > gpurun_out/pt_la_large_$TAG.log 2>&1
 echo "pytest rc=$?" >> gpurun_out/pt_la_large_$TAG.log
 timeout 900 python bench.py --config c4 --steps 60 --warmup 3 --no-cpu-baseline --e2e-max-iter 30 --no-reinversion > gpurun_out/bench_c4_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_la_gemm -s 2 -c 2 -o gpurun_out/prof_la_$TAG python bench.py --config c4 --steps 4 --warmup 3 --no-cpu-baseline --e2e-max-iter 2 --no-profile --no-reinversion > gpurun_out/ncu_la_$TAG.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_la_gemm|k_la_screen|k_la_probe" -s 0 -c 12 -o gpurun_out/prof_la_$TAG python bench.py --config c4 --steps 4 --warmup 3 --no-cpu-baseline --e2e-max-iter 2 --no-profile --no-reinversion > gpurun_out/ncu_la_$TAG.log 2>&1
 tail -n 3 gpurun_out/pt_la_$TAG.log; tail -n 3 gpurun_out/pt_la_large_$TAG.log
 python - <<PY
 import json
