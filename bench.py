@@ -585,7 +585,8 @@ def run_ours(args, cfg):
             "<= the first survivor's +-0; the theta' GEMM skipped) vs scored in full. "
             "price_bounded / price_exact: pricings settled by the DMMA screen with rigorous "
             "error bounds + exact chains for the columns it cannot exclude vs the exact GEMM "
-            "rerun. Decisions are the reference's either way (DESIGN.md §4)"))
+            "rerun. probe_rounds: selections whose DMMA probe screen left candidates for the "
+            "exact probe rounds. Decisions are the reference's either way (DESIGN.md §4)"))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         kc = min(K, cfg["cpu_pivots"])

@@ -217,9 +217,11 @@ int lpsg_reinvert_stats(lpsg_solver* s, long* rebuilds, long* steps, double* res
  * (solver.cpp:215-238, one GPU): how many the bounded selection settled (every
  * later score provably <= the first survivor's) and how many were scored in
  * full. All of them: how many pricings the DMMA screen + exact chains settled
- * and how many needed the exact GEMM after all. Results are identical either way. */
+ * and how many needed the exact GEMM after all; probe_rounds: selections whose
+ * DMMA probe screen left candidates for the exact probe rounds. Results are
+ * identical either way. */
 int lpsg_lookahead_stats(lpsg_solver* s, long long* bounded, long long* full, long long* price_bounded,
-                         long long* price_exact);
+                         long long* price_exact, long long* probe_rounds);
 
 /* ---- multi-GPU -------------------------
  * NCCL unique id for lpsg_config.nccl_id (rank 0 creates it, the caller

@@ -85,7 +85,7 @@ SIGNATURES = [
     ("lpsg_set_view_observer", C.c_int, [_P, VIEW_OBSERVER, _P, C.c_int]),
     ("lpsg_get_memory", C.c_int, [_P, C.POINTER(Memory)]),
     ("lpsg_reinvert_stats", C.c_int, [_P, C.POINTER(C.c_long), C.POINTER(C.c_long), _PD, _PD, _PD]),
-    ("lpsg_lookahead_stats", C.c_int, [_P] + [C.POINTER(C.c_longlong)] * 4),
+    ("lpsg_lookahead_stats", C.c_int, [_P] + [C.POINTER(C.c_longlong)] * 5),
     ("lpsg_get_trace", C.c_int, [_P, C.POINTER(Trace), C.c_long, C.POINTER(C.c_long)]),
     ("lpsg_price", C.c_int, [_P, _PI, _PI, _PD]),
     ("lpsg_compute_direction", C.c_int, [_P, C.c_int, C.c_double]),

@@ -165,6 +165,7 @@ public:
                    bool* first_proven = nullptr);
     long long la_bounded_ = 0, la_full_ = 0;  // select_leaving lookaheads: settled by the probe / fully scored
     long long la_price_bounded_ = 0, la_price_exact_ = 0;  // lookahead pricings: DMMA screen held / exact GEMM rerun
+    long long la_probe_rounds_ = 0;  // bounded selections that needed the exact probe rounds
     int la_bound_min_ = 16;                   // survivors from which the probe / bounded pricing are used
     double* anorm_ = nullptr;                 // ||a_j||_2 of A's columns (bounded pricing), made on first use
     void free_la(LookaheadDev& la, int* rows_d);
@@ -1272,6 +1273,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
             if (bounded) CK(cudaMemcpyAsync(&pfail, la.fail, sizeof(int), cudaMemcpyDeviceToHost, st_));
             CK(cudaStreamSynchronize(st_));
             if (first != 1 && ncl > 0) {  // the screen left candidates unproven: exact rounds
+                ++la_probe_rounds_;
                 L(K_LA_THETA, 0.0, [&] { launch_la_probe_rounds(d_, la, st_); });
                 CK(cudaGetLastError());
                 CK(cudaMemcpyAsync(&first, la.first, sizeof(int), cudaMemcpyDeviceToHost, st_));
@@ -2223,8 +2225,9 @@ int lpsg_reinvert_stats(lpsg_solver* s, long* rebuilds, long* steps, double* res
 }
 
 int lpsg_lookahead_stats(lpsg_solver* s, long long* bounded, long long* full, long long* price_bounded,
-                         long long* price_exact) {
+                         long long* price_exact, long long* probe_rounds) {
     if (!s) return bad("lpsg_lookahead_stats: null solver");
+    if (probe_rounds) *probe_rounds = s->s->la_probe_rounds_;
     if (bounded) *bounded = s->s->la_bounded_;
     if (full) *full = s->s->la_full_;
     if (price_bounded) *price_bounded = s->s->la_price_bounded_;

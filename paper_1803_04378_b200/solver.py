@@ -377,9 +377,10 @@ class SimplexSolver:
         """select_leaving's lookaheads settled by the bounded selection vs scored
         in full; lookahead pricings settled by the DFMA screen vs the exact GEMM
         (include/lpsg.h lpsg_lookahead_stats)."""
-        v = [C.c_longlong() for _ in range(4)]
+        v = [C.c_longlong() for _ in range(5)]
         _check(self.lib.lpsg_lookahead_stats(self._h, *[C.byref(x) for x in v]))
-        return dict(zip(("bounded", "full", "price_bounded", "price_exact"), (x.value for x in v)))
+        return dict(zip(("bounded", "full", "price_bounded", "price_exact", "probe_rounds"),
+                        (x.value for x in v)))
 
     def memory(self) -> dict:
         """SolveReport::memory counterpart (include/lpsg.h lpsg_memory)."""

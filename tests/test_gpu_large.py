@@ -103,6 +103,7 @@ def test_large_c4_full_scoring(name):
         st = s.lookahead_stats()
     _check(z, rep, tr, (name, "off"))
     assert st["bounded"] == 0 and st["full"] > 0 and st["price_bounded"] == 0 and st["price_exact"] == 0, st
+    assert st["probe_rounds"] == 0, st
 
 
 @pytest.mark.parametrize("shards", [2, 4, 8])
