@@ -2024,7 +2024,7 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
 }
 struct LaScreenSmem {
     double W[kLS][kLK][kLC];  // [k][i], rows 128B-swizzled by TMA
-    double A[kLS][kLC][kLN];  // [i][s]
+    double A[kLS][kLC][kLN];  // 8 boxes [i][16 s], rows 128B-swizzled (B fragments: 2-way, not 4-way)
     uint64_t full[kLS];
     double lo[kLK][4];        // per candidate x slot quarter
     int cnt[kLK];             // tile list: slots that may reach the candidate's global bound
@@ -2062,7 +2062,8 @@ k_la_screen(Dev d, LookaheadDev la, const __grid_constant__ CUtensorMap tmW, con
     auto issue = [&](int stage, int i0) {
         mbar_expect_tx(&sm.full[stage], kBytes);
         tma_load_2d(&sm.W[stage][0][0], &tmW, i0, k0, &sm.full[stage]);
-        tma_load_2d(&sm.A[stage][0][0], &tmA, s0, i0, &sm.full[stage]);
+        for (int b = 0; b < kLN / 16; ++b)  // 8 boxes of 16 slots x 16 rows, 128B-swizzled, 2 KB each
+            tma_load_2d(&sm.A[stage][0][0] + b * 16 * kLC, &tmA, s0 + 16 * b, i0, &sm.full[stage]);
     };
     // chunks [c0, c0 + nch) of the reduction (a partial last chunk is zero-filled by TMA)
     const int nall = (m + kLC - 1) / kLC;
@@ -2086,8 +2087,12 @@ k_la_screen(Dev d, LookaheadDev la, const __grid_constant__ CUtensorMap tmW, con
                 const int r = wc * 32 + cb * 8 + g;
                 af[cb] = Ws[r * kLC + ((((e >> 1) ^ (r & 7)) << 1) | (e & 1))];
             }
+            const double* As = &sm.A[stg][0][0];
 #pragma unroll
-            for (int sb = 0; sb < 4; ++sb) bf[sb] = sm.A[stg][e][ws * 32 + sb * 8 + g];  // B: row tq, column g
+            for (int sb = 0; sb < 4; ++sb) {  // B: row tq, column g, in box ws * 2 + sb / 2 (swizzled like W')
+                const int c = (sb & 1) * 8 + g;
+                bf[sb] = As[(ws * 2 + (sb >> 1)) * 16 * kLC + e * 16 + ((((c >> 1) ^ (e & 7)) << 1) | (c & 1))];
+            }
 #pragma unroll
             for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
@@ -2859,11 +2864,12 @@ bool launch_la_price(const Dev& d, LookaheadDev& la, bool bounded, cudaStream_t 
         cudaMemsetAsync(la.fail, 0, sizeof(int), st);
         cudaMemsetAsync(la.npairs, 0, sizeof(int), st);
         k_la_wnorm<<<la.K, 256, 0, st>>>(d, la);
-        CUtensorMap tmWs;
+        CUtensorMap tmWs, tmAs;
         if (la.nblk > 1 &&
-            !encode_2d(&tmWs, la.Wp, (uint64_t)d.m, (uint64_t)la.K, (uint64_t)la.ldx * 8, kLC, kLK, true))
+            (!encode_2d(&tmWs, la.Wp, (uint64_t)d.m, (uint64_t)la.K, (uint64_t)la.ldx * 8, kLC, kLK, true) ||
+             !encode_2d(&tmAs, d.A_nb, (uint64_t)d.ld_nb, (uint64_t)d.m, (uint64_t)d.ld_nb * 8, 16, kLC, true)))
             return false;
-        if (la.nblk > 1) k_la_screen<false><<<grid, kLThreads, sizeof(LaScreenSmem) + 1024, st>>>(d, la, tmWs, tmA);
+        if (la.nblk > 1) k_la_screen<false><<<grid, kLThreads, sizeof(LaScreenSmem) + 1024, st>>>(d, la, tmWs, tmAs);
         k_la_leave<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
         k_la_cands<<<la.K, 256, 0, st>>>(d, la);
         k_la_exact<<<kLaPairs / kDC, kDT, 0, st>>>(d, la);
@@ -2909,7 +2915,7 @@ bool launch_la_probe(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     // the exact rounds below only see the candidates it leaves unproven
     CUtensorMap tmB, tmT;
     if (!encode_2d(&tmB, la.Wp, (uint64_t)d.m, (uint64_t)la.K, (uint64_t)la.ldx * 8, kLC, kLK, true) ||
-        !encode_2d(&tmT, la.Tg, (uint64_t)kLaProbe, (uint64_t)d.m, (uint64_t)kLaProbe * 8, kLN, kLC))
+        !encode_2d(&tmT, la.Tg, (uint64_t)kLaProbe, (uint64_t)d.m, (uint64_t)kLaProbe * 8, 16, kLC, true))
         return false;
     cudaMemsetAsync(la.yacc, 0, sizeof(double) * la.K * kLN, st);
     k_la_probe_norms<<<la.K + kLN, 256, 0, st>>>(d, la);

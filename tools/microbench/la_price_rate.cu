@@ -269,11 +269,13 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                  : "+d"(c[0]), "+d"(c[1]) : "d"(a), "d"(b));
 }
+constexpr int kAP = kLN;  // (PAD variant: B stage as 8 swizzled 16-slot boxes)
 struct SmemD {
     double W[kLS][kLK][kLC];  // [k][i], 128B-swizzled rows
-    double A[kLS][kLC][kLN];  // [i][s]
+    double A[kLS][kLC][kAP];  // [i][s]
     uint64_t full[kLS];
 };
+template <bool PAD>
 __global__ void __launch_bounds__(kLThreads, 2)
 k_price_dmma(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmA, int K, int m, double* out) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -295,7 +297,10 @@ k_price_dmma(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CU
     auto issue = [&](int stage, int i0) {
         mbar_expect_tx(&sm.full[stage], kBytes);
         tma_load_2d(&sm.W[stage][0][0], &tmW, i0, k0, &sm.full[stage]);
-        tma_load_2d(&sm.A[stage][0][0], &tmA, s0, i0, &sm.full[stage]);
+        if (PAD)  // 8 boxes of 16 slots x 16 rows, 128B-swizzled, 2 KB each
+            for (int b = 0; b < kLN / 16; ++b) tma_load_2d(&sm.A[stage][0][0] + b * 256, &tmA, s0 + 16 * b, i0, &sm.full[stage]);
+        else
+            tma_load_2d(&sm.A[stage][0][0], &tmA, s0, i0, &sm.full[stage]);
     };
     const int nch = (m + kLC - 1) / kLC;
     if (t == 0)
@@ -316,7 +321,15 @@ k_price_dmma(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CU
                 af[cb] = Ws[r * kLC + ((((e >> 1) ^ (r & 7)) << 1) | (e & 1))];
             }
 #pragma unroll
-            for (int sb = 0; sb < 4; ++sb) bf[sb] = sm.A[stg][e][ws * 32 + sb * 8 + g];
+            const double* As = &sm.A[stg][0][0];
+            for (int sb = 0; sb < 4; ++sb) {
+                if (PAD) {
+                    const int c = (sb & 1) * 8 + g;
+                    bf[sb] = As[(ws * 2 + (sb >> 1)) * 256 + e * 16 + ((((c >> 1) ^ (e & 7)) << 1) | (c & 1))];
+                } else {
+                    bf[sb] = As[e * kLN + ws * 32 + sb * 8 + g];
+                }
+            }
 #pragma unroll
             for (int cb = 0; cb < 4; ++cb)
 #pragma unroll
@@ -409,15 +422,19 @@ int main() {
                pair == 3 ? "TMA DFMA v-out" : pair == 2 ? "TMA DFMA" : pair ? "TMA pairs" : "TMA", c.name, best,
                in2 / (best * 1e-3) / 1e12, in2 / (best * 1e-3) / 18.5e12);
     }
-    CUtensorMap tmWs;
+    CUtensorMap tmWs, tmA1;
     if (!encode_2d(&tmWs, Wp, m, K, ldx * 8, kLC, kLK, true)) { printf("encode swz failed\n"); return 1; }
-    cudaFuncSetAttribute(k_price_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemD) + 1024);
+    if (!encode_2d(&tmA1, A, ld_nb, m, ld_nb * 8, 16, kLC, true)) { printf("encode swzB failed\n"); return 1; }
+    cudaFuncSetAttribute(k_price_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemD) + 1024);
+    cudaFuncSetAttribute(k_price_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(SmemD) + 1024);
+    for (int pad = 0; pad < 2; ++pad)
     for (const Case& c : cases) {
         dim3 grid((c.n_scan + kLN - 1) / kLN, c.kgrid);
         float best = 1e30f;
         for (int rep = 0; rep < 5; ++rep) {
             cudaEventRecord(e0);
-            k_price_dmma<<<grid, kLThreads, sizeof(SmemD) + 1024>>>(tmWs, tmA, K, m, out);
+            if (pad) k_price_dmma<true><<<grid, kLThreads, sizeof(SmemD) + 1024>>>(tmWs, tmA1, K, m, out);
+            else k_price_dmma<false><<<grid, kLThreads, sizeof(SmemD) + 1024>>>(tmWs, tmA, K, m, out);
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             float ms;
@@ -425,7 +442,7 @@ int main() {
             if (ms < best) best = ms;
         }
         const double fl = 2.0 * m * (double)grid.x * kLN * grid.y * kLK;
-        printf("%-13s %-30s %.3f ms  %.2f TFLOP/s = %.3f of 37.1 (DMMA)\n", "DMMA", c.name, best,
+        printf("%-13s %-30s %.3f ms  %.2f TFLOP/s = %.3f of 37.1 (DMMA)\n", pad ? "DMMA swzB" : "DMMA", c.name, best,
                fl / (best * 1e-3) / 1e12, fl / (best * 1e-3) / 37.1e12);
     }
     printf("%s\n", cudaGetErrorString(cudaGetLastError()));
