@@ -8,7 +8,10 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
-constexpr int kLK = 64, kLN = 128, kLC = 16, kLS = 3, kLThreads = 256;
+#ifndef XLS
+#define XLS 3
+#endif
+constexpr int kLK = 64, kLN = 128, kLC = 16, kLS = XLS, kLThreads = 256;
 
 __device__ __forceinline__ unsigned su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ double xmul(double a, double b) { return __dmul_rn(a, b); }
