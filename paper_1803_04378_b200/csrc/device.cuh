@@ -177,6 +177,7 @@ struct Dev {
     const CUtensorMap* tm_nb;  // 2D TMA descriptors of A_nb, box {wbx slots, price_rows(wbx) rows}
     int price_nwc, price_S, price_smem, price_threads;
     int price_spt;             // slots per consumer thread: 1 (one chain per lane) or 2 (pairs)
+    int price_pf;              // A_nb stages k_price prefetches into L2 before its PDL wait
     int dbg;               // perf-experiment knobs (cfg.reserved[2] minus bit 4); read only
                            // through LPSG_XP, i.e. only in a -DLPSG_EXPERIMENTS build
     int la_exact;          // lookahead theta' keeps the y_i == 0 select (cfg.reserved[2] bit 4):

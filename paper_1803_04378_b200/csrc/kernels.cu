@@ -265,6 +265,11 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         "l"(map), "r"(x), "r"(y), "r"(su32(b))
         : "memory");
 }
+// L2 prefetch of a tensor box (no shared memory, no completion to wait for)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int x, int y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(x), "r"(y)
+                 : "memory");
+}
 // Streaming variants with an L2 eviction-priority hint: A_nb and T are read
 // (and T written) once per pivot and exceed L2, so their lines should not
 // displace anything worth keeping.
@@ -355,6 +360,20 @@ constexpr int kFG = 8;
 // ranges). The grid-wide (max z, min j) reduction is finished by the last CTA.
 __global__ void __launch_bounds__(384) k_price(Dev d) {
     extern __shared__ __align__(1024) unsigned char smem[];
+    // Under PDL this CTA is resident while k_pivot still runs (~10 us in which
+    // HBM idles): warm L2 with the first stages of its A_nb strip. A prefetch
+    // is only a hint and L2 is coherent with k_pivot's slot rewrite, so the
+    // (possibly not yet final) n_scan read here can at worst waste bandwidth.
+    if (threadIdx.x == 0 && d.price_pf > 0) {
+        const int ns0 = *reinterpret_cast<volatile const int*>(&d.ctl->n_scan);
+        const PriceGeom g0 = price_geom(ns0, gridDim.x, blockIdx.x);
+        if (g0.own > 0 && g0.s0 < ns0) {
+            const CUtensorMap* map = d.tm_nb + (g0.wbx / 8 - 1);
+            const int nst = min(d.price_pf, (d.m + g0.R - 1) / g0.R);
+            for (int k = 0; k < nst; ++k)
+                for (int q = 0; q < g0.nb; ++q) tma_prefetch_2d(map, g0.s0 + q * g0.wbx, k * g0.R);
+        }
+    }
     pdl_wait();
     Ctl* c = d.ctl;
     if (c->status != ST_RUNNING) return;

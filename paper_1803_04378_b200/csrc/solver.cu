@@ -541,6 +541,7 @@ void Solver::init(const lpsg_problem& lp) {
     plan_tiles(m, n);
     d_.pdl = (!comm_ && !tiled_ && m <= 12000 && xp_env("LPSG_NO_PDL") == nullptr) ? 1 : 0;
     d_.upd_tma_store = xp_env("LPSG_UPD_STG") == nullptr ? 1 : 0;
+    d_.price_pf = xp_env("LPSG_PRICE_PF") ? atoi(xp_env("LPSG_PRICE_PF")) : 8;
     d_.l2_hint = xp_env("LPSG_NO_L2_HINT") == nullptr ? 1 : 0;
     configure_kernels(d_);
     CK(cudaGetLastError());
