@@ -151,6 +151,32 @@ def test_seeded_parity_with_port(port, rows, cols, form, seed):
     assert np.array_equal(_bits(rep.x), _bits(ref.x))
 
 
+@pytest.mark.parametrize("mode", ["always", "auto", "off"])
+def test_duplicate_columns_exact_ties_with_port(port, mode):
+    """Degenerate LPs whose structural columns are duplicated: every reduced
+    cost, in pricing and in each lookahead's pricing, ties exactly with its
+    twin, so the bounded pricing's candidate lists carry exact ties that only
+    the (max z, min j) rule on exact values resolves. Pivots, x and objective
+    must equal the reference port's, bit for bit, in every lookahead_bound mode."""
+    from oracle.oracle import LP, make_config
+    P = _P()
+    for rows, cols, seed in ((60, 90, 3), (150, 240, 22)):
+        base = P.generate(P.GenSpec(rows, cols, seed=seed, form=P.Form.degenerate))
+        ck = np.asarray(base.col_kind)
+        ns = int(np.sum(ck == 0))
+        assert np.all(ck[:ns] == 0)
+        dup = np.arange(0, ns, 3)
+        A = np.hstack([base.A[:, :ns], base.A[:, dup], base.A[:, ns:]])
+        c = np.concatenate([base.c[:ns], base.c[dup], base.c[ns:]])
+        kind = np.concatenate([ck[:ns], ck[dup], ck[ns:]]).astype(np.uint8)
+        lp = P.StandardFormLP(rows, A.shape[1], np.ascontiguousarray(A), np.asarray(base.b, float), c, kind)
+        ref = port.solve(LP(lp.m, lp.n_total, lp.A, lp.b, lp.c, lp.col_kind), make_config())
+        rep, tr = _solve_traced(lp, lookahead_bound=mode)
+        assert int(rep.status) == ref.status, (rows, mode)
+        _assert_trace(tr, ref.trace, (rows, mode))
+        assert np.array_equal(_bits(rep.x), _bits(ref.x)), (rows, mode)
+
+
 def test_sparse_classes_parity(port):
     from oracle.oracle import LP, make_config
     P = _P()
