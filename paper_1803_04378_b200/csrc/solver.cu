@@ -26,6 +26,7 @@
 #include <string>
 #include <unordered_map>
 #include <thread>
+#include <type_traits>
 #include <unordered_set>
 #include <vector>
 
@@ -168,7 +169,8 @@ public:
     long long la_probe_rounds_ = 0;  // bounded selections that needed the exact probe rounds
     int la_bound_min_ = 16;                   // survivors from which the probe / bounded pricing are used
     double* anorm_ = nullptr;                 // ||a_j||_2 of A's columns (bounded pricing), made on first use
-    void free_la(LookaheadDev& la, int* rows_d);
+    unsigned char* la_arena_ = nullptr;       // lookahead buffers, kept across ties (pool memory)
+    size_t la_arena_bytes_ = 0;
     void step_pivot(int r, int q);
     void read_row(int i, double* out);
 
@@ -692,6 +694,7 @@ void Solver::init(const lpsg_problem& lp) {
 Solver::~Solver() { release(); }
 
 void Solver::release() {
+    if (la_arena_ && st_) cudaFreeAsync(la_arena_, st_);
     if (st_) cudaStreamSynchronize(st_);
     if (sharded_ && d_.xbuf) {
         comm_->sym_free(d_.xbuf);
@@ -711,6 +714,8 @@ void Solver::release() {
     part_row0_ = nullptr;
     xbuf_own_ = nullptr;
     anorm_ = nullptr;
+    la_arena_ = nullptr;
+    la_arena_bytes_ = 0;
     if (hctl_) cudaFreeHost(hctl_);
     if (hlog_) cudaFreeHost(hlog_);
     if (hone_) cudaFreeHost(hone_);
@@ -1176,24 +1181,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
     la.q = entering;
     la.nblk = (hctl_->n_scan + 127) / 128 + 1;  // 128-slot tiles + the leaving column
     la.nblk_t = std::max(1, (d_.mloc + 63) / 64);  // 64-row theta tiles
-    int* rows_d = talloc<int>(kb, st_, pool_);
-    la.rows = rows_d;
-    la.X = talloc<double>((size_t)kb * ldx, st_, pool_);
-    la.Wp = talloc<double>((size_t)kb * ldx, st_, pool_);
-    la.bz = talloc<double>(kb, st_, pool_);
-    la.bj = talloc<int>(kb, st_, pool_);
-    la.theta = talloc<double>(kb, st_, pool_);
-    la.score = talloc<double>(kb, st_, pool_);
-    la.part_z = talloc<double>((size_t)kb * la.nblk, st_, pool_);
-    la.part_j = talloc<int>((size_t)kb * la.nblk, st_, pool_);
-    la.part_t = talloc<double>((size_t)kb * la.nblk_t, st_, pool_);
-    la.pm = talloc<PriceMsg>((size_t)kb, st_, pool_);
-    la.pm_all = sharded_ ? talloc<PriceMsg>((size_t)kb * G, st_, pool_) : nullptr;
-    la.tl = talloc<double>(kb, st_, pool_);
-    la.own_t = talloc<double>(kb, st_, pool_);
     const int P = tiled_ ? (int)parts_.size() : 1;
-    la.tl_all = sharded_ ? talloc<double>((size_t)kb * G, st_, pool_)
-                         : tiled_ ? talloc<double>((size_t)kb * P, st_, pool_) : nullptr;
     la.x_owned_only = tiled_ ? 1 : 0;
     std::vector<int> porder;  // Case 2: the resident partition first, then the others
     if (tiled_) {
@@ -1201,29 +1189,82 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
         for (int p = 0; p < P; ++p)
             if (p != resident_) porder.push_back(p);
     }
-    la.nonfinite = talloc<int>(1, st_, pool_);
-    // bounded pricing (kernels.cu k_la_gemm_price<true>, k_la_cands, k_la_exact):
-    // from la_bound_min_ candidates up, the exact argmax without the exact GEMM
+    // bounded pricing (kernels.cu k_la_screen, k_la_cands, k_la_exact): from
+    // la_bound_min_ candidates up, the exact argmax without the exact GEMM
     const bool bounded = kb >= la_bound_min_;
-    if (bounded) {
-        if (!anorm_) {
-            anorm_ = dalloc<double>(n_total_);
-            launch_colnorm(d_, anorm_, st_);
-        }
-        la.anorm = anorm_;
-        const size_t nt = (size_t)kb * std::max(1, la.nblk - 1);
-        la.wnorm = talloc<double>(kb, st_, pool_);
-        la.tl_s = talloc<int>(nt * kLaTile, st_, pool_);
-        la.tl_z = talloc<double>(nt * kLaTile, st_, pool_);
-        la.tl_n = talloc<int>(nt, st_, pool_);
-        la.part_L = talloc<double>((size_t)kb * la.nblk, st_, pool_);
-        la.cj = talloc<int>((size_t)kb * kLaCand, st_, pool_);
-        la.cz = talloc<double>((size_t)kb * kLaCand, st_, pool_);
-        la.cn = talloc<int>(kb, st_, pool_);
-        la.pairs = talloc<int>(kLaPairs, st_, pool_);
-        la.npairs = talloc<int>(1, st_, pool_);
-        la.fail = talloc<int>(1, st_, pool_);
+    // bounded selection (kernels.cu, k_la_probe*): one GPU, in-core, one batch
+    const bool probe = first_proven && !sharded_ && !tiled_ && kb == K && K >= la_bound_min_;
+    if (bounded && !anorm_) {
+        anorm_ = dalloc<double>(n_total_);
+        launch_colnorm(d_, anorm_, st_);
     }
+    la.anorm = anorm_;
+    // Every buffer of this lookahead is carved from one arena that persists
+    // across lookaheads (grown when a larger tie needs it): a tie costs no
+    // allocator calls (30-odd stream-ordered allocations and frees before).
+    const size_t nt = (size_t)kb * std::max(1, la.nblk - 1);
+    int* rows_d = nullptr;
+    auto carve = [&](unsigned char* base) -> size_t {
+        size_t off = 0;
+        auto take = [&](auto*& ptr, size_t n) {
+            using T = std::remove_pointer_t<std::remove_reference_t<decltype(ptr)>>;
+            ptr = base ? reinterpret_cast<T*>(base + off) : nullptr;
+            off += (std::max<size_t>(n, 1) * sizeof(T) + 255) & ~size_t(255);
+        };
+        take(rows_d, kb);
+        take(la.X, (size_t)kb * ldx);
+        take(la.Wp, (size_t)kb * ldx);
+        take(la.bz, kb);
+        take(la.bj, kb);
+        take(la.theta, kb);
+        take(la.score, kb);
+        take(la.part_z, (size_t)kb * la.nblk);
+        take(la.part_j, (size_t)kb * la.nblk);
+        take(la.part_t, (size_t)kb * la.nblk_t);
+        take(la.pm, kb);
+        if (sharded_) take(la.pm_all, (size_t)kb * G);
+        take(la.tl, kb);
+        take(la.own_t, kb);
+        if (sharded_) take(la.tl_all, (size_t)kb * G);
+        else if (tiled_) take(la.tl_all, (size_t)kb * P);
+        take(la.nonfinite, 1);
+        if (bounded) {
+            take(la.wnorm, kb);
+            take(la.tl_s, nt * kLaTile);
+            take(la.tl_z, nt * kLaTile);
+            take(la.tl_n, nt);
+            take(la.part_L, (size_t)kb * la.nblk);
+            take(la.cj, (size_t)kb * kLaCand);
+            take(la.cz, (size_t)kb * kLaCand);
+            take(la.cn, kb);
+            take(la.pairs, kLaPairs);
+            take(la.npairs, 1);
+            take(la.fail, 1);
+        }
+        if (probe) {
+            take(la.prow, kLaProbe);
+            take(la.nprow, 1);
+            take(la.Tg, (size_t)m * kLaProbe);
+            take(la.ok, K);
+            take(la.clist, K);
+            take(la.yacc, (size_t)K * 128);
+            take(la.pxb, K);
+            take(la.pxn, K);
+            take(la.pbn, K);
+            take(la.ptn, 128);
+            take(la.ncl, 1);
+            take(la.first, 1);
+        }
+        return off;
+    };
+    const size_t need = carve(nullptr);
+    if (need > la_arena_bytes_) {
+        if (la_arena_) CK(cudaFreeAsync(la_arena_, st_));
+        la_arena_bytes_ = need + need / 4;
+        la_arena_ = talloc<unsigned char>(la_arena_bytes_, st_, pool_);
+    }
+    carve(la_arena_);
+    la.rows = rows_d;
     CK(cudaMemsetAsync(la.X, 0, sizeof(double) * (size_t)kb * ldx, st_));
     if (dbg_trace_) fprintf(stderr, "[solver r%d] lookahead K=%d\n", rank_, K);
     temp_alloc_fence();
@@ -1252,19 +1293,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.pm, la.pm_all, sizeof(PriceMsg) * la.K, st_); });
         L(K_OTHER, 0.0, [&] { launch_la_decide(d_, la, sharded_ ? la.pm_all : la.pm, G, st_); });
         // bounded selection (kernels.cu, k_la_probe*): one GPU, in-core, one batch
-        if (first_proven && !sharded_ && !tiled_ && la.K == K && K >= la_bound_min_) {
-            la.prow = talloc<int>(kLaProbe, st_, pool_);
-            la.nprow = talloc<int>(1, st_, pool_);
-            la.Tg = talloc<double>((size_t)m * kLaProbe, st_, pool_);
-            la.ok = talloc<int>(K, st_, pool_);
-            la.clist = talloc<int>(K, st_, pool_);
-            la.yacc = talloc<double>((size_t)K * 128, st_, pool_);
-            la.pxb = talloc<double>(K, st_, pool_);
-            la.pxn = talloc<double>(K, st_, pool_);
-            la.pbn = talloc<double>(K, st_, pool_);
-            la.ptn = talloc<double>(128, st_, pool_);
-            la.ncl = talloc<int>(1, st_, pool_);
-            la.first = talloc<int>(1, st_, pool_);
+        if (probe) {
             L(K_LA_THETA, 2.0 * kf * kLaProbeRound, [&] { la_ok(launch_la_probe(d_, la, st_)); });
             CK(cudaGetLastError());
             int first = 0, ncl = 0;
@@ -1301,12 +1330,9 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
                         rank_, K, first == 1 ? 0 : (-first - 1) / 2,
                         first != 1 && ((-first - 1) & 1) ? "not provably 0" : "ok", distinct, np);
             }
-            void* pb[] = {la.prow, la.nprow, la.Tg, la.ok, la.clist, la.ncl, la.first, la.yacc, la.pxb, la.pxn, la.pbn, la.ptn};
-            for (void* p : pb) CK(cudaFreeAsync(p, st_));
             if (first == 1) {
                 ++la_bounded_;
                 *first_proven = true;
-                free_la(la, rows_d);
                 return;
             }
             ++la_full_;
@@ -1337,15 +1363,6 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
         CK(cudaStreamSynchronize(st_));
         if (bounded) ++(pfail ? la_price_exact_ : la_price_bounded_);
     }
-    free_la(la, rows_d);
-}
-
-void Solver::free_la(LookaheadDev& la, int* rows_d) {
-    void* bufs[] = {rows_d, la.X, la.Wp, la.bz, la.bj, la.theta, la.score, la.part_z, la.part_j, la.part_t,
-                    la.pm, la.pm_all, la.tl, la.tl_all, la.own_t, la.nonfinite, la.wnorm, la.tl_s, la.tl_z, la.tl_n, la.part_L,
-                    la.cj, la.cz, la.cn, la.pairs, la.npairs, la.fail};
-    for (void* p : bufs)
-        if (p) CK(cudaFreeAsync(p, st_));
 }
 
 // One phase, through the reinversion mode when it is on: the device budget
