@@ -65,6 +65,25 @@ def test_sharded_golden_parity(name, shards):
     _check(rep, tr, g, (name, shards))
 
 
+TIE_NAMES = [n for n in NAMES if "_f2_" in n or n.startswith(("beale", "netlib"))]
+
+
+@pytest.mark.parametrize("shards", [2, 4])
+@pytest.mark.parametrize("name", TIE_NAMES)
+def test_sharded_bounded_pricing_always(name, shards):
+    """The bounded pricing (DMMA screen + exact chains) on
+    every tie of >= 2 candidates, per shard over its own columns, merged by the
+    exact (max z, min j) exchange: the same pivots as the reference, bit for bit."""
+    P = _P()
+    g = Golden(name)
+    if shards > g.m:
+        pytest.skip("fewer rows than shards")
+    cfg = P.SolverConfig(max_iter=g.max_iter, pivot_tol=g.pivot_tol, kernel=g.kernel,
+                         anticycle=P.Anticycle(g.anticycle), lookahead_bound="always")
+    rep, tr = P.solve_sharded(_golden_lp(g), cfg, shards=shards, trace=True)
+    _check(rep, tr, g, (name, shards, "always"))
+
+
 P2P_NAMES = ["gen_256x512_f2_s1", "gen_256x512_f0_s1", "gen_1000x2000_f0_s1_max_iter400",
              "gen_2000x4000_f0_s1_max_iter200", "netlib_scsd1", "netlib_sctap1", "netlib_boeing2",
              "beale_3x7", "infeasible_2x2", "unbounded_1x3", "gen_128x256_f2_s5_anticyclenone"]
