@@ -89,6 +89,20 @@ def test_tiled_reproduces_golden(name, parts):
     assert mem["h2d_bytes"] > 8 * g.m * g.m and mem["d2h_bytes"] > 8 * g.m * g.m
 
 
+@pytest.mark.parametrize("name", ["gen_128x256_f2_s5", "gen_256x512_f2_s1", "beale_3x7", "netlib_scsd1",
+                                  "netlib_sctap1"])
+def test_tiled_bounded_pricing_always(name):
+    """Case 2 with the bounded pricing on every tie (the
+    bounded selection itself is in-core only, so ties fall back to full
+    scoring per partition): still the reference's traces, bit for bit."""
+    g = Golden(name)
+    if g.m + 1 < 6:
+        pytest.skip("too few rows for 3 partitions")
+    rep, tr, _ = _run(g, budget_for(g.m, 3), lookahead_bound="always")
+    assert rep.case_used == "Tiled", name
+    _check(rep, tr, g, (name, "always"))
+
+
 def test_in_core_when_the_budget_fits():
     P = _P()
     g = Golden("gen_64x128_f0_s2")
