@@ -578,6 +578,17 @@ def run_ours(args, cfg):
     }
     if exchange:
         line["exchange"] = exchange
+    if (la_stats["bounded"] or la_stats["price_bounded"]) and world == 1:
+        # transparency: the same window with the bounded lookahead off (every
+        # tie scored by both exact GEMMs), the decisions being identical
+        s2 = P.SimplexSolver(lp, solver_config(P, args, world, rank, local, max_iter=W,
+                                               lookahead_bound="off"))
+        s2.solve()
+        s2.set_max_iter(W + K)
+        rep2 = s2.solve()
+        d2 = s2.device_ms()
+        s2.close()
+        la_stats["full_scoring_it_s"] = (rep2.iterations - W) / (d2 / 1e3) if d2 > 0 else None
     if any(la_stats.values()):
         line["lookahead"] = dict(la_stats, note=(
             "lookaheads of >= 16 candidates over the timed + profiled windows. bounded / full: "
@@ -586,7 +597,9 @@ def run_ours(args, cfg):
             "price_bounded / price_exact: pricings settled by the DMMA screen with rigorous "
             "error bounds + exact chains for the columns it cannot exclude vs the exact GEMM "
             "rerun. probe_rounds: selections whose DMMA probe screen left candidates for the "
-            "exact probe rounds. Decisions are the reference's either way (DESIGN.md §4)"))
+            "exact probe rounds. full_scoring_it_s: the same window with lookahead_bound='off' "
+            "(every tie scored by both exact GEMMs). Decisions are the reference's either way "
+            "(DESIGN.md §4.1)"))
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         kc = min(K, cfg["cpu_pivots"])
