@@ -322,7 +322,6 @@ void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int 
 bool launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st);
 // select_leaving's bounded path (unsharded, in-core): la.first = 1 when the
 // first candidate provably wins ("bounded selection")
-void launch_la_probe_prep(const Dev& d, LookaheadDev& la, cudaStream_t st);  // probe rows + gathered T (prefix)
 bool launch_la_probe(const Dev& d, LookaheadDev& la, cudaStream_t st);
 void launch_la_probe_rounds(const Dev& d, LookaheadDev& la, cudaStream_t st);  // when la.ncl > 0
 void launch_la_score(const Dev& d, LookaheadDev& la, const double* tl, int nsrc, cudaStream_t st);

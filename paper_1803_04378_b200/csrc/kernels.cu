@@ -2935,16 +2935,10 @@ bool launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     return true;
 }
 
-// The probe rows and their gathered T columns depend only on the tableau, not
-// on the lookahead's pricing: the solver issues them on its side stream while
-// the pricing screen runs.
-void launch_la_probe_prep(const Dev& d, LookaheadDev& la, cudaStream_t st) {
-    k_la_probe_rows<<<1, 1024, 0, st>>>(d, la);
-    k_la_probe_gather<<<4 * 148, 256, 0, st>>>(d, la);
-}
-
 bool launch_la_probe(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     cudaMemsetAsync(la.ok, 0, sizeof(int) * la.K, st);
+    k_la_probe_rows<<<1, 1024, 0, st>>>(d, la);
+    k_la_probe_gather<<<4 * 148, 256, 0, st>>>(d, la);
     // DMMA screen of the first kLN probe rows for every candidate (split along
     // the reduction to fill the GPU), then certificates from its error bound;
     // the exact rounds below only see the candidates it leaves unproven

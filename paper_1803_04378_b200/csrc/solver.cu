@@ -171,7 +171,7 @@ public:
     double* anorm_ = nullptr;                 // ||a_j||_2 of A's columns (bounded pricing), made on first use
     unsigned char* la_arena_ = nullptr;       // lookahead buffers, kept across ties (pool memory)
     cudaStream_t la_side_ = nullptr;          // the leaving-column dots run here, under the screen
-    cudaEvent_t la_ev_[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t la_ev_[2] = {nullptr, nullptr};
     size_t la_arena_bytes_ = 0;
     void step_pivot(int r, int q);
     void read_row(int i, double* out);
@@ -1298,16 +1298,8 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->sum_i64(reinterpret_cast<long long*>(la.X), (size_t)la.K * ldx, st_); });
         if (bounded && !la_side_ && xp_env("LPSG_LA_NO_SIDE") == nullptr) {
             CK(cudaStreamCreateWithFlags(&la_side_, cudaStreamNonBlocking));
-            for (cudaEvent_t& e : la_ev_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        }
-        // the bounded selection's probe rows and gathered T columns: on the side
-        // stream, under the pricing (the tableau does not change during a lookahead)
-        const bool prep_side = probe && la_side_;
-        if (prep_side) {
-            CK(cudaEventRecord(la_ev_[2], st_));
-            CK(cudaStreamWaitEvent(la_side_, la_ev_[2], 0));
-            launch_la_probe_prep(d_, la, la_side_);
-            CK(cudaEventRecord(la_ev_[3], la_side_));
+            CK(cudaEventCreateWithFlags(&la_ev_[0], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&la_ev_[1], cudaEventDisableTiming));
         }
         L(K_LA_PRICE, kf * (double)hctl_->n_scan,
           [&] { la_ok(launch_la_price(d_, la, bounded, st_, la_side_, la_ev_[0], la_ev_[1])); });
@@ -1315,8 +1307,6 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
         L(K_OTHER, 0.0, [&] { launch_la_decide(d_, la, sharded_ ? la.pm_all : la.pm, G, st_); });
         // bounded selection (kernels.cu, k_la_probe*): one GPU, in-core, one batch
         if (probe) {
-            if (prep_side) CK(cudaStreamWaitEvent(st_, la_ev_[3], 0));
-            else launch_la_probe_prep(d_, la, st_);
             L(K_LA_THETA, 2.0 * kf * kLaProbeRound, [&] { la_ok(launch_la_probe(d_, la, st_)); });
             CK(cudaGetLastError());
             int first = 0, ncl = 0;
