@@ -315,8 +315,7 @@ double fp64_probe_tflops(cudaStream_t st);  // k_fp64_probe, best of 5
 void launch_la_x(const Dev& d, LookaheadDev& la, cudaStream_t st);
 // false: TMA descriptor encode failed. bounded: the DFMA screen + exact chains
 // (la.anorm ... la.fail set); else the exact GEMM over every slot.
-bool launch_la_price(const Dev& d, LookaheadDev& la, bool bounded, cudaStream_t st, cudaStream_t side = nullptr,
-                     cudaEvent_t ev_w = nullptr, cudaEvent_t ev_leave = nullptr);
+bool launch_la_price(const Dev& d, LookaheadDev& la, bool bounded, cudaStream_t st);
 void launch_colnorm(const Dev& d, double* out, cudaStream_t st);  // ||a_j||_2, j < n_total
 void launch_la_decide(const Dev& d, LookaheadDev& la, const PriceMsg* msgs, int nsrc, cudaStream_t st);
 bool launch_la_theta(const Dev& d, LookaheadDev& la, cudaStream_t st);

@@ -2870,8 +2870,7 @@ void launch_la_x(const Dev& d, LookaheadDev& la, cudaStream_t st) {
     k_la_x<<<dim3((d.m + 1 + 255) / 256, la.K), 256, 0, st>>>(d, la);
 }
 
-bool launch_la_price(const Dev& d, LookaheadDev& la, bool bounded, cudaStream_t st, cudaStream_t side,
-                     cudaEvent_t ev_w, cudaEvent_t ev_leave) {
+bool launch_la_price(const Dev& d, LookaheadDev& la, bool bounded, cudaStream_t st) {
     k_la_wp<<<dim3((d.m + 255) / 256, la.K), 256, 0, st>>>(d, la);
     // la.nblk = slot tiles + 1 (the last partial holds the leaving column)
     CUtensorMap tmW, tmA;
@@ -2889,17 +2888,8 @@ bool launch_la_price(const Dev& d, LookaheadDev& la, bool bounded, cudaStream_t 
             (!encode_2d(&tmWs, la.Wp, (uint64_t)d.m, (uint64_t)la.K, (uint64_t)la.ldx * 8, kLC, kLK, true) ||
              !encode_2d(&tmAs, d.A_nb, (uint64_t)d.ld_nb, (uint64_t)d.m, (uint64_t)d.ld_nb * 8, 16, kLC, true)))
             return false;
-        // the leaving-column dots (latency-bound chains on ~K/16 CTAs) run on a
-        // side stream under the screen, which does not need them
-        if (side) {
-            cudaEventRecord(ev_w, st);
-            cudaStreamWaitEvent(side, ev_w, 0);
-            k_la_leave<<<(la.K + kDC - 1) / kDC, kDT, 0, side>>>(d, la);
-            cudaEventRecord(ev_leave, side);
-        }
         if (la.nblk > 1) k_la_screen<false><<<grid, kLThreads, sizeof(LaScreenSmem) + 1024, st>>>(d, la, tmWs, tmAs);
-        if (side) cudaStreamWaitEvent(st, ev_leave, 0);
-        else k_la_leave<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
+        k_la_leave<<<(la.K + kDC - 1) / kDC, kDT, 0, st>>>(d, la);
         k_la_cands<<<la.K, 256, 0, st>>>(d, la);
         k_la_exact<<<kLaPairs / kDC, kDT, 0, st>>>(d, la);
         k_la_cands_best<<<(la.K + 127) / 128, 128, 0, st>>>(d, la);

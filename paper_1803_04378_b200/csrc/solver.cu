@@ -170,8 +170,6 @@ public:
     int la_bound_min_ = 16;                   // survivors from which the probe / bounded pricing are used
     double* anorm_ = nullptr;                 // ||a_j||_2 of A's columns (bounded pricing), made on first use
     unsigned char* la_arena_ = nullptr;       // lookahead buffers, kept across ties (pool memory)
-    cudaStream_t la_side_ = nullptr;          // the leaving-column dots run here, under the screen
-    cudaEvent_t la_ev_[2] = {nullptr, nullptr};
     size_t la_arena_bytes_ = 0;
     void step_pivot(int r, int q);
     void read_row(int i, double* out);
@@ -727,11 +725,6 @@ void Solver::release() {
         cudaEventDestroy(r.a);
         cudaEventDestroy(r.b);
     }
-    if (la_side_) cudaStreamSynchronize(la_side_);
-    if (la_side_) cudaStreamDestroy(la_side_);
-    for (cudaEvent_t& e : la_ev_)
-        if (e) cudaEventDestroy(e), e = nullptr;
-    la_side_ = nullptr;
     if (pool_) cudaMemPoolDestroy(pool_);
     if (st_) cudaStreamDestroy(st_);
     d_ = Dev{};
@@ -1296,13 +1289,7 @@ void Solver::lookahead(const std::vector<int>& rows, int entering, std::vector<d
             L(K_OTHER, 0.0, [&] { launch_la_x(d_, la, st_); });
         }
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->sum_i64(reinterpret_cast<long long*>(la.X), (size_t)la.K * ldx, st_); });
-        if (bounded && !la_side_ && xp_env("LPSG_LA_NO_SIDE") == nullptr) {
-            CK(cudaStreamCreateWithFlags(&la_side_, cudaStreamNonBlocking));
-            CK(cudaEventCreateWithFlags(&la_ev_[0], cudaEventDisableTiming));
-            CK(cudaEventCreateWithFlags(&la_ev_[1], cudaEventDisableTiming));
-        }
-        L(K_LA_PRICE, kf * (double)hctl_->n_scan,
-          [&] { la_ok(launch_la_price(d_, la, bounded, st_, la_side_, la_ev_[0], la_ev_[1])); });
+        L(K_LA_PRICE, kf * (double)hctl_->n_scan, [&] { la_ok(launch_la_price(d_, la, bounded, st_)); });
         if (sharded_) L(K_COMM, 0.0, [&] { comm_->allgather(la.pm, la.pm_all, sizeof(PriceMsg) * la.K, st_); });
         L(K_OTHER, 0.0, [&] { launch_la_decide(d_, la, sharded_ ? la.pm_all : la.pm, G, st_); });
         // bounded selection (kernels.cu, k_la_probe*): one GPU, in-core, one batch
